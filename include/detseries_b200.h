@@ -1,0 +1,167 @@
+/*
+ * detseries_b200.h -- C ABI of the B200 (sm_100a) hot path of arXiv:1308.1536:
+ * arbitrary-precision, unpivoted Gaussian elimination on [A | I] returning all
+ * leading principal minors (running product of pivots) and, for every leading
+ * size m = 2..n, the signed and normalized minors of column m.
+ *
+ * The ABI is plain C: pointers, sizes and integer codes, no torch/CUDA types.
+ * Each entry point names the reference interface it replaces (paths are
+ * relative to the reference package root pkg/src/detseries/).
+ *
+ * ---------------------------------------------------------------------------
+ * Scalar format ("ds SoA").  Precision p bits, L = ceil(p/32) limbs.
+ * A real scalar x != 0 is  x = (-1)^s * M * 2^(e - 32L),  M an integer with
+ * 2^(32L-1) <= M < 2^(32L) whose low 32L-p bits are zero (the MPFR
+ * convention 0.5 <= |x| / 2^e < 1, scalars.py:129-145 canonical form).
+ * M is stored as L little-endian 32-bit limbs (limb L-1 holds the MSB).
+ * cls holds the sign class, with the same codes as the reference wire
+ * format's sign byte (parexec.py:36): 0 = positive, 1 = negative, 2 = +0,
+ * 3 = -0.  Zeros have all limbs 0 and e = 0.
+ *
+ * An array of `count` scalars is structure-of-arrays, limb-plane major:
+ *     limbs[(c*L + l)*count + idx],  exp[c*count + idx],  cls[c*count + idx]
+ * where c is the component (0 = real part; complex scalars have c = 1 for
+ * the imaginary part).  A matrix is count = n*n with idx = row*n + col.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef DETSERIES_B200_H
+#define DETSERIES_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes (mapped to detseries.errors by the Python layer) */
+#define DS_OK 0
+#define DS_ZERO_PIVOT 1          /* errors.ZeroPivot          (errors.py:16-28) */
+#define DS_PRECISION_MISMATCH 2  /* errors.PrecisionMismatch  (errors.py:12-13) */
+#define DS_INVALID 3             /* ValueError                                   */
+#define DS_CUDA 4                /* errors.WorkerFailure      (errors.py:55-60) */
+#define DS_NCCL 5                /* errors.WorkerFailure                         */
+#define DS_OOM 6                 /* MemoryError                                  */
+#define DS_OVERFLOW 7            /* exponent left MPFR's default range           */
+
+#define DS_KIND_REAL 0
+#define DS_KIND_COMPLEX 1
+
+#define DS_CLS_POS 0
+#define DS_CLS_NEG 1
+#define DS_CLS_PZERO 2
+#define DS_CLS_NZERO 3
+
+/* MPFR default exponent range (emin/emax = -/+ (2^30 - 1)) */
+#define DS_EMAX 1073741823
+#define DS_EMIN (-1073741823)
+
+typedef struct ds_soa {
+  uint32_t *limbs; /* [ncomp][L][count] */
+  int32_t *exp;    /* [ncomp][count]    */
+  uint8_t *cls;    /* [ncomp][count]    */
+  int64_t count;
+} ds_soa;
+
+/* Result buffers of one elimination run (host memory, caller-owned).
+ *   pivots, dets : count >= n   (trace.pivots / trace.det_series,
+ *                                elim.py:64-89)
+ *   signed_minors, normalized : count >= n*n; the minors of leading size m
+ *                                live in row m-1, columns 0..m-1
+ *                                (MinorRow.signed / .normalized,
+ *                                elim.py:92-99)
+ *   row_flags[m-1] : bit0 = row m emitted, bit1 = normalized defined
+ *                    (normalized is None when signed[0] == 0, elim.py:151-155)
+ * Any pointer may be NULL to skip that output. */
+typedef struct ds_results {
+  ds_soa pivots;
+  ds_soa dets;
+  ds_soa signed_minors;
+  ds_soa normalized;
+  uint8_t *row_flags;
+} ds_results;
+
+typedef struct ds_ctx ds_ctx;
+
+/* Library version string. */
+const char *ds_version(void);
+
+/* Create a context for an n x n elimination at `prec_bits` (>= 64,
+ * scalars.py:37-54) of `kind` on CUDA `device`.  The matrix is sharded
+ * row-cyclically over `world` ranks and this context holds the rows r with
+ * r % world == rank (parexec.py:39-55, WorkerTopology.owner); world = 1 is
+ * the serial engine (elim.eliminate, elim.py:158).  Replaces the allocation
+ * of MatrixBuffer (matrix.py:24-51) on the device. */
+int ds_create(ds_ctx **out, int n, long prec_bits, int kind, int device, int rank,
+              int world);
+void ds_destroy(ds_ctx *ctx);
+
+/* Copy the rows this rank owns from a full host matrix (count = n*n) into
+ * HBM.  Replaces the initial row scatter of parexec.py:367-368. */
+int ds_load(ds_ctx *ctx, const ds_soa *host_matrix);
+
+/* Copy the rows this rank owns back into a full host matrix (count = n*n):
+ * the in-place L\U state (elim.py:19-22; parexec.py:395-398). */
+int ds_fetch(ds_ctx *ctx, ds_soa *host_matrix);
+
+/* Serial engine (world == 1): run pivot steps [start_step, stop_step) of
+ * elim.eliminate (elim.py:203-228) entirely on the device, then copy the
+ * trace and minors into `res`.  For a resumed run (start_step > 0) res->dets
+ * must hold det_series[start_step-1] (elim.py:201).  On an exact zero pivot
+ * returns DS_ZERO_PIVOT with *steps_done = the 0-based failing step
+ * (ZeroPivot.step - 1, elim.py:209-212) and the partial results copied. */
+int ds_run(ds_ctx *ctx, int collect_minors, int series, int start_step, int stop_step,
+           ds_results *res, int *steps_done);
+
+/* --- sharded engine building blocks (world > 1; the caller broadcasts) ---
+ * Per step i: the owner of row i calls ds_pivot_stage (copies the
+ * unnormalized row i into the pivot buffer: parexec.py:307-309), every rank
+ * broadcasts the pivot buffer from that owner (ncclBroadcast through
+ * torch.distributed), then every rank calls ds_step (det chain, update of
+ * its own rows, minor emission for the row it owns: parexec.py:312-325). */
+int ds_pivot_buffer(ds_ctx *ctx, void **device_ptr, size_t *bytes);
+int ds_pivot_stage(ds_ctx *ctx, int step);
+int ds_step(ds_ctx *ctx, int step, int collect_minors, int series);
+/* Status of the device abort flag: *failed_step = -1 when no zero pivot was
+ * seen, else the 0-based step.  Synchronises the context stream. */
+int ds_status(ds_ctx *ctx, int *failed_step);
+/* Copy trace (replicated on every rank) and the minors rows this rank owns
+ * (row m-1 owned when (m-1) % world == rank) into `res`. */
+int ds_results_fetch(ds_ctx *ctx, int upto_step, ds_results *res);
+/* Seed the device det chain (resume, elim.py:201): det = host scalar. */
+int ds_set_det(ds_ctx *ctx, const ds_soa *det1);
+
+/* CUDA stream the context launches on (cudaStream_t as void*). */
+void *ds_stream(ds_ctx *ctx);
+/* Launch on the caller's stream from now on (e.g. torch's current stream, so
+ * the NCCL broadcast of the pivot buffer is stream-ordered with the kernels
+ * without host synchronisation).  NULL restores the context's own stream. */
+int ds_set_stream(ds_ctx *ctx, void *stream);
+/* Use caller-owned device memory of >= the ds_pivot_buffer size as the
+ * pivot buffer (e.g. a torch tensor that torch.distributed broadcasts in
+ * place).  NULL restores the internal buffer. */
+int ds_use_pivot_buffer(ds_ctx *ctx, void *device_ptr, size_t bytes);
+/* In-process broadcast for virtual shards (par_eliminate transport="local"):
+ * copy src's pivot buffer into dst's, ordered after src's pending work. */
+int ds_pivot_copy(ds_ctx *dst, ds_ctx *src);
+/* Number of kernel launches issued by this context since creation. */
+int64_t ds_launch_count(ds_ctx *ctx);
+
+/* Last error message of this context (or of the last failed ds_create when
+ * ctx is NULL). */
+const char *ds_last_error(ds_ctx *ctx);
+
+/* ---- correctly-rounded scalar kernels (conformance surface) ----
+ * Element-wise RN(a op b) over `count` real (kind 0) or complex (kind 1)
+ * scalars at precision prec_bits, computed on `device`.  op: 0 = mul,
+ * 1 = sub, 2 = div, 3 = add.  Host buffers.  These are the device routines
+ * k_update / k_mult / k_emit use; they stand in for mpfr_mul/sub/div and
+ * mpc_mul/sub/div. */
+int ds_scalar_op(int op, int kind, long prec_bits, int device, const ds_soa *a,
+                 const ds_soa *b, ds_soa *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DETSERIES_B200_H */

@@ -1,0 +1,841 @@
+// ds_engine.cu -- device engine and C ABI for the sm_100a hot path of
+// arXiv:1308.1536 (include/detseries_b200.h).
+//
+// Per pivot step i (elim.py:203-228; parexec.py:290-333 for the sharded form):
+//   k_pivot   : exact zero test of the pivot (elim.py:209-212), pivots[i],
+//               det chain det = piv | det*piv (elim.py:213-215)
+//   k_mult    : z_j = RN(a_ji / piv) for this rank's rows j > i, a_ji <- -z_j
+//               (elim.py:47, 53)
+//   k_update  : a_jk <- RN(a_jk - RN(z_j * b_k)) for k != i (elim.py:49-52);
+//               the real case runs the fused DFMA kernel of ds_update.cu
+//   k_emit    : signed minors RN(det * L_{m,k}) + det, normalized RN(s_k/s_0)
+//               for m = i+2 on the rank owning row i+1 (elim.py:56-61, 138-155)
+// Kernels early-exit once the device abort flag holds a failed step, so the
+// host never synchronises per step.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <string>
+
+#include "ds_mp.cuh"
+#include "ds_update.cuh"
+
+using namespace ds;
+
+#define DS_VERSION "detseries_b200 0.1 (sm_100a)"
+
+struct ds_ctx {
+  int n, L, p, kind, ncomp, device, rank, world, nloc;
+  cudaStream_t stream, own_stream;
+  cudaEvent_t ev;
+  // matrix rows owned by this rank: [ncomp][L][nloc*n] limbs
+  uint32_t* a_limbs;
+  int32_t* a_exp;
+  uint8_t* a_cls;
+  int64_t a_count;
+  // broadcast pivot buffer (same byte layout as the oracle's)
+  uint8_t* pbuf;       // active pivot buffer (own or caller-provided)
+  uint8_t* own_pbuf;
+  size_t pbuf_bytes;
+  // multipliers z_j for local rows: [ncomp][L][nloc]
+  uint32_t* z_limbs;
+  int32_t* z_exp;
+  uint8_t* z_cls;
+  // trace: pivots/dets [ncomp][L][n]; det running value [ncomp][L][1]
+  uint32_t *piv_limbs, *det_limbs, *cur_limbs;
+  int32_t *piv_exp, *det_exp, *cur_exp;
+  uint8_t *piv_cls, *det_cls, *cur_cls;
+  // minors for owned rows: [ncomp][L][nloc*n] (row m-1 local index (m-1)/world)
+  uint32_t *sig_limbs, *nrm_limbs;
+  int32_t *sig_exp, *nrm_exp;
+  uint8_t *sig_cls, *nrm_cls;
+  uint8_t* row_flags;  // [n]
+  // status: [0] failed step (-1), [1] have_det, [2] range error count, [3] warnings
+  int32_t* status;
+  // per-thread scratch for the general engine
+  uint32_t* scratch;
+  int64_t scratch_threads;
+  int64_t scratch_words;  // words per thread
+  // fused update engine workspace
+  UpdatePlan plan;
+  int64_t launches;
+  std::string err;
+};
+
+static std::string g_last_error;
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      if (ctx) ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);      \
+      g_last_error = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+      return DS_CUDA;                                                              \
+    }                                                                              \
+  } while (0)
+
+static inline int nlimbs(long p) { return (int)((p + 31) / 32); }
+
+static size_t pbuf_size(int n, int L, int ncomp) {
+  return (size_t)4 * ncomp * L * n + (size_t)4 * ncomp * n + (((size_t)ncomp * n + 3) & ~(size_t)3);
+}
+
+struct PB {  // pivot buffer view
+  uint32_t* limbs;
+  int32_t* exp;
+  uint8_t* cls;
+};
+__host__ __device__ static inline PB pb_view(uint8_t* p, int n, int L, int ncomp) {
+  PB v;
+  v.limbs = (uint32_t*)p;
+  v.exp = (int32_t*)(p + (size_t)4 * ncomp * L * n);
+  v.cls = (uint8_t*)(p + (size_t)4 * ncomp * L * n + (size_t)4 * ncomp * n);
+  return v;
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ Val val_at(const uint32_t* limbs, const int32_t* ex, const uint8_t* cl, int64_t count,
+                                      int c, int L, int64_t idx) {
+  Val v;
+  v.m = CPtr{limbs + (int64_t)c * L * count + idx, count};
+  v.e = ex[(int64_t)c * count + idx];
+  v.c = cl[(int64_t)c * count + idx];
+  return v;
+}
+
+struct Out {
+  Ptr m;
+  int32_t* e;
+  uint8_t* c;
+};
+__device__ __forceinline__ Out out_at(uint32_t* limbs, int32_t* ex, uint8_t* cl, int64_t count, int c, int L,
+                                      int64_t idx) {
+  Out o;
+  o.m = Ptr{limbs + (int64_t)c * L * count + idx, count};
+  o.e = ex + (int64_t)c * count + idx;
+  o.c = cl + (int64_t)c * count + idx;
+  return o;
+}
+
+__device__ __forceinline__ void neg_copy(Out o, const Val& v, int L) {
+  for (int l = 0; l < L; l++) o.m[l] = v.m[l];
+  *o.e = (int32_t)v.e;
+  uint8_t c = v.c;
+  *o.c = (c == DS_CLS_POS) ? DS_CLS_NEG : (c == DS_CLS_NEG) ? DS_CLS_POS : (c == DS_CLS_PZERO) ? DS_CLS_NZERO : DS_CLS_PZERO;
+}
+
+__device__ __forceinline__ void set_val(Out o, const Val& v, int L) {
+  for (int l = 0; l < L; l++) o.m[l] = v.m[l];
+  *o.e = (int32_t)v.e;
+  *o.c = v.c;
+}
+
+// generic scalar ops on one (possibly complex) value; scratch tmp per thread
+__device__ bool g_mul(Out o0, Out o1, Val a0, Val a1, Val b0, Val b1, int kind, int L, int p, Ptr tmp) {
+  if (kind == DS_KIND_REAL) return mul_rn(o0.m, o0.e, o0.c, a0, b0, L, p, tmp);
+  bool ok = cmul_part(o0.m, o0.e, o0.c, a0, b0, a1, b1, true, L, p, tmp);
+  ok &= cmul_part(o1.m, o1.e, o1.c, a0, b1, a1, b0, false, L, p, tmp);
+  return ok;
+}
+
+__device__ bool g_div(Out o0, Out o1, Val a0, Val a1, Val b0, Val b1, int kind, int L, int p, Ptr tmp,
+                      unsigned int* warn) {
+  if (kind == DS_KIND_REAL) return div_rn(o0.m, o0.e, o0.c, a0, b0, L, p, tmp);
+  bool ok = cdiv_part(o0.m, o0.e, o0.c, a0, a1, b0, b1, false, L, p, tmp, warn);
+  ok &= cdiv_part(o1.m, o1.e, o1.c, a0, a1, b0, b1, true, L, p, tmp, warn);
+  return ok;
+}
+
+__device__ bool g_sub(Out o0, Out o1, Val a0, Val a1, Val b0, Val b1, int kind, int L, int p, Ptr tmp) {
+  bool ok = add_rn(o0.m, o0.e, o0.c, a0, b0, true, L, p, tmp);
+  if (kind == DS_KIND_COMPLEX) ok &= add_rn(o1.m, o1.e, o1.c, a1, b1, true, L, p, tmp);
+  return ok;
+}
+
+__device__ bool g_add(Out o0, Out o1, Val a0, Val a1, Val b0, Val b1, int kind, int L, int p, Ptr tmp) {
+  bool ok = add_rn(o0.m, o0.e, o0.c, a0, b0, false, L, p, tmp);
+  if (kind == DS_KIND_COMPLEX) ok &= add_rn(o1.m, o1.e, o1.c, a1, b1, false, L, p, tmp);
+  return ok;
+}
+
+// ---------------------------------------------------------------- kernels
+struct KArgs {
+  int n, L, p, kind, ncomp, rank, world, nloc;
+  uint32_t* a_limbs; int32_t* a_exp; uint8_t* a_cls; int64_t a_count;
+  uint8_t* pbuf;
+  uint32_t* z_limbs; int32_t* z_exp; uint8_t* z_cls;
+  uint32_t *piv_limbs, *det_limbs, *cur_limbs;
+  int32_t *piv_exp, *det_exp, *cur_exp;
+  uint8_t *piv_cls, *det_cls, *cur_cls;
+  uint32_t *sig_limbs, *nrm_limbs;
+  int32_t *sig_exp, *nrm_exp;
+  uint8_t *sig_cls, *nrm_cls;
+  uint8_t* row_flags;
+  int32_t* status;
+  uint32_t* scratch; int64_t scratch_threads; int64_t scratch_words;
+};
+
+static KArgs kargs(ds_ctx* c) {
+  KArgs k;
+  k.n = c->n; k.L = c->L; k.p = c->p; k.kind = c->kind; k.ncomp = c->ncomp; k.rank = c->rank;
+  k.world = c->world; k.nloc = c->nloc;
+  k.a_limbs = c->a_limbs; k.a_exp = c->a_exp; k.a_cls = c->a_cls; k.a_count = c->a_count;
+  k.pbuf = c->pbuf;
+  k.z_limbs = c->z_limbs; k.z_exp = c->z_exp; k.z_cls = c->z_cls;
+  k.piv_limbs = c->piv_limbs; k.det_limbs = c->det_limbs; k.cur_limbs = c->cur_limbs;
+  k.piv_exp = c->piv_exp; k.det_exp = c->det_exp; k.cur_exp = c->cur_exp;
+  k.piv_cls = c->piv_cls; k.det_cls = c->det_cls; k.cur_cls = c->cur_cls;
+  k.sig_limbs = c->sig_limbs; k.nrm_limbs = c->nrm_limbs; k.sig_exp = c->sig_exp; k.nrm_exp = c->nrm_exp;
+  k.sig_cls = c->sig_cls; k.nrm_cls = c->nrm_cls; k.row_flags = c->row_flags; k.status = c->status;
+  k.scratch = c->scratch; k.scratch_threads = c->scratch_threads; k.scratch_words = c->scratch_words;
+  return k;
+}
+
+__device__ __forceinline__ Ptr thread_scratch(const KArgs& k, int64_t tid) {
+  return Ptr{k.scratch + tid, k.scratch_threads};
+}
+
+// owner stages its row i into the pivot buffer
+__global__ void k_stage(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int64_t jl = i / k.world;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  int64_t tot = (int64_t)k.ncomp * k.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(t / k.n);
+    int col = (int)(t % k.n);
+    int64_t src = jl * k.n + col;
+    for (int l = 0; l < k.L; l++)
+      pb.limbs[((int64_t)c * k.L + l) * k.n + col] = k.a_limbs[((int64_t)c * k.L + l) * k.a_count + src];
+    pb.exp[(int64_t)c * k.n + col] = k.a_exp[(int64_t)c * k.a_count + src];
+    pb.cls[(int64_t)c * k.n + col] = k.a_cls[(int64_t)c * k.a_count + src];
+  }
+}
+
+// zero test + pivots[i] + det chain (single thread, general engine)
+__global__ void k_pivot(KArgs k, int i) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (k.status[0] >= 0) return;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Val p0 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  Val p1 = k.kind == DS_KIND_COMPLEX ? val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, i) : p0;
+  bool zero = is_zero_cls(p0.c) && (k.kind == DS_KIND_REAL || is_zero_cls(p1.c));
+  if (zero) {  // elim.py:209-212 exact zero only
+    k.status[0] = i;
+    return;
+  }
+  Out pv0 = out_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, 0, k.L, i);
+  Out pv1 = out_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, k.ncomp - 1, k.L, i);
+  set_val(pv0, p0, k.L);
+  if (k.kind == DS_KIND_COMPLEX) set_val(pv1, p1, k.L);
+  Out c0 = out_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0);
+  Out c1 = out_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0);
+  Out d0 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
+  Out d1 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
+  if (!k.status[1]) {  // det = piv (unrounded, elim.py:214)
+    set_val(c0, p0, k.L);
+    if (k.kind == DS_KIND_COMPLEX) set_val(c1, p1, k.L);
+    k.status[1] = 1;
+  } else {
+    // det*piv into d (scratch), then copy to cur
+    Val q0 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0);
+    Val q1 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0);
+    Ptr tmp = thread_scratch(k, 0);
+    if (!g_mul(d0, d1, q0, q1, p0, p1, k.kind, k.L, k.p, tmp)) atomicAdd(&k.status[2], 1);
+    Val r0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
+    Val r1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
+    set_val(c0, r0, k.L);
+    if (k.kind == DS_KIND_COMPLEX) set_val(c1, r1, k.L);
+    return;
+  }
+  Val r0 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0);
+  Val r1 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0);
+  set_val(d0, r0, k.L);
+  if (k.kind == DS_KIND_COMPLEX) set_val(d1, r1, k.L);
+}
+
+// first local row index with global row > i
+__host__ __device__ static inline int first_local_after(int i, int rank, int world) {
+  int first = i + 1;
+  int k0 = (first - rank + world - 1) / world;
+  return k0 < 0 ? 0 : k0;
+}
+
+// z_j = RN(a_ji / piv), a_ji <- -z_j  (elim.py:47, 53)
+__global__ void k_mult(KArgs k, int i, int jl0) {
+  if (k.status[0] >= 0) return;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int nrows = k.nloc - jl0;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Val b0 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  Val b1 = k.kind == DS_KIND_COMPLEX ? val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, i) : b0;
+  for (int64_t r = tid; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t jl = jl0 + r;
+    int64_t idx = jl * k.n + i;
+    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+    Val a1 = k.kind == DS_KIND_COMPLEX ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx) : a0;
+    Out z0 = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 0, k.L, jl);
+    Out z1 = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, k.ncomp - 1, k.L, jl);
+    Ptr tmp = thread_scratch(k, tid);
+    if (!g_div(z0, z1, a0, a1, b0, b1, k.kind, k.L, k.p, tmp, (unsigned int*)&k.status[3]))
+      atomicAdd(&k.status[2], 1);
+    Val zv0 = val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 0, k.L, jl);
+    Out ao0 = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+    neg_copy(ao0, zv0, k.L);
+    if (k.kind == DS_KIND_COMPLEX) {
+      Val zv1 = val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 1, k.L, jl);
+      Out ao1 = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx);
+      neg_copy(ao1, zv1, k.L);
+    }
+  }
+}
+
+// general-engine update: a_jk <- RN(a_jk - RN(z_j * b_k)); used for complex
+// values (4 exact products per element) and as the reference path the fused
+// real kernel is tested against.
+__global__ void k_update_general(KArgs k, int i, int jl0, int collect_minors) {
+  if (k.status[0] >= 0) return;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int nrows = k.nloc - jl0;
+  int kfirst = collect_minors ? 0 : i + 1;
+  int ncols = k.n - kfirst - (collect_minors ? 1 : 0);  // all k != i in range
+  if (ncols <= 0) return;
+  int64_t total = (int64_t)nrows * ncols;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Ptr tmp = thread_scratch(k, tid);
+  Ptr tv = tmp;                  // t components: 2 * L limbs
+  Ptr work = tmp.off(2 * (int64_t)k.L + 4);
+  int32_t te[2];
+  uint8_t tc[2];
+  for (int64_t w = tid; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t jl = jl0 + w / ncols;
+    int kk = kfirst + (int)(w % ncols);
+    if (collect_minors && kk >= i) kk += 1;  // skip column i
+    int64_t idx = jl * k.n + kk;
+    Val z0 = val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 0, k.L, jl);
+    Val z1 = k.kind == DS_KIND_COMPLEX ? val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 1, k.L, jl) : z0;
+    Val b0 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, kk);
+    Val b1 = k.kind == DS_KIND_COMPLEX ? val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, kk) : b0;
+    Out t0{tv, &te[0], &tc[0]};
+    Out t1{tv.off(k.L), &te[1], &tc[1]};
+    bool ok = g_mul(t0, t1, z0, z1, b0, b1, k.kind, k.L, k.p, work);
+    Val tv0{CPtr{tv.p, tv.s}, te[0], tc[0]};
+    Val tv1{CPtr{tv.off(k.L).p, tv.s}, te[1], tc[1]};
+    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+    Val a1 = k.kind == DS_KIND_COMPLEX ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx) : a0;
+    Out o0 = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+    Out o1 = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, k.ncomp - 1, k.L, idx);
+    // add_rn reads a fully before writing (result goes to a's own slots):
+    // stage a - t through scratch to avoid aliasing
+    Ptr r0 = work.off(2 * (int64_t)k.L + 4);
+    int32_t re0, re1;
+    uint8_t rc0, rc1;
+    ok &= add_rn(r0, &re0, &rc0, a0, tv0, true, k.L, k.p, work);
+    if (k.kind == DS_KIND_COMPLEX) {
+      Ptr r1 = r0.off(k.L);
+      ok &= add_rn(r1, &re1, &rc1, a1, tv1, true, k.L, k.p, work);
+      for (int l = 0; l < k.L; l++) o1.m[l] = r1[l];
+      *o1.e = re1;
+      *o1.c = rc1;
+    }
+    for (int l = 0; l < k.L; l++) o0.m[l] = r0[l];
+    *o0.e = re0;
+    *o0.c = rc0;
+    if (!ok) atomicAdd(&k.status[2], 1);
+  }
+}
+
+// signed minors for m = i+2 from local row (i+1): sig_k = RN(det * a_{i+1,k}),
+// k < m-1, sig_{m-1} = det   (elim.py:56-61)
+__global__ void k_emit_signed(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int m = i + 2;
+  int64_t jl = (i + 1) / k.world;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Val d0 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0);
+  Val d1 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0);
+  for (int64_t kk = tid; kk < m; kk += (int64_t)gridDim.x * blockDim.x) {
+    int64_t oidx = jl * k.n + kk;
+    Out s0 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, oidx);
+    Out s1 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, oidx);
+    if (kk == m - 1) {
+      set_val(s0, d0, k.L);
+      if (k.kind == DS_KIND_COMPLEX) set_val(s1, d1, k.L);
+      continue;
+    }
+    int64_t aidx = jl * k.n + kk;
+    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, aidx);
+    Val a1 = k.kind == DS_KIND_COMPLEX ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, aidx) : a0;
+    Ptr tmp = thread_scratch(k, tid);
+    if (!g_mul(s0, s1, d0, d1, a0, a1, k.kind, k.L, k.p, tmp)) atomicAdd(&k.status[2], 1);
+  }
+}
+
+// normalized = RN(sig_k / sig_0) unless sig_0 == 0 (elim.py:138-155)
+__global__ void k_emit_norm(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int m = i + 2;
+  int64_t jl = (i + 1) / k.world;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
+  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, jl * k.n);
+  bool lead_zero = is_zero_cls(l0.c) && (k.kind == DS_KIND_REAL || is_zero_cls(l1.c));
+  if (tid == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
+  if (lead_zero) return;
+  for (int64_t kk = tid; kk < m; kk += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = jl * k.n + kk;
+    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
+    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, idx);
+    Out o0 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, 0, k.L, idx);
+    Out o1 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, k.ncomp - 1, k.L, idx);
+    Ptr tmp = thread_scratch(k, tid);
+    if (!g_div(o0, o1, s0, s1, l0, l1, k.kind, k.L, k.p, tmp, (unsigned int*)&k.status[3]))
+      atomicAdd(&k.status[2], 1);
+  }
+}
+
+// element-wise conformance op (ds_scalar_op)
+__global__ void k_scalar_op(int op, int kind, int L, int p, int64_t count, const uint32_t* al, const int32_t* ae,
+                            const uint8_t* ac, const uint32_t* bl, const int32_t* be, const uint8_t* bc,
+                            uint32_t* ol, int32_t* oe, uint8_t* oc, uint32_t* scratch, int64_t sthreads,
+                            int32_t* status) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int ncomp = kind == DS_KIND_COMPLEX ? 2 : 1;
+  for (int64_t e = tid; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    Val a0 = val_at(al, ae, ac, count, 0, L, e), b0 = val_at(bl, be, bc, count, 0, L, e);
+    Val a1 = kind ? val_at(al, ae, ac, count, 1, L, e) : a0;
+    Val b1 = kind ? val_at(bl, be, bc, count, 1, L, e) : b0;
+    Out o0 = out_at(ol, oe, oc, count, 0, L, e), o1 = out_at(ol, oe, oc, count, ncomp - 1, L, e);
+    Ptr tmp{scratch + tid, sthreads};
+    bool ok;
+    switch (op) {
+      case 0: ok = g_mul(o0, o1, a0, a1, b0, b1, kind, L, p, tmp); break;
+      case 1: ok = g_sub(o0, o1, a0, a1, b0, b1, kind, L, p, tmp); break;
+      case 2: ok = g_div(o0, o1, a0, a1, b0, b1, kind, L, p, tmp, (unsigned int*)&status[3]); break;
+      default: ok = g_add(o0, o1, a0, a1, b0, b1, kind, L, p, tmp); break;
+    }
+    if (!ok) atomicAdd(&status[2], 1);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static int64_t general_scratch_words(int L, int kind) {
+  int64_t w = 8 * (int64_t)L + 64;                        // real div / mul / add
+  if (kind == DS_KIND_COMPLEX) w = cdiv_scratch_words(L, 32 * L) + 16;
+  w += 6 * (int64_t)L + 16;                               // update: t (2L) + result (2L) + pad
+  return w;
+}
+
+template <typename T>
+static int dmalloc(ds_ctx* ctx, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    ctx->err = std::string("cudaMalloc failed: ") + cudaGetErrorString(e);
+    g_last_error = ctx->err;
+    return e == cudaErrorMemoryAllocation ? DS_OOM : DS_CUDA;
+  }
+  return DS_OK;
+}
+
+extern "C" {
+
+const char* ds_version(void) { return DS_VERSION; }
+
+const char* ds_last_error(ds_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+void* ds_stream(ds_ctx* ctx) { return (void*)ctx->stream; }
+
+int ds_set_stream(ds_ctx* ctx, void* stream) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return DS_OK;
+}
+
+int ds_use_pivot_buffer(ds_ctx* ctx, void* dptr, size_t bytes) {
+  if (dptr && bytes < ctx->pbuf_bytes) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->pbuf = dptr ? (uint8_t*)dptr : ctx->own_pbuf;
+  return DS_OK;
+}
+
+int ds_pivot_copy(ds_ctx* dst, ds_ctx* src) {
+  ds_ctx* ctx = dst;
+  if (dst->pbuf_bytes != src->pbuf_bytes) return DS_INVALID;
+  CK(cudaSetDevice(src->device));
+  CK(cudaEventRecord(src->ev, src->stream));
+  CK(cudaSetDevice(dst->device));
+  CK(cudaStreamWaitEvent(dst->stream, src->ev, 0));
+  if (dst->device == src->device) {
+    CK(cudaMemcpyAsync(dst->pbuf, src->pbuf, dst->pbuf_bytes, cudaMemcpyDeviceToDevice, dst->stream));
+  } else {
+    CK(cudaMemcpyPeerAsync(dst->pbuf, dst->device, src->pbuf, src->device, dst->pbuf_bytes, dst->stream));
+  }
+  // src must not overwrite its buffer before the copy has read it
+  CK(cudaEventRecord(dst->ev, dst->stream));
+  CK(cudaSetDevice(src->device));
+  CK(cudaStreamWaitEvent(src->stream, dst->ev, 0));
+  return DS_OK;
+}
+
+int64_t ds_launch_count(ds_ctx* ctx) { return ctx->launches; }
+
+void ds_destroy(ds_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  void* ptrs[] = {ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->own_pbuf, ctx->z_limbs, ctx->z_exp, ctx->z_cls,
+                  ctx->piv_limbs, ctx->det_limbs, ctx->cur_limbs, ctx->piv_exp, ctx->det_exp, ctx->cur_exp,
+                  ctx->piv_cls, ctx->det_cls, ctx->cur_cls, ctx->sig_limbs, ctx->nrm_limbs, ctx->sig_exp,
+                  ctx->nrm_exp, ctx->sig_cls, ctx->nrm_cls, ctx->row_flags, ctx->status, ctx->scratch};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  update_plan_free(&ctx->plan);
+  if (ctx->ev) cudaEventDestroy(ctx->ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int rank, int world) {
+  *out = nullptr;
+  if (n < 1 || prec_bits < 64 || prec_bits > (1L << 24) || (kind != DS_KIND_REAL && kind != DS_KIND_COMPLEX) ||
+      world < 1 || rank < 0 || rank >= world) {
+    g_last_error = "ds_create: invalid arguments";
+    return DS_INVALID;
+  }
+  ds_ctx* ctx = new ds_ctx();
+  ctx->n = n; ctx->p = (int)prec_bits; ctx->L = nlimbs(prec_bits); ctx->kind = kind;
+  ctx->ncomp = kind == DS_KIND_COMPLEX ? 2 : 1; ctx->device = device; ctx->rank = rank; ctx->world = world;
+  ctx->nloc = (n - rank + world - 1) / world;
+  ctx->launches = 0;
+  memset(&ctx->plan, 0, sizeof(ctx->plan));
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  CK(cudaEventCreateWithFlags(&ctx->ev, cudaEventDisableTiming));
+  int L = ctx->L, nc = ctx->ncomp;
+  ctx->a_count = (int64_t)ctx->nloc * n;
+  int rc;
+#define AL(ptr, cnt) if ((rc = dmalloc(ctx, &ptr, (size_t)(cnt))) != DS_OK) { ds_destroy(ctx); return rc; }
+  AL(ctx->a_limbs, (int64_t)nc * L * ctx->a_count);
+  AL(ctx->a_exp, (int64_t)nc * ctx->a_count);
+  AL(ctx->a_cls, (int64_t)nc * ctx->a_count);
+  ctx->pbuf_bytes = pbuf_size(n, L, nc);
+  AL(ctx->own_pbuf, ctx->pbuf_bytes);
+  ctx->pbuf = ctx->own_pbuf;
+  AL(ctx->z_limbs, (int64_t)nc * L * ctx->nloc);
+  AL(ctx->z_exp, (int64_t)nc * ctx->nloc);
+  AL(ctx->z_cls, (int64_t)nc * ctx->nloc);
+  AL(ctx->piv_limbs, (int64_t)nc * L * n); AL(ctx->piv_exp, (int64_t)nc * n); AL(ctx->piv_cls, (int64_t)nc * n);
+  AL(ctx->det_limbs, (int64_t)nc * L * n); AL(ctx->det_exp, (int64_t)nc * n); AL(ctx->det_cls, (int64_t)nc * n);
+  AL(ctx->cur_limbs, (int64_t)nc * L); AL(ctx->cur_exp, nc); AL(ctx->cur_cls, nc);
+  AL(ctx->sig_limbs, (int64_t)nc * L * ctx->a_count);
+  AL(ctx->sig_exp, (int64_t)nc * ctx->a_count);
+  AL(ctx->sig_cls, (int64_t)nc * ctx->a_count);
+  AL(ctx->nrm_limbs, (int64_t)nc * L * ctx->a_count);
+  AL(ctx->nrm_exp, (int64_t)nc * ctx->a_count);
+  AL(ctx->nrm_cls, (int64_t)nc * ctx->a_count);
+  AL(ctx->row_flags, n);
+  AL(ctx->status, 8);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  ctx->scratch_threads = (int64_t)sms * 4 * 128;
+  ctx->scratch_words = general_scratch_words(L, kind);
+  AL(ctx->scratch, ctx->scratch_threads * ctx->scratch_words);
+#undef AL
+  CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
+  int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
+  if (kind == DS_KIND_REAL) {
+    rc = update_plan_init(&ctx->plan, n, ctx->p, device);
+    if (rc != DS_OK) {
+      ctx->err = g_last_error;
+      ds_destroy(ctx);
+      return rc;
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = ctx;
+  return DS_OK;
+}
+
+int ds_load(ds_ctx* ctx, const ds_soa* h) {
+  CK(cudaSetDevice(ctx->device));
+  int n = ctx->n, L = ctx->L;
+  if (h->count != (int64_t)n * n) return DS_INVALID;
+  // gather owned rows (row-cyclic) plane by plane; contiguous when world == 1
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++) {
+      const uint32_t* src = h->limbs + ((int64_t)c * L + l) * h->count;
+      uint32_t* dst = ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count;
+      if (ctx->world == 1) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * h->count, cudaMemcpyHostToDevice, ctx->stream));
+      } else {
+        CK(cudaMemcpy2DAsync(dst, sizeof(uint32_t) * n, src + (int64_t)ctx->rank * n,
+                             sizeof(uint32_t) * n * ctx->world, sizeof(uint32_t) * n, ctx->nloc,
+                             cudaMemcpyHostToDevice, ctx->stream));
+      }
+    }
+    const int32_t* se = h->exp + (int64_t)c * h->count;
+    const uint8_t* sc = h->cls + (int64_t)c * h->count;
+    CK(cudaMemcpy2DAsync(ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, se + (int64_t)ctx->rank * n,
+                         sizeof(int32_t) * n * ctx->world, sizeof(int32_t) * n, ctx->nloc, cudaMemcpyHostToDevice,
+                         ctx->stream));
+    CK(cudaMemcpy2DAsync(ctx->a_cls + (int64_t)c * ctx->a_count, n, sc + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+                         n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // reset run state
+  CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
+  int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+int ds_fetch(ds_ctx* ctx, ds_soa* h) {
+  CK(cudaSetDevice(ctx->device));
+  int n = ctx->n, L = ctx->L;
+  if (h->count != (int64_t)n * n) return DS_INVALID;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++) {
+      uint32_t* dst = h->limbs + ((int64_t)c * L + l) * h->count;
+      const uint32_t* src = ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count;
+      CK(cudaMemcpy2DAsync(dst + (int64_t)ctx->rank * n, sizeof(uint32_t) * n * ctx->world, src, sizeof(uint32_t) * n,
+                           sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaMemcpy2DAsync(h->exp + (int64_t)c * h->count + (int64_t)ctx->rank * n, sizeof(int32_t) * n * ctx->world,
+                         ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpy2DAsync(h->cls + (int64_t)c * h->count + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+                         ctx->a_cls + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+int ds_pivot_buffer(ds_ctx* ctx, void** dptr, size_t* bytes) {
+  *dptr = ctx->pbuf;
+  *bytes = ctx->pbuf_bytes;
+  return DS_OK;
+}
+
+static int grid_for(ds_ctx* ctx, int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  int64_t gmax = ctx->scratch_threads / block;
+  if (g > gmax) g = gmax;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int ds_pivot_stage(ds_ctx* ctx, int i) {
+  if (i < 0 || i >= ctx->n || i % ctx->world != ctx->rank) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  KArgs k = kargs(ctx);
+  int g = (int)(((int64_t)ctx->ncomp * ctx->n + 255) / 256);
+  k_stage<<<g, 256, 0, ctx->stream>>>(k, i);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return DS_OK;
+}
+
+// use the general engine for the real update too (testing / A-B checks)
+static int g_force_general = -1;
+static bool force_general() {
+  if (g_force_general < 0) {
+    const char* s = getenv("DS_FORCE_GENERAL_UPDATE");
+    g_force_general = (s && s[0] == '1') ? 1 : 0;
+  }
+  return g_force_general == 1;
+}
+
+int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
+  if (i < 0 || i >= ctx->n) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  KArgs k = kargs(ctx);
+  cudaStream_t s = ctx->stream;
+  k_pivot<<<1, 32, 0, s>>>(k, i);
+  ctx->launches++;
+  int jl0 = first_local_after(i, ctx->rank, ctx->world);
+  int nrows = ctx->nloc - jl0;
+  if (nrows > 0) {
+    k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
+    ctx->launches++;
+    if (ctx->kind == DS_KIND_REAL && ctx->plan.enabled && !force_general()) {
+      int rc = update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf, ctx->z_limbs,
+                             ctx->z_exp, ctx->z_cls, ctx->nloc, ctx->n, i, jl0, collect_minors, ctx->status,
+                             &ctx->launches);
+      if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
+    } else {
+      int kfirst = collect_minors ? 0 : i + 1;
+      int64_t ncols = ctx->n - kfirst - (collect_minors ? 1 : 0);
+      if (ncols > 0) {
+        k_update_general<<<grid_for(ctx, nrows * ncols, 128), 128, 0, s>>>(k, i, jl0, collect_minors);
+        ctx->launches++;
+      }
+    }
+  }
+  if (collect_minors && i + 1 < ctx->n) {
+    int m = i + 2;
+    if ((series || m == ctx->n) && (i + 1) % ctx->world == ctx->rank) {
+      k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
+      k_emit_norm<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
+      ctx->launches += 2;
+    }
+  }
+  CK(cudaGetLastError());
+  return DS_OK;
+}
+
+int ds_status(ds_ctx* ctx, int* failed_step) {
+  CK(cudaSetDevice(ctx->device));
+  int32_t st[8];
+  CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *failed_step = st[0];
+  if (st[2] != 0) {
+    ctx->err = "exponent left the MPFR default range";
+    return DS_OVERFLOW;
+  }
+  return DS_OK;
+}
+
+int ds_set_det(ds_ctx* ctx, const ds_soa* d) {
+  CK(cudaSetDevice(ctx->device));
+  int L = ctx->L;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++)
+      CK(cudaMemcpyAsync(ctx->cur_limbs + (int64_t)c * L + l, d->limbs + ((int64_t)c * L + l) * d->count,
+                         sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->cur_exp + c, d->exp + (int64_t)c * d->count, sizeof(int32_t), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->cur_cls + c, d->cls + (int64_t)c * d->count, 1, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  int one = 1;
+  CK(cudaMemcpyAsync(ctx->status + 1, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+static int copy_vec(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
+                    int64_t src_count, int64_t n_items) {
+  if (!dst || !dst->limbs || n_items <= 0) return DS_OK;
+  int L = ctx->L;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++)
+      CK(cudaMemcpyAsync(dst->limbs + ((int64_t)c * L + l) * dst->count, limbs + ((int64_t)c * L + l) * src_count,
+                         sizeof(uint32_t) * n_items, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(dst->exp + (int64_t)c * dst->count, ex + (int64_t)c * src_count, sizeof(int32_t) * n_items,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(dst->cls + (int64_t)c * dst->count, cl + (int64_t)c * src_count, n_items,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  return DS_OK;
+}
+
+static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl) {
+  // owned minors rows (local index jl <-> global row rank + jl*world) into a
+  // full n*n host matrix
+  if (!dst || !dst->limbs) return DS_OK;
+  int n = ctx->n, L = ctx->L;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++)
+      CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + (int64_t)ctx->rank * n,
+                           sizeof(uint32_t) * n * ctx->world, limbs + ((int64_t)c * L + l) * ctx->a_count,
+                           sizeof(uint32_t) * n, sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + (int64_t)ctx->rank * n, sizeof(int32_t) * n * ctx->world,
+                         ex + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+                         cl + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  return DS_OK;
+}
+
+int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) {
+  CK(cudaSetDevice(ctx->device));
+  int rc;
+  if ((rc = copy_vec(ctx, &r->pivots, ctx->piv_limbs, ctx->piv_exp, ctx->piv_cls, ctx->n, upto)) != DS_OK) return rc;
+  if ((rc = copy_vec(ctx, &r->dets, ctx->det_limbs, ctx->det_exp, ctx->det_cls, ctx->n, upto)) != DS_OK) return rc;
+  if ((rc = copy_rows(ctx, &r->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls)) != DS_OK) return rc;
+  if ((rc = copy_rows(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls)) != DS_OK) return rc;
+  if (r->row_flags) {
+    // flags of rows this rank owns (m-1 % world == rank)
+    uint8_t* tmp = (uint8_t*)malloc(ctx->n);
+    CK(cudaMemcpyAsync(tmp, ctx->row_flags, ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int m1 = ctx->rank; m1 < ctx->n; m1 += ctx->world) r->row_flags[m1] = tmp[m1];
+    free(tmp);
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop_step, ds_results* res,
+           int* steps_done) {
+  if (ctx->world != 1) return DS_INVALID;
+  if (start_step < 0 || stop_step > ctx->n || start_step > stop_step) return DS_INVALID;
+  int rc;
+  for (int i = start_step; i < stop_step; i++) {
+    if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) return rc;
+    if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) return rc;
+  }
+  int failed;
+  rc = ds_status(ctx, &failed);
+  int upto = failed >= 0 ? failed : stop_step;
+  *steps_done = upto;
+  if (res) {
+    int rc2 = ds_results_fetch(ctx, upto, res);
+    if (rc2 != DS_OK) return rc2;
+  }
+  if (rc != DS_OK) return rc;
+  return failed >= 0 ? DS_ZERO_PIVOT : DS_OK;
+}
+
+int ds_scalar_op(int op, int kind, long prec_bits, int device, const ds_soa* a, const ds_soa* b, ds_soa* out) {
+  ds_ctx* ctx = nullptr;
+  if (prec_bits < 64 || a->count != b->count || a->count != out->count) return DS_INVALID;
+  CK(cudaSetDevice(device));
+  int L = nlimbs(prec_bits), nc = kind == DS_KIND_COMPLEX ? 2 : 1;
+  int64_t cnt = a->count;
+  if (cnt == 0) return DS_OK;
+  size_t lb = sizeof(uint32_t) * nc * L * cnt, eb = sizeof(int32_t) * nc * cnt, cb = (size_t)nc * cnt;
+  uint8_t* buf;
+  int64_t sthreads = 148 * 4 * 128;
+  int64_t swords = general_scratch_words(L, kind);
+  size_t total = 3 * (lb + eb + cb) + 64 + sizeof(uint32_t) * sthreads * swords + 64;
+  CK(cudaMalloc(&buf, total));
+  uint8_t* q = buf;
+  auto take = [&](size_t bytes) { uint8_t* r = q; q += (bytes + 15) & ~(size_t)15; return r; };
+  uint32_t *al = (uint32_t*)take(lb), *bl = (uint32_t*)take(lb), *ol = (uint32_t*)take(lb);
+  int32_t *ae = (int32_t*)take(eb), *be = (int32_t*)take(eb), *oe = (int32_t*)take(eb);
+  uint8_t *ac = take(cb), *bc = take(cb), *oc = take(cb);
+  int32_t* st = (int32_t*)take(64);
+  uint32_t* scratch = (uint32_t*)take(sizeof(uint32_t) * sthreads * swords);
+  CK(cudaMemcpy(al, a->limbs, lb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(bl, b->limbs, lb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ae, a->exp, eb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(be, b->exp, eb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ac, a->cls, cb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(bc, b->cls, cb, cudaMemcpyHostToDevice));
+  CK(cudaMemset(st, 0, 64));
+  int block = 128;
+  int64_t g = (cnt + block - 1) / block;
+  if (g > sthreads / block) g = sthreads / block;
+  k_scalar_op<<<(int)g, block>>>(op, kind, L, (int)prec_bits, cnt, al, ae, ac, bl, be, bc, ol, oe, oc, scratch,
+                                 sthreads, st);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out->limbs, ol, lb, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out->exp, oe, eb, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out->cls, oc, cb, cudaMemcpyDeviceToHost));
+  int32_t hst[16];
+  CK(cudaMemcpy(hst, st, 64, cudaMemcpyDeviceToHost));
+  CK(cudaFree(buf));
+  return hst[2] ? DS_OVERFLOW : DS_OK;
+}
+
+}  // extern "C"

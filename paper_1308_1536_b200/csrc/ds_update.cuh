@@ -1,0 +1,20 @@
+// ds_update.cuh -- interface of the fused real update engine (ds_update.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+struct UpdatePlan {
+  int enabled;
+  int n, p, L, D;     // precision, 32-bit limbs, 24-bit digits
+  int device, sms;
+  int tr, tc, w;       // tile rows/cols, register block
+  size_t smem;
+  void* workspace;
+};
+
+int update_plan_init(UpdatePlan* plan, int n, int p, int device);
+void update_plan_free(UpdatePlan* plan);
+int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
+                  int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
+                  const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
+                  int64_t* launches);

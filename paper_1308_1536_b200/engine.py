@@ -1,0 +1,165 @@
+"""Device elimination context: a thin Python owner of one `ds_ctx`
+(libdetseries_b200.so) holding this rank's row-cyclic shard in HBM.
+
+world == 1 runs the whole step loop natively (`run`).  world > 1 exposes
+the per-step building blocks (`stage`, `step`) and the broadcast buffer so a
+driver can broadcast each pivot row from its owner (parexec.py:300-317
+semantics) -- see parexec.py of this package.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._native import DS_INVALID, DS_OK, DS_OOM, DS_OVERFLOW, DS_ZERO_PIVOT, ds_results
+from .errors import DeviceUnavailable, WorkerFailure
+from .soa import SoA
+
+
+@dataclass
+class HostResults:
+    """Host copies of one run's outputs, in the ds SoA layout."""
+
+    pivots: SoA
+    dets: SoA
+    signed: SoA | None
+    normalized: SoA | None
+    row_flags: np.ndarray
+
+    @classmethod
+    def alloc(cls, n: int, ncomp: int, L: int, minors: bool, pinned: bool = False) -> "HostResults":
+        return cls(SoA(ncomp, L, n, pinned=pinned), SoA(ncomp, L, n, pinned=pinned),
+                   SoA(ncomp, L, n * n, pinned=pinned) if minors else None,
+                   SoA(ncomp, L, n * n, pinned=pinned) if minors else None,
+                   np.zeros(n, dtype=np.uint8))
+
+    def c(self) -> ds_results:
+        z = _native.ds_soa(0, 0, 0, 0)
+        r = ds_results()
+        r.pivots = self.pivots.c()
+        r.dets = self.dets.c()
+        r.signed_minors = self.signed.c() if self.signed is not None else z
+        r.normalized = self.normalized.c() if self.normalized is not None else z
+        r.row_flags = self.row_flags.ctypes.data
+        return r
+
+
+def _check(rc: int, ctx, what: str, rank: int = 0):
+    if rc == DS_OK or rc == DS_ZERO_PIVOT:
+        return
+    msg = _native.last_error(ctx)
+    if rc == DS_OOM:
+        raise MemoryError(f"{what}: device allocation failed: {msg}")
+    if rc == DS_INVALID:
+        raise ValueError(f"{what}: invalid arguments {msg}")
+    if rc == DS_OVERFLOW:
+        raise OverflowError(f"{what}: exponent left MPFR's default range ({msg})")
+    raise WorkerFailure(rank, f"{what} failed with code {rc}: {msg}")
+
+
+class DeviceElimination:
+    """One rank's device context (ds_create .. ds_destroy)."""
+
+    def __init__(self, n: int, prec_bits: int, kind: str, device: int = 0, rank: int = 0, world: int = 1):
+        self.lib = _native.lib()
+        self.n, self.prec_bits, self.kind = n, prec_bits, kind
+        self.ncomp = 2 if kind == "complex" else 1
+        self.L = (prec_bits + 31) // 32
+        self.device, self.rank, self.world = device, rank, world
+        ctx = ctypes.c_void_p()
+        rc = self.lib.ds_create(ctypes.byref(ctx), n, prec_bits,
+                                _native.DS_KIND_COMPLEX if kind == "complex" else _native.DS_KIND_REAL,
+                                device, rank, world)
+        if rc != DS_OK:
+            _check(rc, None, "ds_create", rank)
+        self.ctx = ctx
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.ds_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- data movement ---------------------------------------------------
+    def load(self, matrix: SoA):
+        s = matrix.c()
+        _check(self.lib.ds_load(self.ctx, ctypes.byref(s)), self.ctx, "ds_load", self.rank)
+
+    def fetch(self, matrix: SoA):
+        s = matrix.c()
+        _check(self.lib.ds_fetch(self.ctx, ctypes.byref(s)), self.ctx, "ds_fetch", self.rank)
+
+    def set_det(self, det: SoA):
+        s = det.c()
+        _check(self.lib.ds_set_det(self.ctx, ctypes.byref(s)), self.ctx, "ds_set_det", self.rank)
+
+    # -- serial engine -----------------------------------------------------
+    def run(self, collect_minors: bool, series: bool, start: int, stop: int, res: HostResults):
+        """Steps [start, stop) on the device; returns (rc, steps_done)."""
+        r = res.c()
+        done = ctypes.c_int(0)
+        rc = self.lib.ds_run(self.ctx, int(collect_minors), int(series), start, stop, ctypes.byref(r),
+                             ctypes.byref(done))
+        _check(rc, self.ctx, "ds_run", self.rank)
+        return rc, done.value
+
+    # -- sharded building blocks ---------------------------------------------
+    def pivot_buffer(self):
+        p = ctypes.c_void_p()
+        nbytes = ctypes.c_size_t()
+        _check(self.lib.ds_pivot_buffer(self.ctx, ctypes.byref(p), ctypes.byref(nbytes)), self.ctx,
+               "ds_pivot_buffer", self.rank)
+        return p.value, nbytes.value
+
+    def stage(self, i: int):
+        _check(self.lib.ds_pivot_stage(self.ctx, i), self.ctx, "ds_pivot_stage", self.rank)
+
+    def step(self, i: int, collect_minors: bool, series: bool):
+        _check(self.lib.ds_step(self.ctx, i, int(collect_minors), int(series)), self.ctx, "ds_step", self.rank)
+
+    def status(self) -> int:
+        f = ctypes.c_int(-1)
+        _check(self.lib.ds_status(self.ctx, ctypes.byref(f)), self.ctx, "ds_status", self.rank)
+        return f.value
+
+    def results(self, upto: int, res: HostResults):
+        r = res.c()
+        _check(self.lib.ds_results_fetch(self.ctx, upto, ctypes.byref(r)), self.ctx, "ds_results_fetch",
+               self.rank)
+
+    def stream(self) -> int:
+        return self.lib.ds_stream(self.ctx) or 0
+
+    def launches(self) -> int:
+        return int(self.lib.ds_launch_count(self.ctx))
+
+
+def scalar_op(op: str, kind: str, prec_bits: int, a: SoA, b: SoA, device: int = 0) -> SoA:
+    """Element-wise correctly rounded op on the device (conformance surface)."""
+    lib = _native.lib()
+    code = {"mul": 0, "sub": 1, "div": 2, "add": 3}[op]
+    out = SoA.like(a)
+    sa, sb, so = a.c(), b.c(), out.c()
+    rc = lib.ds_scalar_op(code, _native.DS_KIND_COMPLEX if kind == "complex" else _native.DS_KIND_REAL,
+                          prec_bits, device, ctypes.byref(sa), ctypes.byref(sb), ctypes.byref(so))
+    if rc not in (DS_OK,):
+        _check(rc, None, "ds_scalar_op")
+    return out
+
+
+__all__ = ["DeviceElimination", "HostResults", "scalar_op", "DeviceUnavailable"]

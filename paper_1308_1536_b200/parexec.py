@@ -1,0 +1,357 @@
+"""Row-cyclic sharded elimination (reference parexec.py:1-424) over B200 ranks.
+
+Rows are interleaved across T ranks (rank r owns rows i with i % T == r,
+parexec.py:50-52 in 0-based form).  At step i the owner of row i stages that
+row, UNNORMALIZED, into its pivot buffer; the buffer is broadcast to every
+rank; every rank recomputes the det chain and applies the identical per-row
+update to the rows it owns; the owner of row i+1 emits the minor row.  A row's
+final value depends only on its own history and the broadcast pivot rows, so
+results are bit-identical for every T (parexec.py:3-8) -- the G-invariance the
+tests gate on.
+
+Transports:
+  * "local"  -- T virtual shards in this process, one device context each
+                (round-robin over the visible GPUs); the broadcast is a
+                device-to-device / peer copy of the pivot buffer.
+  * "process" / "nccl" -- one process per GPU under torch.distributed (the
+                caller ran init_process_group, e.g. via torchrun); the
+                broadcast is torch.distributed.broadcast of a device tensor
+                that IS the pivot buffer (NCCL over NVLink), stream-ordered
+                with the kernels on torch's current stream.
+The wire format of the reference (pack_row / unpack_row, MPRW v1 with CRC32,
+parexec.py:72-157) is kept for API compatibility; the device path does not
+serialize -- HBM already holds the binary limb layout.
+"""
+
+from __future__ import annotations
+
+import struct
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import mp
+from .elim import EliminationTrace, MinorSeries, minor_rows_from_results
+from .engine import DeviceElimination, HostResults
+from .errors import CorruptPayload, ZeroPivot
+from .matrix import MatrixBuffer
+from .mp import mpc, mpfr
+from .scalars import Precision
+from .soa import SoA
+
+WIRE_MAGIC = b"MPRW"
+WIRE_VERSION = 1
+ABORT_MAGIC = b"MPRA"
+_SIGN_POS, _SIGN_NEG, _SIGN_PZERO, _SIGN_NZERO = 0, 1, 2, 3
+
+
+@dataclass(frozen=True)
+class WorkerTopology:
+    """Row ownership for T workers (parexec.py:39-55), 1-based like the reference."""
+
+    workers: int
+    n: int
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ValueError("worker count must be >= 1")
+
+    def owner(self, row: int) -> int:
+        return ((row - 1) % self.workers) + 1
+
+    def owned_rows(self, worker: int) -> list:
+        return list(range(worker, self.n + 1, self.workers))
+
+
+@dataclass
+class CommStats:
+    """Broadcast accounting (parexec.py:58-69); bytes are pivot-buffer bytes."""
+
+    broadcasts: int = 0
+    bytes_total: int = 0
+    per_step_bytes: list = field(default_factory=list)
+    minor_messages: int = 0
+    fanout_deliveries: int = 0
+
+
+# ------------------------------------------------------------------ wire format
+
+def _pack_real(out: bytearray, x):
+    if x == 0:
+        out.append(_SIGN_NZERO if mp.is_signed(x) else _SIGN_PZERO)
+        out += struct.pack("<qI", 0, 0)
+        return
+    m, e = x.as_mantissa_exp()
+    m, e = int(m), int(e)
+    out.append(_SIGN_NEG if m < 0 else _SIGN_POS)
+    mag = abs(m)
+    nl = (mag.bit_length() + 63) // 64
+    out += struct.pack("<qI", e, nl)
+    out += mag.to_bytes(nl * 8, "little")
+
+
+def pack_row(step: int, scalars, kind: str) -> bytes:
+    """MPRW v1: magic, u8 version, u32 step, u32 records, records, CRC32."""
+    out = bytearray(WIRE_MAGIC)
+    out += struct.pack("<BII", WIRE_VERSION, step, len(scalars) * (2 if kind == "complex" else 1))
+    for x in scalars:
+        for part in ((x.real, x.imag) if kind == "complex" else (x,)):
+            _pack_real(out, part)
+    out += struct.pack("<I", zlib.crc32(bytes(out)))
+    return bytes(out)
+
+
+def _unpack_real(data: bytes, off: int, bits: int):
+    sign = data[off]
+    e, nl = struct.unpack_from("<qI", data, off + 1)
+    off += 13
+    if sign in (_SIGN_PZERO, _SIGN_NZERO):
+        if nl:
+            raise CorruptPayload("zero record with nonzero limb count")
+        return (mpfr("-0") if sign == _SIGN_NZERO else mpfr(0)), off
+    if sign not in (_SIGN_POS, _SIGN_NEG):
+        raise CorruptPayload(f"bad sign byte {sign}")
+    if off + nl * 8 > len(data):
+        raise CorruptPayload("truncated limb data")
+    mag = int.from_bytes(data[off:off + nl * 8], "little")
+    off += nl * 8
+    if mag.bit_length() > bits:
+        raise CorruptPayload("mantissa wider than the declared precision")
+    x = mpfr(-mag if sign == _SIGN_NEG else mag)
+    return mp.mul_2exp(x, e), off
+
+
+def unpack_row(data: bytes, prec: Precision, kind: str):
+    if len(data) < 17:
+        raise CorruptPayload("payload shorter than the fixed header")
+    if data[:4] != WIRE_MAGIC:
+        raise CorruptPayload(f"bad magic {data[:4]!r}")
+    (crc,) = struct.unpack_from("<I", data, len(data) - 4)
+    if zlib.crc32(data[:-4]) != crc:
+        raise CorruptPayload("CRC mismatch")
+    version, step, records = struct.unpack_from("<BII", data, 4)
+    if version != WIRE_VERSION:
+        raise CorruptPayload(f"unsupported wire version {version}")
+    if kind == "complex" and records % 2:
+        raise CorruptPayload("odd record count for complex payload")
+    off, reals = 13, []
+    with prec.context():
+        for _ in range(records):
+            x, off = _unpack_real(data, off, prec.bits)
+            reals.append(x)
+        if off != len(data) - 4:
+            raise CorruptPayload("trailing bytes after the last record")
+        if kind == "complex":
+            return step, [mpc(reals[k], reals[k + 1]) for k in range(0, records, 2)]
+    return step, reals
+
+
+def pack_abort(step: int, worker: int) -> bytes:
+    return ABORT_MAGIC + struct.pack("<II", step, worker)
+
+
+def is_abort(data: bytes) -> bool:
+    return data[:4] == ABORT_MAGIC
+
+
+def unpack_abort(data: bytes):
+    return struct.unpack_from("<II", data, 4)
+
+
+def block_reassign_plan(step: int, n: int, workers: int) -> list:
+    """Contiguous blocks over rows step+1..n with sizes within one
+    (parexec.py:173-194); provided for API parity, unused by the executors."""
+    remaining = n - step
+    if remaining <= 0:
+        return []
+    base, extra = divmod(remaining, workers)
+    plan, row = [], step + 1
+    for w in range(1, workers + 1):
+        size = base + (1 if w <= extra else 0)
+        if size == 0:
+            break
+        plan.append((w, row, row + size - 1))
+        row += size
+    return plan
+
+
+# ------------------------------------------------------------------ executors
+
+def _assemble(A: MatrixBuffer, trace: EliminationTrace, res: HostResults, done: int, collect_minors: bool,
+              sink, out: MinorSeries | None):
+    p = A.prec.bits
+    for i in range(done):
+        trace.pivots.append(res.pivots.get(i, p))
+        trace.det_series.append(res.dets.get(i, p))
+    trace.step = done
+    if collect_minors:
+        emit = sink if sink is not None else out.add
+        for row in minor_rows_from_results(res, A.n, p):
+            emit(row)
+
+
+def _local_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats, devices):
+    import torch
+    n, p = A.n, A.prec.bits
+    devs = devices if devices is not None else list(range(max(1, torch.cuda.device_count())))
+    soa = A.to_soa()
+    ranks = [DeviceElimination(n, p, A.kind, devs[r % len(devs)], r, workers) for r in range(workers)]
+    try:
+        for e in ranks:
+            e.load(soa)
+        _, pbytes = ranks[0].pivot_buffer()
+        lib = ranks[0].lib
+        for i in range(n):
+            owner = ranks[i % workers]
+            owner.stage(i)
+            for e in ranks:
+                if e is not owner:
+                    rc = lib.ds_pivot_copy(e.ctx, owner.ctx)
+                    if rc != 0:
+                        raise RuntimeError(f"ds_pivot_copy failed: {rc}")
+            for e in ranks:
+                e.step(i, collect_minors, series)
+            stats.broadcasts += 1
+            stats.bytes_total += pbytes
+            stats.per_step_bytes.append(pbytes)
+            stats.fanout_deliveries += workers
+        failed = [e.status() for e in ranks]
+        f = max(failed)
+        done = f if f >= 0 else n
+        res = HostResults.alloc(n, ranks[0].ncomp, ranks[0].L, collect_minors)
+        for e in ranks:  # trace is replicated; each rank adds its owned minors rows
+            e.results(done, res)
+            e.fetch(soa)
+        stats.minor_messages = sum(1 for m in range(2, n + 1) if res.row_flags[m - 1] & 1)
+    finally:
+        for e in ranks:
+            e.close()
+    A.assign_soa(soa)
+    return res, done
+
+
+def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcast, stats: CommStats | None = None):
+    """Generic per-rank step loop of the message-passing executor.
+
+    engine    -- this rank's context (stage/step/status), a DeviceElimination
+                 on a GPU; the CPU tests pass the C oracle's context instead.
+    pivot     -- the tensor holding the pivot buffer bytes (device or host).
+    broadcast -- callable(tensor, src_rank) (torch.distributed.broadcast).
+    Returns the failed step (-1 if none).
+    """
+    world, rank = engine.world, engine.rank
+    nbytes = pivot.numel() * pivot.element_size()
+    for i in range(n):
+        owner = i % world
+        if rank == owner:
+            engine.stage(i)
+        broadcast(pivot, owner)
+        engine.step(i, collect_minors, series)
+        if stats is not None:
+            stats.broadcasts += 1
+            stats.bytes_total += nbytes
+            stats.per_step_bytes.append(nbytes)
+            stats.fanout_deliveries += world
+    return engine.status()
+
+
+def allreduce_gather(res: HostResults, soa: SoA | None, rank: int, world: int, allreduce):
+    """Combine per-rank owned rows (minors and matrix rows) into full copies on
+    every rank: non-owned entries are zeroed and an integer SUM all-reduce
+    reassembles them exactly."""
+    n = len(res.row_flags)
+    own = np.zeros(n, dtype=bool)
+    own[rank::world] = True
+
+    def combine(a: SoA):
+        count = a.count
+        rows = count // n
+        mask = np.repeat(own, rows) if rows > 1 else own
+        if rows > 1:
+            a.limbs[:, :, ~mask] = 0
+            a.exp[:, ~mask] = 0
+            a.cls[:, ~mask] = 0
+        allreduce(a.limbs.view(np.int32))
+        allreduce(a.exp)
+        allreduce(a.cls.view(np.uint8))
+
+    if res.signed is not None:
+        combine(res.signed)
+        combine(res.normalized)
+    flags = res.row_flags.copy()
+    flags[~own] = 0
+    allreduce(flags)
+    res.row_flags[:] = flags
+    if soa is not None:
+        mrows = np.repeat(own, n)
+        soa.limbs[:, :, ~mrows] = 0
+        soa.exp[:, ~mrows] = 0
+        soa.cls[:, ~mrows] = 0
+        allreduce(soa.limbs.view(np.int32))
+        allreduce(soa.exp)
+        allreduce(soa.cls)
+
+
+def _process_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats):
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        raise RuntimeError("transport='process' needs torch.distributed initialized (one process per GPU, "
+                           "e.g. torchrun); use transport='local' for in-process shards")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if world != workers:
+        raise ValueError(f"workers={workers} but the process group has {world} ranks")
+    n, p = A.n, A.prec.bits
+    dev = torch.cuda.current_device()
+    eng = DeviceElimination(n, p, A.kind, dev, rank, world)
+    try:
+        soa = A.to_soa()
+        eng.load(soa)
+        _, pbytes = eng.pivot_buffer()
+        pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+        eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
+        eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream)
+        failed = dist_run(eng, n, collect_minors, series, pivot, lambda t, src: dist.broadcast(t, src=src), stats)
+        # agree on the failed step (identical on every rank by construction)
+        f = torch.tensor([failed], dtype=torch.int64, device=f"cuda:{dev}")
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+        failed = int(f.item())
+        done = failed if failed >= 0 else n
+        res = HostResults.alloc(n, eng.ncomp, eng.L, collect_minors)
+        eng.results(done, res)
+        eng.fetch(soa)
+        eng.lib.ds_set_stream(eng.ctx, None)
+        eng.lib.ds_use_pivot_buffer(eng.ctx, None, 0)
+    finally:
+        eng.close()
+
+    def allreduce(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{dev}")
+        dist.all_reduce(t)
+        arr[...] = t.cpu().numpy()
+
+    allreduce_gather(res, soa, rank, world, allreduce)
+    A.assign_soa(soa)
+    return res, done
+
+
+def par_eliminate(A: MatrixBuffer, workers: int, transport: str = "local", collect_minors: bool = True,
+                  series: bool = True, sink=None, devices=None):
+    """Sharded elimination of A in place over `workers` ranks
+    (parexec.py:408-424).  Returns (trace, minor_series, comm_stats), bit-
+    identical to eliminate() for every worker count and transport."""
+    if transport not in ("local", "process", "nccl"):
+        raise ValueError(f"unknown transport {transport!r}")
+    topo = WorkerTopology(workers, A.n)  # validates workers >= 1
+    stats = CommStats()
+    trace = EliminationTrace(n=A.n, prec=A.prec)
+    out = MinorSeries(A.prec) if collect_minors else None
+    if transport == "local":
+        res, done = _local_run(A, topo.workers, collect_minors, series, stats, devices)
+    else:
+        res, done = _process_run(A, topo.workers, collect_minors, series, stats)
+    _assemble(A, trace, res, done, collect_minors, sink, out)
+    if done < A.n:
+        raise ZeroPivot(done + 1, trace=trace, series=out)
+    return trace, out, stats
