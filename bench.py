@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: all leading minors + last-column minors of an
+N x N matrix at p bits, one pass of the unpivoted elimination per "step".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json metric "limb-MAC/s + seconds to all minors
+(N=2000 @4096b) at 1/2/4/8 B200 vs INT32 peak"): N=2000, p=4096 bits (L=128
+limbs), collect_minors + series (every leading size emitted), real matrix.
+
+value    = schoolbook limb-MACs of the whole elimination (n(n-1)^2/2 * L^2)
+           / device time of one pass, inputs resident in HBM (restored from a
+           device snapshot each step; minors stay in HBM), max over ranks.
+e2e      = same metric through the C ABI with HOST buffers: per step the
+           pinned host matrix is copied in (ds_load), the pass runs, and the
+           pivots/dets/signed/normalized minors are copied out.
+roofline = the fused update kernel (ds_update.cu) timed live with CUDA
+           events around every launch: achieved schoolbook limb-MAC/s vs the
+           INT32-IMAD limb-product roofline (measured IMAD rate / 2).
+cpu_baseline / --impl reference = the reference hot loop (elim.py:37-53)
+           restated over MPFR (oracle/), all host threads, bounded sample.
+Multi-GPU (torchrun): row-cyclic shards, per-step NCCL broadcast of the pivot
+row (parexec.py semantics), strong scaling of the same N x N problem.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# measured on this pool's B200 (tools/microbench/imad_tput.cu, gpurun_out/imad_tput.txt):
+# IMAD 1.79e13 lane-ops/s, DFMA 1.78e13 lane-ops/s at 1965 MHz
+IMAD_OPS_PER_S = 1.79e13
+DFMA_OPS_PER_S = 1.78e13
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=2000)
+    ap.add_argument("--prec", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def work_limb_macs(n: int, L: int, complex_: bool = False) -> float:
+    return n * (n - 1) ** 2 / 2 * L * L * (4 if complex_ else 1)
+
+
+def workload(args) -> dict:
+    return {"workload": f"N={args.n} random_uniform real matrix @{args.prec}b: all leading minors + "
+                        f"last-column signed/normalized minors for every size (SURVEY 8d config 3')",
+            "n": args.n, "prec_bits": args.prec, "limbs": (args.prec + 31) // 32, "kind": "real",
+            "collect_minors": True, "series": True,
+            "l2": "inputs larger than L2 (matrix %.1f GB)" % (args.n * args.n * (4 * ((args.prec + 31) // 32) + 5) / 1e9)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower() == "active":
+                    reasons.add(name)
+        sm_sorted = sorted(sm)
+        return {"sm_mhz": sm_sorted[len(sm_sorted) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference(n: int, p: int, seconds: float, A=None):
+    """Time the reference hot loop (oracle = elim.py:37-53 over MPFR) on a
+    bounded sample: pivot steps i = 0, 1, ... applied to all later rows of a
+    full-width matrix until ~`seconds` of wall time; all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    L = (p + 31) // 32
+    threads = len(os.sched_getaffinity(0))
+    rows_per_call = max(threads * 4, 64)
+    A = random_uniform_soa(rows_per_call + 1, p, 3) if A is None else A
+    # a full-width sample: pivot row + rows_per_call rows of width n
+    from paper_1308_1536_b200.soa import SoA
+    big = random_uniform_soa(1, p, 5)  # placeholder for shape
+    prow = SoA(1, L, n)
+    rows = SoA(1, L, rows_per_call * n)
+    src = random_uniform_soa(int(np.ceil(np.sqrt((rows_per_call + 1) * n))) + 1, p, 11)
+    prow.limbs[:] = src.limbs[:, :, :n]
+    prow.exp[:] = src.exp[:, :n]
+    prow.cls[:] = src.cls[:, :n]
+    rows.limbs[:] = src.limbs[:, :, n:n + rows_per_call * n]
+    rows.exp[:] = src.exp[:, n:n + rows_per_call * n]
+    rows.cls[:] = src.cls[:, n:n + rows_per_call * n]
+    del big
+    total_t, total_macs, calls = 0.0, 0.0, 0
+    i = 0
+    while total_t < seconds and i < n - 1:
+        dt = oracle.time_apply_pivot_rows(n, p, "real", i, prow, rows, rows_per_call, threads, True)
+        total_t += dt
+        total_macs += rows_per_call * (n - 1)
+        calls += 1
+        i += 1
+    rate = total_macs * L * L / total_t
+    return {"value": rate, "unit": "limb-MAC/s", "cores": threads, "kind": "port",
+            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}) of elim.py:37-53 "
+                      f"over MPFR 4.2.1, {total_macs:.3g} MACs in {total_t:.2f}s on {threads} threads",
+            "seconds_to_all_minors_extrapolated": work_limb_macs(n, L) / rate}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    L = (args.prec + 31) // 32
+    per = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_reference(args.n, args.prec, per / 4)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_reference(args.n, args.prec, per))
+    wall = time.perf_counter() - t0
+    rate = sum(v["value"] for v in vals) / len(vals)
+    base = vals[-1]
+    out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
+           "value": rate, "unit": "limb-MAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "mpfr (u64 limbs)", "data": "synthetic", "impl": "reference",
+           "config": workload(args),
+           "seconds_to_all_minors": work_limb_macs(args.n, L) / rate,
+           "cpu_baseline": {"value": rate, "unit": "limb-MAC/s", "cores": base["cores"], "kind": "port",
+                            "sample": base["sample"]},
+           "e2e": {"value": rate, "unit": "limb-MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+    from paper_1308_1536_b200.synth import random_uniform_soa
+
+    n, p = args.n, args.prec
+    L = (p + 31) // 32
+    A = random_uniform_soa(n, p, 2000, pinned=True)  # identical on every rank
+    eng = DeviceElimination(n, p, "real", local, rank, world)
+    stream = torch.cuda.current_stream()
+    pivot = None
+    if world > 1:
+        from paper_1308_1536_b200.parexec import dist_run
+        _, pbytes = eng.pivot_buffer()
+        pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{local}")
+        eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
+    eng.lib.ds_set_stream(eng.ctx, stream.cuda_stream)
+    res = HostResults.alloc(n, 1, L, True, pinned=True)
+
+    def one_pass(resident: bool):
+        if resident:
+            eng.snapshot(False)
+        else:
+            eng.load(A)
+        if world == 1:
+            if resident:
+                eng.run_resident(True, True, 0, n)
+            else:
+                eng.run(True, True, 0, n, res)
+        else:
+            dist_run(eng, n, True, True, pivot, lambda t, src: dist.broadcast(t, src=src))
+            if not resident:
+                eng.results(n, res)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    eng.load(A)
+    eng.snapshot(True)
+    for _ in range(args.warmup):
+        one_pass(True)
+    barrier()
+    # ---- timed: resident inputs (value), update kernel profiled live
+    eng.profile(True)
+    eng.profile_read()
+    launches0 = eng.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_pass(True)
+        ev1.record(stream)
+        barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    upd_ms, upd_launches, upd_work = eng.profile_read()
+    eng.profile(False)
+    gpu_launches = eng.launches() - launches0
+    total_work = work_limb_macs(n, L)
+    value = total_work / (ms / 1e3)
+    # ---- timed: end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        one_pass(False)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_pass(False)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+        h2d = A.nbytes if world == 1 else A.nbytes  # each rank copies its rows; host buffer is the full matrix
+        d2h = res.pivots.nbytes + res.dets.nbytes + res.signed.nbytes + res.normalized.nbytes + res.row_flags.nbytes
+        e2e = {"value": total_work / e2e_s, "unit": "limb-MAC/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "seconds_to_all_minors": e2e_s}
+    # ---- roofline of the fused update kernel
+    imad_peak = IMAD_OPS_PER_S / 2  # one 32x32->64 limb product = 2 IMAD (lo + hi)
+    achieved = upd_work / (upd_ms / 1e3 / args.steps * args.steps) if upd_ms > 0 else 0.0
+    roof = {"kernel": "k_update_dfma (ds_update.cu) + digit prep", "bound": "int32-imad (limb products)",
+            "achieved": achieved, "peak": imad_peak, "unit": "limb-MAC/s", "frac": achieved / imad_peak,
+            "traffic": None, "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
+            "launches_per_step": upd_launches / args.steps,
+            "note": "peak = measured IMAD rate / 2; the kernel runs the products on the FP64 pipe "
+                    "(exact 24-bit digit DFMAs) with a short product, so frac > 1 is possible; "
+                    "pipe utilisation from ncu in profiles/"}
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            try:
+                cpu = cpu_reference(n, p, args.cpu_seconds)
+            except Exception as exc:  # never fail the GPU line on the baseline
+                cpu = {"error": repr(exc)}
+        out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
+               "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64 (exact 24-bit digit products) + u32 limbs", "data": "synthetic",
+               "config": workload(args), "seconds_to_all_minors": ms / 1e3,
+               "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
+               "clocks": clk.summary(), "parallelism": f"row-cyclic x{world}"}
+        print(json.dumps(out), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,18 @@ int ds_use_pivot_buffer(ds_ctx *ctx, void *device_ptr, size_t bytes);
 int ds_pivot_copy(ds_ctx *dst, ds_ctx *src);
 /* Number of kernel launches issued by this context since creation. */
 int64_t ds_launch_count(ds_ctx *ctx);
+/* Device-side snapshot of this rank's rows: save = 1 copies them to a
+ * backup buffer in HBM, save = 0 restores them and resets the run state
+ * (abort flag, det chain, emitted-row flags).  Lets a caller re-run the
+ * elimination on resident inputs (benchmarks, checkpoint/resume). */
+int ds_snapshot(ds_ctx *ctx, int save);
+/* Update-kernel profiling: while enabled, every update launch (digit prep +
+ * fused update) is bracketed by CUDA events on the context stream.
+ * ds_profile_read synchronises, returns the summed kernel time (ms), the
+ * number of launches and their algorithmic work in schoolbook limb-MACs
+ * (rows * cols * L^2, x4 for complex), then clears the counters. */
+int ds_profile(ds_ctx *ctx, int enable);
+int ds_profile_read(ds_ctx *ctx, double *update_ms, int64_t *launches, double *limb_macs);
 
 /* Last error message of this context (or of the last failed ds_create when
  * ctx is NULL). */

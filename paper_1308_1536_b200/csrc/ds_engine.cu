@@ -18,6 +18,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <string>
+#include <vector>
 
 #include "ds_mp.cuh"
 #include "ds_update.cuh"
@@ -58,6 +59,16 @@ struct ds_ctx {
   uint32_t* scratch;
   int64_t scratch_threads;
   int64_t scratch_words;  // words per thread
+  // device snapshot of the local rows (ds_snapshot)
+  uint32_t* snap_limbs;
+  int32_t* snap_exp;
+  uint8_t* snap_cls;
+  // update profiling
+  int prof_on;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  size_t prof_used;
+  int64_t prof_launches;
+  double prof_work;
   // fused update engine workspace
   UpdatePlan plan;
   int64_t launches;
@@ -495,6 +506,10 @@ void ds_destroy(ds_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   update_plan_free(&ctx->plan);
+  if (ctx->snap_limbs) cudaFree(ctx->snap_limbs);
+  if (ctx->snap_exp) cudaFree(ctx->snap_exp);
+  if (ctx->snap_cls) cudaFree(ctx->snap_cls);
+  for (cudaEvent_t ev : ctx->prof_ev) cudaEventDestroy(ev);
   if (ctx->ev) cudaEventDestroy(ctx->ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -661,9 +676,28 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   ctx->launches++;
   int jl0 = first_local_after(i, ctx->rank, ctx->world);
   int nrows = ctx->nloc - jl0;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (ctx->prof_on && nrows > 0) {
+    if (ctx->prof_used + 2 > ctx->prof_ev.size()) {
+      for (int q = 0; q < 256; q++) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        ctx->prof_ev.push_back(ev);
+      }
+    }
+    pe0 = ctx->prof_ev[ctx->prof_used];
+    pe1 = ctx->prof_ev[ctx->prof_used + 1];
+    ctx->prof_used += 2;
+  }
   if (nrows > 0) {
     k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
     ctx->launches++;
+    int ncols_u = collect_minors ? ctx->n - 1 : ctx->n - 1 - i;
+    if (pe0) {
+      CK(cudaEventRecord(pe0, s));
+      ctx->prof_launches++;
+      ctx->prof_work += (double)nrows * ncols_u * (double)ctx->L * ctx->L * (ctx->kind == DS_KIND_COMPLEX ? 4.0 : 1.0);
+    }
     if (ctx->kind == DS_KIND_REAL && ctx->plan.enabled && !force_general()) {
       int rc = update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf, ctx->z_limbs,
                              ctx->z_exp, ctx->z_cls, ctx->nloc, ctx->n, i, jl0, collect_minors, ctx->status,
@@ -677,6 +711,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         ctx->launches++;
       }
     }
+    if (pe1) CK(cudaEventRecord(pe1, s));
   }
   if (collect_minors && i + 1 < ctx->n) {
     int m = i + 2;
@@ -687,6 +722,56 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     }
   }
   CK(cudaGetLastError());
+  return DS_OK;
+}
+
+int ds_snapshot(ds_ctx* ctx, int save) {
+  CK(cudaSetDevice(ctx->device));
+  int nc = ctx->ncomp, L = ctx->L;
+  size_t lb = sizeof(uint32_t) * nc * L * ctx->a_count, eb = sizeof(int32_t) * nc * ctx->a_count,
+         cb = (size_t)nc * ctx->a_count;
+  if (save) {
+    int rc;
+    if (!ctx->snap_limbs) {
+      if ((rc = dmalloc(ctx, &ctx->snap_limbs, lb / 4)) != DS_OK) return rc;
+      if ((rc = dmalloc(ctx, &ctx->snap_exp, eb / 4)) != DS_OK) return rc;
+      if ((rc = dmalloc(ctx, &ctx->snap_cls, cb)) != DS_OK) return rc;
+    }
+    CK(cudaMemcpyAsync(ctx->snap_limbs, ctx->a_limbs, lb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->snap_exp, ctx->a_exp, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->snap_cls, ctx->a_cls, cb, cudaMemcpyDeviceToDevice, ctx->stream));
+    return DS_OK;
+  }
+  if (!ctx->snap_limbs) return DS_INVALID;
+  CK(cudaMemcpyAsync(ctx->a_limbs, ctx->snap_limbs, lb, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->a_exp, ctx->snap_exp, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->a_cls, ctx->snap_cls, cb, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->row_flags, 0, ctx->n, ctx->stream));
+  CK(cudaMemsetAsync(ctx->status + 1, 0, 7 * sizeof(int32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->status, 0xff, sizeof(int32_t), ctx->stream));  // -1
+  return DS_OK;
+}
+
+int ds_profile(ds_ctx* ctx, int enable) {
+  ctx->prof_on = enable ? 1 : 0;
+  return DS_OK;
+}
+
+int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot = 0;
+  for (size_t q = 0; q + 1 < ctx->prof_used; q += 2) {
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, ctx->prof_ev[q], ctx->prof_ev[q + 1]));
+    tot += f;
+  }
+  *ms = tot;
+  *launches = ctx->prof_launches;
+  *work = ctx->prof_work;
+  ctx->prof_used = 0;
+  ctx->prof_launches = 0;
+  ctx->prof_work = 0;
   return DS_OK;
 }
 

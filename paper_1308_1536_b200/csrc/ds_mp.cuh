@@ -41,13 +41,13 @@ struct Val {
   uint8_t c;  // DS_CLS_*
 };
 
-__device__ __forceinline__ bool is_zero_cls(uint8_t c) { return c >= DS_CLS_PZERO; }
-__device__ __forceinline__ int neg_of(uint8_t c) { return (c == DS_CLS_NEG || c == DS_CLS_NZERO) ? 1 : 0; }
-__device__ __forceinline__ uint8_t zero_cls(int neg) { return neg ? DS_CLS_NZERO : DS_CLS_PZERO; }
-__device__ __forceinline__ uint8_t nz_cls(int neg) { return neg ? DS_CLS_NEG : DS_CLS_POS; }
+static __device__ __forceinline__ bool is_zero_cls(uint8_t c) { return c >= DS_CLS_PZERO; }
+static __device__ __forceinline__ int neg_of(uint8_t c) { return (c == DS_CLS_NEG || c == DS_CLS_NZERO) ? 1 : 0; }
+static __device__ __forceinline__ uint8_t zero_cls(int neg) { return neg ? DS_CLS_NZERO : DS_CLS_PZERO; }
+static __device__ __forceinline__ uint8_t nz_cls(int neg) { return neg ? DS_CLS_NEG : DS_CLS_POS; }
 
 // bits [q, q+32) of a big integer S (n limbs); zero outside [0, 32n)
-__device__ __forceinline__ uint32_t bits32(CPtr S, int n, int64_t q) {
+static __device__ __forceinline__ uint32_t bits32(CPtr S, int n, int64_t q) {
   int64_t lw = q >> 5;  // floor
   int sh = (int)(q & 31);
   uint32_t lo = (lw >= 0 && lw < n) ? S[lw] : 0u;
@@ -56,7 +56,7 @@ __device__ __forceinline__ uint32_t bits32(CPtr S, int n, int64_t q) {
 }
 
 // position of the highest set bit of S, or -1 if S == 0
-__device__ __forceinline__ int64_t top_bit(CPtr S, int n) {
+static __device__ __forceinline__ int64_t top_bit(CPtr S, int n) {
   for (int k = n - 1; k >= 0; k--) {
     uint32_t v = S[k];
     if (v) return (int64_t)k * 32 + 31 - __clz(v);
@@ -65,7 +65,7 @@ __device__ __forceinline__ int64_t top_bit(CPtr S, int n) {
 }
 
 // any bit of S in [0, q) set?
-__device__ __forceinline__ bool any_below(CPtr S, int n, int64_t q) {
+static __device__ __forceinline__ bool any_below(CPtr S, int n, int64_t q) {
   if (q <= 0) return false;
   int64_t full = q >> 5;
   for (int64_t k = 0; k < full && k < n; k++)
@@ -84,7 +84,7 @@ struct RoundOut {
 // sticky tail (true value in (S, S+1) units when sticky) to p bits, ties to
 // even.  Writes the left-aligned L-limb mantissa to `out`.  `base` is the
 // exponent of S's LSB: value = S * 2^base.  Returns the MPFR exponent.
-__device__ RoundOut round_big(Ptr out, int L, int p, CPtr S, int n, int64_t base, bool sticky_in) {
+static __device__ RoundOut round_big(Ptr out, int L, int p, CPtr S, int n, int64_t base, bool sticky_in) {
   int64_t hb = top_bit(S, n);
   int64_t lsb = hb - p + 1;  // bit position (in S) of the result's LSB
   bool rbit = false, sticky = sticky_in;
@@ -132,7 +132,7 @@ __device__ RoundOut round_big(Ptr out, int L, int p, CPtr S, int n, int64_t base
 }
 
 // P (2L limbs) = A * B, full schoolbook with 64-bit accumulation
-__device__ void mul_full(Ptr P, CPtr A, CPtr B, int L) {
+static __device__ void mul_full(Ptr P, CPtr A, CPtr B, int L) {
   for (int k = 0; k < 2 * L; k++) P[k] = 0;
   for (int i = 0; i < L; i++) {
     uint64_t carry = 0;
@@ -149,11 +149,11 @@ __device__ void mul_full(Ptr P, CPtr A, CPtr B, int L) {
 
 // store result: out mantissa already written; sets exp/cls with range check.
 // returns false on exponent overflow/underflow.
-__device__ __forceinline__ bool range_ok(int64_t e) { return e >= DS_EMIN && e <= DS_EMAX; }
+static __device__ __forceinline__ bool range_ok(int64_t e) { return e >= DS_EMIN && e <= DS_EMAX; }
 
 // ---------------------------------------------------------------- real mul
 // r = RN(a * b).  tmp needs 2L words.
-__device__ bool mul_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, int L, int p,
+static __device__ bool mul_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, int L, int p,
                        Ptr tmp) {
   int neg = neg_of(a.c) ^ neg_of(b.c);
   if (is_zero_cls(a.c) || is_zero_cls(b.c)) {
@@ -170,7 +170,7 @@ __device__ bool mul_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val
 }
 
 // compare |a| vs |b| for nonzero a, b: -1, 0, 1
-__device__ int cmp_abs(const Val& a, const Val& b, int L) {
+static __device__ int cmp_abs(const Val& a, const Val& b, int L) {
   if (a.e != b.e) return a.e > b.e ? 1 : -1;
   for (int l = L - 1; l >= 0; l--) {
     uint32_t x = a.m[l], y = b.m[l];
@@ -179,14 +179,14 @@ __device__ int cmp_abs(const Val& a, const Val& b, int L) {
   return 0;
 }
 
-__device__ __forceinline__ void copy_val(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, int L, int neg) {
+static __device__ __forceinline__ void copy_val(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, int L, int neg) {
   for (int l = 0; l < L; l++) rm[l] = a.m[l];
   *re = (int32_t)a.e;
   *rc = is_zero_cls(a.c) ? a.c : nz_cls(neg);
 }
 
 // r = RN(a + (-1)^sub_b * b).  tmp needs 2L + 3 words.
-__device__ bool add_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, bool negate_b,
+static __device__ bool add_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, bool negate_b,
                        int L, int p, Ptr tmp) {
   int na = neg_of(a.c), nb = neg_of(b.c) ^ (negate_b ? 1 : 0);
   bool za = is_zero_cls(a.c), zb = is_zero_cls(b.c);
@@ -216,7 +216,7 @@ __device__ bool add_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val
     return true;
   }
   // S = MX * 2^d +- MY, in n = L + ceil(d/32) + 1 limbs
-  int dl = (int)(d >> 5), db = (int)(d & 31);
+  int dl = (int)(d >> 5);
   int n = L + dl + 2;
   // X shifted left by d bits
   for (int k = 0; k < n; k++) {
@@ -238,7 +238,7 @@ __device__ bool add_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val
       tmp[k] = (uint32_t)(t + (borrow << 32));
     }
   }
-  (void)db;
+
   RoundOut ro = round_big(rm, L, p, CPtr{tmp.p, tmp.s}, n, Y.e - 32 * (int64_t)L, false);
   *re = (int32_t)ro.e;
   *rc = nz_cls(nx);
@@ -249,7 +249,7 @@ __device__ bool add_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val
 // U: nu limbs (modified in place to hold the remainder in its low nv limbs),
 // V: nv limbs with the MSB of V[nv-1] set (normalized), nu > nv.
 // Q: nu - nv limbs.  Returns true if the remainder is nonzero.
-__device__ bool divrem_norm(Ptr Q, Ptr U, int nu, CPtr V, int nv) {
+static __device__ bool divrem_norm(Ptr Q, Ptr U, int nu, CPtr V, int nv) {
   uint64_t vtop = V[nv - 1];
   uint64_t vnext = nv >= 2 ? V[nv - 2] : 0;
   for (int j = nu - nv - 1; j >= 0; j--) {
@@ -292,7 +292,7 @@ __device__ bool divrem_norm(Ptr Q, Ptr U, int nu, CPtr V, int nv) {
 }
 
 // r = RN(a / b), b != 0.  tmp needs 3L + 8 words.
-__device__ bool div_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, int L, int p,
+static __device__ bool div_rn(Ptr rm, int32_t* re, uint8_t* rc, const Val& a, const Val& b, int L, int p,
                        Ptr tmp) {
   int neg = neg_of(a.c) ^ neg_of(b.c);
   if (is_zero_cls(a.c)) {
@@ -344,7 +344,7 @@ struct XSum {
 // out needs nx + ny + win_bits/32 + 4 words.  Zero terms: IEEE zero-sum
 // rules (x + y of signed zeros is -0 only if both are -0; exact nonzero
 // cancellation gives +0).
-__device__ XSum exact_sum(Ptr out, XTerm X, XTerm Y, bool subY, int64_t win_bits) {
+static __device__ XSum exact_sum(Ptr out, XTerm X, XTerm Y, bool subY, int64_t win_bits) {
   XSum r;
   r.pert = 0;
   int sx = X.neg, sy = Y.neg ^ (subY ? 1 : 0);
@@ -407,7 +407,7 @@ __device__ XSum exact_sum(Ptr out, XTerm X, XTerm Y, bool subY, int64_t win_bits
 }
 
 // round an XSum to p bits (value = S * 2^base, perturbation-aware)
-__device__ bool round_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr S, const XSum& x, int L, int p) {
+static __device__ bool round_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr S, const XSum& x, int L, int p) {
   if (x.zero) {
     for (int l = 0; l < L; l++) rm[l] = 0;
     *re = 0;
@@ -431,7 +431,7 @@ __device__ bool round_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr S, const XSum& 
   return range_ok(ro.e);
 }
 
-__device__ __forceinline__ XTerm prod_term(Ptr P, const Val& A, const Val& B, int L) {
+static __device__ __forceinline__ XTerm prod_term(Ptr P, const Val& A, const Val& B, int L) {
   XTerm t;
   t.neg = neg_of(A.c) ^ neg_of(B.c);
   t.zero = is_zero_cls(A.c) || is_zero_cls(B.c);
@@ -443,7 +443,7 @@ __device__ __forceinline__ XTerm prod_term(Ptr P, const Val& A, const Val& B, in
 }
 
 // r = RN(A*B -/+ C*D): one component of mpc_mul.  tmp: 8L + 8 words.
-__device__ bool cmul_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& A, const Val& B, const Val& C,
+static __device__ bool cmul_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& A, const Val& B, const Val& C,
                           const Val& D, bool sub, int L, int p, Ptr tmp) {
   XTerm x = prod_term(tmp, A, B, L);
   XTerm y = prod_term(tmp.off(2 * L), C, D, L);
@@ -456,7 +456,7 @@ __device__ bool cmul_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& A, const 
 
 // q = RN(N / D) for exact sums N (numerator) and D > 0.  Writes rm/re/rc.
 // tmp: nN + nD + (p+2)/32 + 8 words (U, Q).
-__device__ bool div_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr N, XSum xn, Ptr D, XSum xd, int L,
+static __device__ bool div_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr N, XSum xn, Ptr D, XSum xd, int L,
                          int p, Ptr tmp, unsigned int* warn) {
   if (xn.zero) {
     for (int l = 0; l < L; l++) rm[l] = 0;
@@ -513,22 +513,22 @@ __device__ bool div_xsum(Ptr rm, int32_t* re, uint8_t* rc, Ptr N, XSum xn, Ptr D
 }
 
 // window (in bits) inside which complex-division sums are kept exact
-__device__ __forceinline__ int64_t cdiv_window(int p) { return 4 * (int64_t)p + 64; }
+static __device__ __forceinline__ int64_t cdiv_window(int p) { return 4 * (int64_t)p + 64; }
 
 // limbs of one exact-sum window in cdiv_part (terms of 2L limbs, gap <= win)
-__host__ __device__ __forceinline__ int cdiv_nwin(int L, int p) {
+static __host__ __device__ __forceinline__ int cdiv_nwin(int L, int p) {
   return 4 * L + (int)((4 * (int64_t)p + 64) / 32) + 6;
 }
 
 // scratch words needed by cdiv_part: 4 products (8L) + N, D windows +
 // U (<= nwin + L + 3) + Q (<= nwin + L)
-__host__ __device__ __forceinline__ int64_t cdiv_scratch_words(int L, int p) {
+static __host__ __device__ __forceinline__ int64_t cdiv_scratch_words(int L, int p) {
   return 8 * (int64_t)L + 4 * (int64_t)cdiv_nwin(L, p) + 2 * (int64_t)L + 64;
 }
 
 // One component of mpc_div:  re: (ar*br + ai*bi) / (br^2 + bi^2)
 //                            im: (ai*br - ar*bi) / (br^2 + bi^2)
-__device__ bool cdiv_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& ar, const Val& ai, const Val& br,
+static __device__ bool cdiv_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& ar, const Val& ai, const Val& br,
                           const Val& bi, bool imag, int L, int p, Ptr tmp, unsigned int* warn) {
   int64_t win = cdiv_window(p);
   int nwin = cdiv_nwin(L, p);

@@ -142,6 +142,28 @@ class DeviceElimination:
         _check(self.lib.ds_results_fetch(self.ctx, upto, ctypes.byref(r)), self.ctx, "ds_results_fetch",
                self.rank)
 
+    def snapshot(self, save: bool):
+        """save=True: keep a device copy of this rank's rows; save=False:
+        restore it and reset the run state (resident re-runs)."""
+        _check(self.lib.ds_snapshot(self.ctx, int(save)), self.ctx, "ds_snapshot", self.rank)
+
+    def run_resident(self, collect_minors: bool, series: bool, start: int, stop: int):
+        """Steps [start, stop) with results left in HBM (no D2H)."""
+        done = ctypes.c_int(0)
+        rc = self.lib.ds_run(self.ctx, int(collect_minors), int(series), start, stop, None, ctypes.byref(done))
+        _check(rc, self.ctx, "ds_run", self.rank)
+        return rc, done.value
+
+    def profile(self, enable: bool):
+        self.lib.ds_profile(self.ctx, int(enable))
+
+    def profile_read(self):
+        """(update kernel ms, launches, schoolbook limb-MACs) since the last read."""
+        ms, n, w = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _check(self.lib.ds_profile_read(self.ctx, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(w)), self.ctx,
+               "ds_profile_read", self.rank)
+        return ms.value, n.value, w.value
+
     def stream(self) -> int:
         return self.lib.ds_stream(self.ctx) or 0
 
