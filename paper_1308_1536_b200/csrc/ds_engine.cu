@@ -22,6 +22,7 @@
 
 #include "ds_mp.cuh"
 #include "ds_update.cuh"
+#include "ds_warpdiv.cuh"
 
 using namespace ds;
 
@@ -72,6 +73,8 @@ struct ds_ctx {
   // fused update engine workspace
   UpdatePlan plan;
   int64_t launches;
+  int host_have_det;   // a det chain value exists (first step sets det = piv)
+  int det_from_cur;    // next det product reads the ds_set_det seed in `cur`
   std::string err;
 };
 
@@ -208,20 +211,26 @@ __device__ __forceinline__ Ptr thread_scratch(const KArgs& k, int64_t tid) {
   return Ptr{k.scratch + tid, k.scratch_threads};
 }
 
-// owner stages its row i into the pivot buffer
+// owner stages its row i into the pivot buffer: one thread per (component,
+// limb plane, column), coalesced along the row
 __global__ void k_stage(KArgs k, int i) {
   if (k.status[0] >= 0) return;
   int64_t jl = i / k.world;
   PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
-  int64_t tot = (int64_t)k.ncomp * k.n;
+  int64_t planes = (int64_t)k.ncomp * (k.L + 2);  // L limb planes + exp + cls per component
+  int64_t tot = planes * k.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(t / k.n);
     int col = (int)(t % k.n);
+    int64_t pl = t / k.n;
+    int c = (int)(pl / (k.L + 2));
+    int l = (int)(pl % (k.L + 2));
     int64_t src = jl * k.n + col;
-    for (int l = 0; l < k.L; l++)
+    if (l < k.L)
       pb.limbs[((int64_t)c * k.L + l) * k.n + col] = k.a_limbs[((int64_t)c * k.L + l) * k.a_count + src];
-    pb.exp[(int64_t)c * k.n + col] = k.a_exp[(int64_t)c * k.a_count + src];
-    pb.cls[(int64_t)c * k.n + col] = k.a_cls[(int64_t)c * k.a_count + src];
+    else if (l == k.L)
+      pb.exp[(int64_t)c * k.n + col] = k.a_exp[(int64_t)c * k.a_count + src];
+    else
+      pb.cls[(int64_t)c * k.n + col] = k.a_cls[(int64_t)c * k.a_count + src];
   }
 }
 
@@ -431,6 +440,146 @@ __global__ void k_scalar_op(int op, int kind, int L, int p, int64_t count, const
   }
 }
 
+// ---------------------------------------------------------------- warp division
+// q = RN(a / b) for real scalars, one warp per quotient (ds_warpdiv.cuh).
+// smem per warp: V (L) | U (nu + 32K) | Q (nu - L), nu = L + kq + 1.
+__host__ __device__ static inline int wdiv_kq(int p) { return (p + 2 + 31) / 32; }
+__host__ __device__ static inline int wdiv_words(int L, int p, int K) {
+  int nu = L + wdiv_kq(p) + 1;
+  return L + (nu + 32 * K) + (nu - L) + 4;
+}
+
+template <int K>
+__device__ void wdiv_rn(Out o, const Val& a, const Val& b, int L, int p, uint32_t* sm, int32_t* status) {
+  const int lane = threadIdx.x & 31;
+  int neg = neg_of(a.c) ^ neg_of(b.c);
+  if (is_zero_cls(a.c)) {
+    for (int l = lane; l < L; l += 32) o.m[l] = 0u;
+    if (lane == 0) {
+      *o.e = 0;
+      *o.c = zero_cls(neg);
+    }
+    return;
+  }
+  const int kq = wdiv_kq(p);
+  const int nu = L + kq + 1;
+  uint32_t* V = sm;
+  uint32_t* U = V + L;
+  uint32_t* Q = U + nu + 32 * K;
+  for (int l = lane; l < L; l += 32) V[l] = b.m[l];
+  for (int k = lane; k < nu + 32 * K; k += 32) U[k] = (k >= kq && k < kq + L) ? a.m[k - kq] : 0u;
+  uint32_t vb[K];
+#pragma unroll
+  for (int u = 0; u < K; u++) {
+    int l = lane * K + u;
+    vb[u] = l < L ? b.m[l] : 0u;
+  }
+  __syncwarp();
+  bool rem = dsw::wdivrem<K>(Q, U, nu, V, vb, L);
+  __syncwarp();
+  int64_t e = dsw::wround(Q, nu - L, rem, a.e - b.e - 32 * (int64_t)kq, L, p, o.m.p, o.m.s);
+  if (lane == 0) {
+    *o.e = (int32_t)e;
+    *o.c = nz_cls(neg);
+    if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&status[2], 1);
+  }
+}
+
+template <int K>
+__global__ void k_mult_w(KArgs k, int i, int jl0, int wwords) {
+  extern __shared__ uint32_t wsm[];
+  if (k.status[0] >= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= k.nloc - jl0) return;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Val b = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  int64_t jl = jl0 + r;
+  int64_t idx = jl * k.n + i;
+  Val a = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+  Out z = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 0, k.L, jl);
+  wdiv_rn<K>(z, a, b, k.L, k.p, wsm + warp * wwords, k.status);
+  __syncwarp();
+  __threadfence_block();
+  // a_ji <- -z_j (elim.py:53)
+  Val zv = val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, 0, k.L, jl);
+  Out ao = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+  for (int l = lane; l < k.L; l += 32) ao.m[l] = zv.m[l];
+  if (lane == 0) {
+    *ao.e = (int32_t)zv.e;
+    uint8_t c = zv.c;
+    *ao.c = (c == DS_CLS_POS) ? DS_CLS_NEG : (c == DS_CLS_NEG) ? DS_CLS_POS : (c == DS_CLS_PZERO) ? DS_CLS_NZERO : DS_CLS_PZERO;
+  }
+}
+
+template <int K>
+__global__ void k_emit_norm_w(KArgs k, int i, int wwords) {
+  extern __shared__ uint32_t wsm[];
+  if (k.status[0] >= 0) return;
+  const int warp = threadIdx.x >> 5;
+  int m = i + 2;
+  int64_t jl = (i + 1) / k.world;
+  const int64_t kk = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
+  bool lead_zero = is_zero_cls(l0.c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
+  if (lead_zero || kk >= m) return;
+  int64_t idx = jl * k.n + kk;
+  Val s = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
+  Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, 0, k.L, idx);
+  wdiv_rn<K>(o, s, l0, k.L, k.p, wsm + warp * wwords, k.status);
+}
+
+// first step: det = piv (unrounded, elim.py:214); pivots[i] = piv; zero test
+__global__ void k_pivot_lite(KArgs k, int i, int first) {
+  if (k.status[0] >= 0) return;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Val p0 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  Val p1 = k.kind == DS_KIND_COMPLEX ? val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, i) : p0;
+  bool zero = is_zero_cls(p0.c) && (k.kind == DS_KIND_REAL || is_zero_cls(p1.c));
+  __syncthreads();
+  if (zero) {
+    if (threadIdx.x == 0) k.status[0] = i;
+    return;
+  }
+  for (int c = 0; c < k.ncomp; c++) {
+    Val pv = val_at(pb.limbs, pb.exp, pb.cls, k.n, c, k.L, i);
+    Out o = out_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, c, k.L, i);
+    Out d = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, c, k.L, i);
+    for (int l = threadIdx.x; l < k.L; l += blockDim.x) {
+      o.m[l] = pv.m[l];
+      if (first) d.m[l] = pv.m[l];
+    }
+    if (threadIdx.x == 0) {
+      *o.e = (int32_t)pv.e;
+      *o.c = pv.c;
+      if (first) {
+        *d.e = (int32_t)pv.e;
+        *d.c = pv.c;
+      }
+    }
+  }
+}
+
+// sig_{m-1} = det_i (elim.py:60)
+__global__ void k_emit_last(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int64_t jl = (i + 1) / k.world;
+  int64_t idx = jl * k.n + (i + 1);
+  for (int c = 0; c < k.ncomp; c++) {
+    Val d = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, c, k.L, i);
+    Out o = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, c, k.L, idx);
+    for (int l = threadIdx.x; l < k.L; l += blockDim.x) o.m[l] = d.m[l];
+    if (threadIdx.x == 0) {
+      *o.e = (int32_t)d.e;
+      *o.c = d.c;
+    }
+  }
+}
+
+// copy the seed det (ds_set_det) into det[i-1]'s role: det[i] = RN(seed * piv)
+// is computed by mul_row_launch directly from `cur`.
+
 // ---------------------------------------------------------------- host side
 static int64_t general_scratch_words(int L, int kind) {
   int64_t w = 8 * (int64_t)L + 64;                        // real div / mul / add
@@ -604,6 +753,8 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
                          n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
   }
   // reset run state
+  ctx->host_have_det = 0;
+  ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
   int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
@@ -650,7 +801,9 @@ int ds_pivot_stage(ds_ctx* ctx, int i) {
   if (i < 0 || i >= ctx->n || i % ctx->world != ctx->rank) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
   KArgs k = kargs(ctx);
-  int g = (int)(((int64_t)ctx->ncomp * ctx->n + 255) / 256);
+  int64_t tot = (int64_t)ctx->ncomp * (ctx->L + 2) * ctx->n;
+  int g = (int)((tot + 255) / 256);
+  if (g > 148 * 16) g = 148 * 16;
   k_stage<<<g, 256, 0, ctx->stream>>>(k, i);
   ctx->launches++;
   CK(cudaGetLastError());
@@ -667,13 +820,78 @@ static bool force_general() {
   return g_force_general == 1;
 }
 
+static int warp_k(int L) {
+  int K = 1;
+  while (32 * K < L) K *= 2;
+  return K;
+}
+
+#define WDIV_DISPATCH(K_, KERNEL, grid, block, smem, s, ...)                 \
+  switch (K_) {                                                              \
+    case 1: KERNEL<1><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
+    case 2: KERNEL<2><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
+    case 4: KERNEL<4><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
+    case 8: KERNEL<8><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
+    case 16: KERNEL<16><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    default: KERNEL<32><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+  }
+
+static bool fast_real(ds_ctx* ctx) {
+  return ctx->kind == DS_KIND_REAL && ctx->plan.enabled && !force_general() && ctx->L <= 1024;
+}
+
+static void set_wdiv_attrs(int maxsm) {
+  static bool done = false;
+  if (done) return;
+  done = true;
+#define SA(KERNEL) \
+  cudaFuncSetAttribute(KERNEL<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  SA(k_mult_w)
+  SA(k_emit_norm_w)
+#undef SA
+}
+
 int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   if (i < 0 || i >= ctx->n) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
   KArgs k = kargs(ctx);
   cudaStream_t s = ctx->stream;
-  k_pivot<<<1, 32, 0, s>>>(k, i);
-  ctx->launches++;
+  const bool fast = fast_real(ctx);
+  const int L = ctx->L, n = ctx->n;
+  const int K = warp_k(L);
+  const int wwords = wdiv_words(L, ctx->p, K);
+  const int wpb = 4;  // warps per block for the division kernels
+  if (fast) {
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    set_wdiv_attrs(maxsm);
+  }
+  PB pb = pb_view(ctx->pbuf, n, L, ctx->ncomp);
+  // ---- pivot: zero test, pivots[i], det chain (elim.py:209-215)
+  if (fast) {
+    int first = ctx->host_have_det ? 0 : 1;
+    k_pivot_lite<<<1, 128, 0, s>>>(k, i, first);
+    ctx->launches++;
+    if (!first) {
+      const uint32_t* xl = ctx->det_from_cur ? ctx->cur_limbs : ctx->det_limbs + (i - 1);
+      int64_t xc = ctx->det_from_cur ? 1 : n;
+      const int32_t* xe = ctx->det_from_cur ? ctx->cur_exp : ctx->det_exp + (i - 1);
+      const uint8_t* xk = ctx->det_from_cur ? ctx->cur_cls : ctx->det_cls + (i - 1);
+      int rc = mul_row_launch(&ctx->plan, s, xl, xc, xe, xk, pb.limbs + i, n, pb.exp + i, pb.cls + i, 1,
+                              ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i, ctx->status, &ctx->launches);
+      if (rc != DS_OK) { ctx->err = "det product launch failed"; return rc; }
+    }
+  } else {
+    k_pivot<<<1, 32, 0, s>>>(k, i);
+    ctx->launches++;
+  }
+  ctx->host_have_det = 1;
+  ctx->det_from_cur = 0;
   int jl0 = first_local_after(i, ctx->rank, ctx->world);
   int nrows = ctx->nloc - jl0;
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
@@ -690,22 +908,30 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     ctx->prof_used += 2;
   }
   if (nrows > 0) {
-    k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
+    // ---- multipliers z_j = RN(a_ji / piv), a_ji <- -z_j (elim.py:47, 53)
+    if (fast) {
+      int blocks = (nrows + wpb - 1) / wpb;
+      size_t smem = (size_t)wpb * wwords * 4;
+      WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords);
+    } else {
+      k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
+    }
     ctx->launches++;
-    int ncols_u = collect_minors ? ctx->n - 1 : ctx->n - 1 - i;
+    // ---- update of the trailing rows (elim.py:49-52)
+    int ncols_u = collect_minors ? n - 1 : n - 1 - i;
     if (pe0) {
       CK(cudaEventRecord(pe0, s));
       ctx->prof_launches++;
-      ctx->prof_work += (double)nrows * ncols_u * (double)ctx->L * ctx->L * (ctx->kind == DS_KIND_COMPLEX ? 4.0 : 1.0);
+      ctx->prof_work += (double)nrows * ncols_u * (double)L * L * (ctx->kind == DS_KIND_COMPLEX ? 4.0 : 1.0);
     }
-    if (ctx->kind == DS_KIND_REAL && ctx->plan.enabled && !force_general()) {
-      int rc = update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf, ctx->z_limbs,
-                             ctx->z_exp, ctx->z_cls, ctx->nloc, ctx->n, i, jl0, collect_minors, ctx->status,
-                             &ctx->launches);
+    if (fast) {
+      int rc = update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
+                             ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
+                             ctx->status, &ctx->launches);
       if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
     } else {
       int kfirst = collect_minors ? 0 : i + 1;
-      int64_t ncols = ctx->n - kfirst - (collect_minors ? 1 : 0);
+      int64_t ncols = n - kfirst - (collect_minors ? 1 : 0);
       if (ncols > 0) {
         k_update_general<<<grid_for(ctx, nrows * ncols, 128), 128, 0, s>>>(k, i, jl0, collect_minors);
         ctx->launches++;
@@ -713,12 +939,27 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     }
     if (pe1) CK(cudaEventRecord(pe1, s));
   }
-  if (collect_minors && i + 1 < ctx->n) {
+  // ---- minors of leading size m = i+2 (elim.py:220-226)
+  if (collect_minors && i + 1 < n) {
     int m = i + 2;
-    if ((series || m == ctx->n) && (i + 1) % ctx->world == ctx->rank) {
-      k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
-      k_emit_norm<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
-      ctx->launches += 2;
+    if ((series || m == n) && (i + 1) % ctx->world == ctx->rank) {
+      int64_t jl = (i + 1) / ctx->world;
+      if (fast) {
+        int rc = mul_row_launch(&ctx->plan, s, ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i,
+                                ctx->a_limbs + jl * n, ctx->a_count, ctx->a_exp + jl * n, ctx->a_cls + jl * n, i + 1,
+                                ctx->sig_limbs + jl * n, ctx->a_count, ctx->sig_exp + jl * n, ctx->sig_cls + jl * n,
+                                ctx->status, &ctx->launches);
+        if (rc != DS_OK) { ctx->err = "minor product launch failed"; return rc; }
+        k_emit_last<<<1, 128, 0, s>>>(k, i);
+        int blocks = (m + wpb - 1) / wpb;
+        size_t smem = (size_t)wpb * wwords * 4;
+        WDIV_DISPATCH(K, k_emit_norm_w, blocks, 32 * wpb, smem, s, k, i, wwords);
+        ctx->launches += 2;
+      } else {
+        k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
+        k_emit_norm<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
+        ctx->launches += 2;
+      }
     }
   }
   CK(cudaGetLastError());
@@ -746,6 +987,8 @@ int ds_snapshot(ds_ctx* ctx, int save) {
   CK(cudaMemcpyAsync(ctx->a_limbs, ctx->snap_limbs, lb, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->a_exp, ctx->snap_exp, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->a_cls, ctx->snap_cls, cb, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->host_have_det = 0;
+  ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, ctx->n, ctx->stream));
   CK(cudaMemsetAsync(ctx->status + 1, 0, 7 * sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->status, 0xff, sizeof(int32_t), ctx->stream));  // -1
@@ -801,6 +1044,8 @@ int ds_set_det(ds_ctx* ctx, const ds_soa* d) {
   }
   int one = 1;
   CK(cudaMemcpyAsync(ctx->status + 1, &one, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->host_have_det = 1;
+  ctx->det_from_cur = 1;
   CK(cudaStreamSynchronize(ctx->stream));
   return DS_OK;
 }

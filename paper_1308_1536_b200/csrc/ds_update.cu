@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 #include <string>
 
 #include "../../include/detseries_b200.h"
@@ -53,82 +54,124 @@ constexpr int FLUSH = 64;     // s-steps between carry flushes (64 * 2^46 < 2^53
 constexpr double R24 = 1.0 / 16777216.0;
 constexpr double B24 = 16777216.0;
 
+// Generic fused product / update over a tile of (rows r) x (columns c):
+//   mode 0 (update): out[r,c] <- RN(out[r,c] - RN(z_r * b_c))   (elim.py:50-52)
+//   mode 1 (mul)   : out[r,c] <- RN(z_r * b_c)                  (elim.py:59, 214)
+// z_r: digits zdig[r*Db + s], meta zexp/zcls/zf[r]
+// b_c: column k = bmap(c): digits bdig[s*bstride + k], meta bexp/bcls/bf[k]
+// out: element index (orow0 + r) * ostride + ocol(c), limb planes o_count apart
 struct UArgs {
-  int p, L, Db, zb, n, i, jl0, nrows, ncols, collect_minors;
+  int p, L, Db, zb, mode;
+  int nrows, ncols;
   int c_lo, cmax, eps;
-  uint32_t* a_limbs;
-  int32_t* a_exp;
-  uint8_t* a_cls;
-  int64_t a_count;
-  const double* zdig;  // [nloc][Db]
-  const double* bdig;  // [Db][n]
-  const double* zf;    // [nloc] leading 64 bits of z as a double in [1,2)
-  const double* bf;    // [n]
-  const int32_t* z_exp;
-  const uint8_t* z_cls;
-  const int32_t* b_exp;
-  const uint8_t* b_cls;
+  const double* zdig;
+  const double* zf;
+  const int32_t* zexp;
+  const uint8_t* zcls;
+  const double* bdig;
+  const double* bf;
+  const int32_t* bexp;
+  const uint8_t* bcls;
+  int64_t bstride;
+  int col_off;   // k = c + col_off
+  int skip_col;  // column k == skip_col is left untouched (the pivot column)
+  int ocol_off;  // output column = (o_same ? k : c + ocol_off)
+  int o_same;
+  uint32_t* o_limbs;
+  int32_t* o_exp;
+  uint8_t* o_cls;
+  int64_t o_count, ostride, orow0;
   int32_t* status;
 };
 
-__device__ __forceinline__ int map_col(const UArgs& a, int c) {
-  if (!a.collect_minors) return a.i + 1 + c;
-  return c < a.i ? c : c + 1;
+__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
+  unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc));
+}
+// 8-byte async copy with zero fill when !valid (src-size 0)
+__device__ __forceinline__ void cp_async8z(double* smem_dst, const double* gsrc, bool valid) {
+  unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(n));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 // ------------------------------------------------------------ prep kernels
-// Balanced radix-2^24 digits of the p-bit integer mantissa m = M >> (32L-p),
-// d_s in [-2^23, 2^23), m = sum d_s 2^(24 s), Db = ceil(p/24) + 1 digits.
-__global__ void k_prep_digits(const uint32_t* limbs, int64_t count, int64_t first, int64_t num, int L, int p,
-                              int Db, double* dig, int64_t es, int64_t ds, double* topf) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= num) return;
-  int64_t idx = first + e;
-  ds::CPtr M{limbs + idx, count};
-  int zb = 32 * L - p;
-  int ndig = (p + 23) / 24;
-  int carry = 0;
-  for (int s = 0; s < Db; s++) {
-    int v = carry;
-    if (s < ndig) {
-      uint32_t u = ds::bits32(M, L, (int64_t)24 * s + zb) & 0xFFFFFFu;
-      if (24 * s + 24 > p) u &= (1u << (p - 24 * s)) - 1u;
-      v += (int)u;
-    }
-    carry = 0;
-    if (v >= (1 << 23)) {
-      v -= (1 << 24);
-      carry = 1;
-    }
-    dig[idx * es + (int64_t)s * ds] = (double)v;
+// Balanced radix-2^24 digits of the p-bit integer mantissa m = M >> (32L-p):
+// with u_s the unsigned 24-bit digits and c_s = [u_{s-1} >= 2^23],
+//     d_s = u_s + c_s - 2^24 [u_s >= 2^23]   in [-2^23, 2^23],
+// which telescopes to sum d_s 2^(24s) = m with no carry chain, so every
+// digit is computed independently (one thread per (element, digit)).
+// Element e (limbs src[e + l*count]) -> dig[e*es + s*ds]; topf[e] = leading
+// 64 bits as a double in [1, 2).
+__device__ __forceinline__ uint32_t udigit(ds::CPtr M, int L, int p, int zb, int s) {
+  if (s < 0 || 24 * s >= p) return 0u;
+  return ds::bits32(M, L, (int64_t)24 * s + zb) & 0xFFFFFFu;
+}
+
+__global__ void k_prep_digits(const uint32_t* src, int64_t count, int64_t num, int L, int p, int Db, double* dig,
+                              int64_t es, int64_t ds_, double* topf) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= num * Db) return;
+  // consecutive threads -> consecutive elements when ds_ == 1 is not the
+  // layout: choose the mapping that makes the digit stores coalesced
+  int64_t e, s;
+  if (es == 1) {  // dig[s*ds + e]: element-fastest
+    e = t % num;
+    s = t / num;
+  } else {        // dig[e*es + s]: digit-fastest
+    e = t / Db;
+    s = t % Db;
   }
-  uint64_t top = ((uint64_t)M[L - 1] << 32) | M[L - 2];
-  topf[idx] = (double)top * 0x1p-63;
+  ds::CPtr M{src + e, count};
+  int zb = 32 * L - p;
+  uint32_t u = udigit(M, L, p, zb, (int)s);
+  uint32_t up = udigit(M, L, p, zb, (int)s - 1);
+  int d = (int)u + (up >= (1u << 23) ? 1 : 0) - (u >= (1u << 23) ? (1 << 24) : 0);
+  dig[e * es + s * ds_] = (double)d;
+  if (s == 0) {
+    uint64_t top = ((uint64_t)M[L - 1] << 32) | M[L - 2];
+    topf[e] = (double)top * 0x1p-63;
+  }
+}
+
+static inline void prep_launch(const uint32_t* src, int64_t count, int64_t num, int L, int p, int Db, double* dig,
+                               int64_t es, int64_t ds_, double* topf, cudaStream_t s) {
+  int64_t tot = num * Db;
+  k_prep_digits<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(src, count, num, L, p, Db, dig, es, ds_, topf);
 }
 
 // ------------------------------------------------------------ S window
-// Exact aligned sum S = |X| -/+ |Y| of a and t on a window of L+2 limbs:
-// limb 0 = guard (register), limbs 1..L = a's own slots (in place), limb L+1
-// = carry (register).  X is the operand with the larger exponent, anchored at
-// limbs 1..L; Y is shifted right by dq limbs + dr bits; Y bits below the
-// window become the sticky bit (effective subtraction borrows 1 ulp-of-guard
-// when sticky, the standard round/sticky trick).
+// Exact aligned sum S = |X| -/+ |Y| of a and t on a window of L+2 limbs held
+// in SHARED memory (limb w at S[w*nth]): limb 0 = guard, limbs 1..L = X's
+// mantissa positions, limb L+1 = carry.  a's limbs were prefetched into
+// limbs 1..L with cp.async while the product ran.  X is the operand with the
+// larger exponent; Y is shifted right by dq limbs + dr bits; Y bits below the
+// window become the sticky bit (effective subtraction borrows one guard ulp
+// when sticky -- the standard round/sticky trick).
 struct SWin {
-  uint32_t* A;
-  int64_t st;
+  uint32_t* S;
+  int nth;
   int L;
-  bool xa;      // X = a (Y = t) or X = t (Y = a)
-  bool sub;     // effective subtraction
-  bool yzero;   // Y == 0 (a == 0)
+  bool xa;     // X = a (Y = t) or X = t (Y = a)
+  bool sub;    // effective subtraction
+  bool yzero;  // Y == 0 (a == 0, or a pure product)
   int dq, dr;
   uint32_t prev;
   int q, w;
-  uint32_t S0, SL1;
   uint32_t cb;
   bool sticky;
   uint32_t curA;
 
-  __device__ __forceinline__ uint32_t aload(int l) const { return (l >= 0 && l < L) ? A[(int64_t)l * st] : 0u; }
+  __device__ __forceinline__ uint32_t get(int wi) const {
+    return (wi >= 0 && wi <= L + 1) ? S[wi * nth] : 0u;
+  }
+  __device__ __forceinline__ void set(int wi, uint32_t v) { S[wi * nth] = v; }
+  // a limb l (0 <= l < L) lives in window slot l + 1 until overwritten
+  __device__ __forceinline__ uint32_t aload(int l) const { return (l >= 0 && l < L) ? S[(l + 1) * nth] : 0u; }
 
   __device__ __forceinline__ void emit(uint32_t X, uint32_t Yb) {
     uint32_t s;
@@ -141,45 +184,43 @@ struct SWin {
       s = (uint32_t)t;
       cb = (uint32_t)(t >> 32);
     }
-    if (w == 0) S0 = s;
-    else if (w == L + 1) SL1 = s;
-    else A[(int64_t)(w - 1) * st] = s;
+    S[w * nth] = s;
     w++;
   }
 
   __device__ __forceinline__ uint32_t abits(int wi) {
-    // Y = a:  window limb wi <- a bits [32(wi-1+dq)+dr, +32)
     uint32_t nxt = aload(wi + dq);
     uint32_t v = dr ? ((curA >> dr) | (nxt << (32 - dr))) : curA;
     curA = nxt;
     return v;
   }
 
-  __device__ void init(uint32_t* A_, int64_t st_, int L_, bool xa_, bool sub_, bool yzero_, int64_t shift) {
-    A = A_; st = st_; L = L_; xa = xa_; sub = sub_; yzero = yzero_;
-    if (shift > 32 * (int64_t)(L + 3)) shift = 32 * (int64_t)(L + 3);  // all of Y below the window
+  __device__ void init(int L_, bool xa_, bool sub_, bool yzero_, int64_t shift) {
+    L = L_; xa = xa_; sub = sub_; yzero = yzero_;
+    if (shift > 32 * (int64_t)(L + 3)) shift = 32 * (int64_t)(L + 3);
     dq = (int)(shift >> 5);
     dr = (int)(shift & 31);
-    prev = 0; q = 0; w = 0; S0 = 0; SL1 = 0; cb = 0; sticky = false; curA = 0;
-    if (!xa) {
-      if (yzero) {
-        emit(0u, 0u);
-        return;
-      }
-      // sticky: a bits [0, 32(dq-1)+dr)
-      int64_t below = 32 * (int64_t)(dq - 1) + dr;
-      for (int l = 0; l < L && (int64_t)l * 32 < below; l++) {
-        uint32_t v = aload(l);
-        int64_t lim = below - 32 * (int64_t)l;
-        if (lim < 32) v &= (1u << lim) - 1u;
-        if (v) sticky = true;
-      }
-      curA = aload(dq - 1);
-      emit(0u, abits(0));
+    prev = 0; q = 0; w = 0; cb = 0; sticky = false; curA = 0;
+    if (xa) {
+      S[0] = 0u;
+      S[(L + 1) * nth] = 0u;
+      return;
     }
+    if (yzero) {
+      emit(0u, 0u);
+      return;
+    }
+    int64_t below = 32 * (int64_t)(dq - 1) + dr;  // a bits [0, below) are under the window
+    for (int l = 0; l < L && (int64_t)l * 32 < below; l++) {
+      uint32_t v = aload(l);
+      int64_t lim = below - 32 * (int64_t)l;
+      if (lim < 32) v &= (1u << lim) - 1u;
+      if (v) sticky = true;
+    }
+    curA = aload(dq - 1);
+    emit(0u, abits(0));
   }
 
-  // next limb of t (T_0 .. T_{L-1} left-aligned mantissa, then T_L = overflow)
   __device__ __forceinline__ void push(uint32_t T) {
     if (xa) {
       int wq = q - dq;
@@ -188,14 +229,12 @@ struct SWin {
       } else {
         if (wq == 0 && dr > 0 && (prev & ((1u << dr) - 1u))) sticky = true;
         uint32_t Yb = dr ? ((prev >> dr) | (T << (32 - dr))) : prev;
-        uint32_t X = (wq >= 1 && wq <= L) ? A[(int64_t)(wq - 1) * st] : 0u;
-        emit(X, Yb);
+        emit((wq >= 1 && wq <= L) ? S[wq * nth] : 0u, Yb);
       }
       prev = T;
       q++;
     } else {
-      uint32_t Yb = yzero ? 0u : abits(w);
-      emit(T, Yb);
+      emit(T, yzero ? 0u : abits(w));
     }
   }
 
@@ -203,119 +242,101 @@ struct SWin {
     if (xa)
       while (w <= L + 1) push(0u);
   }
-
-  __device__ __forceinline__ uint32_t get(int wi) const {
-    if (wi == 0) return S0;
-    if (wi == L + 1) return SL1;
-    if (wi < 0 || wi > L + 1) return 0u;
-    return A[(int64_t)(wi - 1) * st];
-  }
-  __device__ __forceinline__ void set(int wi, uint32_t v) {
-    if (wi == 0) S0 = v;
-    else if (wi == L + 1) SL1 = v;
-    else A[(int64_t)(wi - 1) * st] = v;
-  }
 };
 
-// ------------------------------------------------------------ digit consumers
+// ------------------------------------------------------------ limb consumers
+// The product arrives low -> high as 32-bit limbs of P (blocks of W digits
+// starting at a column c0 = 0 mod 4 are exactly 3W/4 whole limbs).
 // Top-bit probe (exact dry product): is bit 2p-1 of P set?
 struct DryTop {
   int bitpos;
   int top;
-  __device__ __forceinline__ bool digit(int c, uint32_t v) {
-    int pos = 24 * c;
-    if (bitpos >= pos && bitpos < pos + 24) top = (v >> (bitpos - pos)) & 1u;
+  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+    if ((bitpos >> 5) == g) top = (v >> (bitpos & 31)) & 1u;
     return true;
   }
   __device__ __forceinline__ bool finish(double) { return true; }
 };
 
-// Rounds P = z*b to the p-bit t and streams t's limbs into the S window.
+// Rounds P = z*b to the p-bit t (P bit r = t's LSB) and streams t's
+// left-aligned limbs T_0..T_{L-1} (+ overflow limb T_L) into the S window.
+// T_l = P bits [o + 32l, o + 32l + 32), o = r - zb, low zb bits of T_0
+// masked, the round increment added at bit zb of T_0.
 struct Emit {
   SWin* S;
-  int r, zb, p, L, cmax;
+  int r, zb, p, L, o, oq, orr;
   bool exact;
-  int lo_chk, hi_chk;  // decision region (short product)
-  bool allz, allo, sticky, decided;
-  uint32_t rbit, tcarry;
-  uint64_t buf;
-  int nb, tl;
-  bool excess;
+  int lo_chk, hi_chk;  // short-product decision region [lo_chk, hi_chk]
+  bool allz, allo, sticky, decided, excess;
+  uint32_t rbit, tcarry, prevP;
+  int tl, gtop, gn;
 
-  __device__ __forceinline__ bool digit(int c, uint32_t v) {
-    if (c > cmax) {
-      if (v) excess = true;
-      return true;
-    }
-    int pos = 24 * c;
+  __device__ __forceinline__ void setup() {
+    o = r - zb;
+    oq = o >> 5;
+    orr = o & 31;
+    prevP = 0;
+    gn = 0;
+    gtop = (r + p + 31) >> 5;  // P limbs >= gtop (and bits >= r+p) must be zero
+  }
+
+  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+    const int lo = 32 * g;
+    gn = g + 1;
     if (!decided) {
-      if (pos < r) {  // bits of this digit below r
-        int nlow = r - pos < 24 ? r - pos : 24;
-        uint32_t vl = v & ((1u << nlow) - 1u);
-        int rb = r - 1 - pos;  // round bit position inside the digit
-        if (rb >= 0 && rb < 24) rbit = (v >> rb) & 1u;
+      if (lo < r) {
+        int rb = r - 1 - lo;  // round bit inside this limb?
+        if (rb >= 0 && rb < 32) rbit = (v >> rb) & 1u;
         if (exact) {
-          uint32_t below = (rb >= 24) ? vl : (rb > 0 ? (vl & ((1u << rb) - 1u)) : 0u);
+          uint32_t below = rb >= 32 ? v : (rb > 0 ? (v & ((1u << rb) - 1u)) : 0u);
           if (below) sticky = true;
         } else {
-          int lo = pos > lo_chk ? pos : lo_chk;
-          int hi = (pos + 23) < hi_chk ? (pos + 23) : hi_chk;
-          if (hi >= lo) {
-            int len = hi - lo + 1;
-            uint32_t m = (len >= 32) ? 0xffffffffu : ((1u << len) - 1u);
-            uint32_t bits = (v >> (lo - pos)) & m;
-            if (bits != 0) allz = false;
-            if (bits != m) allo = false;
+          int a0 = lo > lo_chk ? lo : lo_chk;
+          int a1 = (lo + 31) < hi_chk ? (lo + 31) : hi_chk;
+          if (a1 >= a0) {
+            int len = a1 - a0 + 1;
+            uint32_t m = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+            uint32_t bits = (v >> (a0 - lo)) & m;
+            allz &= bits == 0u;
+            allo &= bits == m;
           }
         }
       }
-      if (r >= pos && r < pos + 24) {  // digit holding t's LSB: decide
-        uint32_t lsb = (v >> (r - pos)) & 1u;
-        uint32_t inc;
+      if (r >= lo && r < lo + 32) {  // limb holding t's LSB: decide
+        uint32_t lsb = (v >> (r - lo)) & 1u;
         if (exact) {
-          inc = rbit & ((sticky ? 1u : 0u) | lsb);
+          tcarry = rbit & ((sticky ? 1u : 0u) | lsb);
         } else {
-          if (allz || allo) return false;  // undecided: caller reruns exact
-          inc = rbit;
+          if (allz || allo) return false;  // undecided: rerun with the full product
+          tcarry = rbit;
         }
         decided = true;
-        tcarry = inc;
       }
     }
-    if (pos + 24 > r) {  // bits >= r belong to the mantissa of t
-      int sh = r > pos ? r - pos : 0;
-      buf |= (uint64_t)(v >> sh) << nb;
-      nb += 24 - sh;
-      while (tl < L) {
-        int need = tl == 0 ? 32 - zb : 32;
-        if (nb < need) break;
-        uint32_t limb;
-        if (tl == 0) {
-          uint64_t part = buf & ((need == 32) ? 0xffffffffull : ((1ull << need) - 1ull));
-          uint64_t sum = (part << zb) + ((uint64_t)tcarry << zb);
-          limb = (uint32_t)sum;
-          tcarry = (uint32_t)(sum >> 32);
-        } else {
-          uint64_t sum = (buf & 0xffffffffull) + tcarry;
-          limb = (uint32_t)sum;
-          tcarry = (uint32_t)(sum >> 32);
-        }
-        buf >>= need;
-        nb -= need;
-        S->push(limb);
-        tl++;
-      }
-      if (tl == L && nb > 0) {
-        if (buf) excess = true;
-        buf = 0;
-        nb = 0;
-      }
+    // T limb l = funnel(P_{oq+l}, P_{oq+l+1}) >> orr
+    int l = orr ? g - oq - 1 : g - oq;
+    if (l >= 0 && l < L) {
+      uint32_t t = orr ? ((prevP >> orr) | (v << (32 - orr))) : v;
+      if (l == 0 && zb) t &= ~((1u << zb) - 1u);
+      uint32_t add = (l == 0) ? (tcarry << zb) : tcarry;
+      uint32_t s = t + add;
+      tcarry = (s < t) ? 1u : 0u;
+      S->push(s);
+      tl = l + 1;
+    } else if (l >= L) {
+      // bits at and above r + p must be zero
+      uint32_t hiw = (l == L && orr) ? ((prevP >> orr) | (v << (32 - orr))) : v;
+      if (hiw) excess = true;
     }
+    prevP = v;
     return true;
   }
 
   __device__ __forceinline__ bool finish(double carry) {
-    if (carry != 0.0 || tl != L) excess = true;
+    if (carry != 0.0) excess = true;
+    // P's remaining limbs are zero: flush the last T limbs
+    for (int guard = 0; tl < L && guard < L + 4; guard++) limb(gn, 0u);
+    if (tl != L) excess = true;
     S->push(tcarry);  // overflow limb T_L (t rounded up to 2^p)
     S->finish();
     return true;
@@ -323,117 +344,185 @@ struct Emit {
 };
 
 // ------------------------------------------------------------ the product
-// P = sum_c col_c 2^(24c), col_c = sum_{s+t=c} z_s b_t, for columns
-// c >= c_start, streamed low -> high as nonnegative digits to `cons`.
+// Accumulators of output digit columns [c0, c0+W) (+ the overflow slot acc[W])
+// of P = sum_c col_c 2^(24c), col_c = sum_{s+t=c} z_s b_t, starting from zero.
+// z digits zrow[s] (padded by W zeros), b digits bcol[(t + 2W) * BS]
+// (padded by 2W below and W above).  Every partial sum is an exact integer
+// below 2^53 (carries flushed every FLUSH steps).
+template <int W, int BS>
+__device__ __forceinline__ void block_accumulate(const double* __restrict__ zrow, const double* __restrict__ bcol,
+                                                 int Db, int c0, double (&acc)[W + 1]) {
+#pragma unroll
+  for (int w = 0; w <= W; w++) acc[w] = 0.0;
+  int s_lo = c0 - (Db - 1);
+  if (s_lo < 0) s_lo = 0;
+  int s_hi = c0 + W - 1;
+  if (s_hi > Db - 1) s_hi = Db - 1;
+  if (s_lo > s_hi) return;
+  double ph[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) ph[w] = bcol[(c0 + w - s_lo + 2 * W) * BS];
+  int ngroups = (s_hi - s_lo + W) / W;
+  int s = s_lo;
+  for (int g = 0; g < ngroups; g++) {
+#pragma unroll
+    for (int u = 0; u < W; u++) {
+      double zv = zrow[s + u];
+#pragma unroll
+      for (int w = 0; w < W; w++) acc[w] = fma(zv, ph[(w - u + W) % W], acc[w]);
+      ph[(2 * W - 1 - u) % W] = bcol[(c0 - (s + u) - 1 + 2 * W) * BS];
+    }
+    s += W;
+    if (((g + 1) & (FLUSH / W - 1)) == 0) {
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        double q = rint(acc[w] * R24);
+        acc[w] = fma(-q, B24, acc[w]);
+        acc[w + 1] += q;
+      }
+    }
+  }
+}
+
+// Final normalisation of one block (c0 = 0 mod 4) with the incoming carry;
+// packs the W nonnegative 24-bit digits into 3W/4 whole limbs of P (limb
+// index 3*c0/4) and feeds them to `cons`; false if the consumer aborted.
 template <int W, class C>
+__device__ __forceinline__ bool block_emit(double (&acc)[W + 1], double& carry, int c0, C& cons) {
+  acc[0] += carry;
+  uint32_t dg[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    double q = floor(acc[w] * R24);
+    acc[w] = fma(-q, B24, acc[w]);
+    acc[w + 1] += q;
+    dg[w] = (uint32_t)(int)acc[w];
+  }
+  carry = acc[W];
+  const int g0 = (3 * c0) >> 2;
+#pragma unroll
+  for (int k = 0; k < W / 4; k++) {
+    uint32_t d0 = dg[4 * k], d1 = dg[4 * k + 1], d2 = dg[4 * k + 2], d3 = dg[4 * k + 3];
+    if (!cons.limb(g0 + 3 * k, d0 | (d1 << 24))) return false;
+    if (!cons.limb(g0 + 3 * k + 1, (d1 >> 8) | (d2 << 16))) return false;
+    if (!cons.limb(g0 + 3 * k + 2, (d2 >> 16) | (d3 << 8))) return false;
+  }
+  return true;
+}
+
+// P = sum_c col_c 2^(24c) for columns c >= c_start, streamed low -> high as
+// nonnegative digits to `cons` (one thread).
+template <int W, int BS, class C>
 __device__ __forceinline__ bool product(const double* __restrict__ zrow, const double* __restrict__ bcol, int Db,
                                         int c_start, int cmax, C& cons) {
   double carry = 0.0;
   for (int c0 = c_start; c0 <= cmax; c0 += W) {
     double acc[W + 1];
-    acc[0] = carry;
-#pragma unroll
-    for (int w = 1; w <= W; w++) acc[w] = 0.0;
-    int s_lo = c0 - (Db - 1);
-    if (s_lo < 0) s_lo = 0;
-    int s_hi = c0 + W - 1;
-    if (s_hi > Db - 1) s_hi = Db - 1;
-    if (s_lo <= s_hi) {
-      double ph[W];
-#pragma unroll
-      for (int w = 0; w < W; w++) ph[w] = bcol[(c0 + w - s_lo + 2 * W) * TC];
-      int ngroups = (s_hi - s_lo + W) / W;
-      int s = s_lo;
-      for (int g = 0; g < ngroups; g++) {
-#pragma unroll
-        for (int u = 0; u < W; u++) {
-          double zv = zrow[s + u];
-#pragma unroll
-          for (int w = 0; w < W; w++) acc[w] = fma(zv, ph[(w - u + W) % W], acc[w]);
-          ph[(2 * W - 1 - u) % W] = bcol[(c0 - (s + u) - 1 + 2 * W) * TC];
-        }
-        s += W;
-        if (((g + 1) & (FLUSH / W - 1)) == 0) {
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            double q = rint(acc[w] * R24);
-            acc[w] = fma(-q, B24, acc[w]);
-            acc[w + 1] += q;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < W; w++) {
-      double q = floor(acc[w] * R24);
-      acc[w] = fma(-q, B24, acc[w]);
-      acc[w + 1] += q;
-    }
-#pragma unroll
-    for (int w = 0; w < W; w++)
-      if (!cons.digit(c0 + w, (uint32_t)(int)acc[w])) return false;
-    carry = acc[W];
+    block_accumulate<W, BS>(zrow, bcol, Db, c0, acc);
+    if (!block_emit<W>(acc, carry, c0, cons)) return false;
   }
   return cons.finish(carry);
 }
 
 // ------------------------------------------------------------ element
-template <int W>
-__device__ void update_element(const UArgs& a, const double* zrow, const double* bcol, int jl, int k) {
+// The whole element: sign/zero logic, normalisation prediction, product
+// (short, exact fallback), streamed rounding into the S window, final RN.
+// SPLIT: lanes of the warp compute disjoint column blocks in parallel and
+// lane 0 consumes them (pure products of the det chain / minors emission).
+template <int W, int BS, bool SPLIT>
+__device__ void fused_element(const UArgs& a, const double* zrow, const double* bcol, uint32_t* Sw, int nth, int r,
+                              int k, int64_t oidx, double* blk) {
   const int L = a.L, p = a.p;
-  int64_t idx = (int64_t)jl * a.n + k;
-  uint8_t ca = a.a_cls[idx];
-  uint8_t cz = a.z_cls[jl];
-  uint8_t cb = a.b_cls[k];
+  uint8_t cz = a.zcls[r];
+  uint8_t cb = a.bcls[k];
+  int st = (cz & 1) ^ (cb & 1);
+  bool mul = a.mode == 1;
+  uint8_t ca = mul ? DS_CLS_PZERO : a.o_cls[oidx];
   bool za = ca >= DS_CLS_PZERO;
-  int sa = ca & 1, st = (cz & 1) ^ (cb & 1);
+  int sa = ca & 1;
   if (cz >= DS_CLS_PZERO || cb >= DS_CLS_PZERO) {  // t = (-1)^st 0
-    if (!za) return;                                // a - 0 = a
-    a.a_cls[idx] = (sa && !st) ? DS_CLS_NZERO : DS_CLS_PZERO;
+    if (mul) {
+      for (int l = 0; l < L; l++) a.o_limbs[(int64_t)l * a.o_count + oidx] = 0u;
+      a.o_exp[oidx] = 0;
+      a.o_cls[oidx] = st ? DS_CLS_NZERO : DS_CLS_PZERO;
+      return;
+    }
+    if (!za) return;  // a - 0 = a
+    a.o_cls[oidx] = (sa && !st) ? DS_CLS_NZERO : DS_CLS_PZERO;
     return;
   }
-  int32_t ea = a.a_exp[idx];
-  double pr = a.zf[jl] * a.bf[k];
+  int32_t ea = za ? 0 : a.o_exp[oidx];
+  double pr = a.zf[r] * a.bf[k];
   int norm = pr >= 2.0 ? 1 : 0;
   bool confident = fabs(pr - 2.0) > 0x1p-42;
-  int64_t ebase = (int64_t)a.z_exp[jl] + a.b_exp[k];
-  if (!za && (int64_t)ea - (ebase - 1) >= (int64_t)p + 2 + 1) return;  // a dominates whatever the norm
+  int64_t ebase = (int64_t)a.zexp[r] + a.bexp[k];
+  if (!za && (int64_t)ea - (ebase - 1) >= (int64_t)p + 3) return;  // a dominates whatever the norm
   if (!confident) {
     DryTop dt;
     dt.bitpos = 2 * p - 1;
     dt.top = 0;
-    product<W>(zrow, bcol, a.Db, 0, a.cmax, dt);
+    if (!SPLIT || (threadIdx.x & 31) == 0) product<W, BS>(zrow, bcol, a.Db, 0, a.cmax, dt);
     norm = dt.top;
+    if (SPLIT) norm = __shfl_sync(0xffffffffu, norm, 0);
   }
   int64_t et = ebase - (norm ? 0 : 1);
   int64_t d = za ? -(int64_t)(1 << 30) : (int64_t)ea - et;
   if (!za && d >= (int64_t)p + 2) return;  // RN(a - t) = a
   bool xa = !za && d >= 0;
-  bool sub = !za && (sa == st);  // a + (-t): magnitudes subtract iff signs of a and -t differ
-  int neg = xa ? sa : (st ^ 1);
+  bool sub = !za && (sa == st);           // a + (-t): magnitudes subtract iff sign(a) == sign(t)
+  int neg = mul ? st : (xa ? sa : (st ^ 1));
   int64_t E = xa ? ea : et;
-  uint32_t* A = a.a_limbs + idx;
-  int64_t stA = a.a_count;
 
+  const int lane = threadIdx.x & 31;
   SWin S;
+  S.S = Sw;
+  S.nth = nth;
   Emit em;
   bool done = false;
   for (int attempt = 0; attempt < 2 && !done; attempt++) {
     bool exact = attempt == 1 || a.c_lo == 0;
-    S.init(A, stA, L, xa, sub, za, xa ? d : (za ? 0 : -d));
+    if (!SPLIT || lane == 0) S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
     em.S = &S;
     em.r = norm ? p : p - 1;
-    em.zb = a.zb; em.p = p; em.L = L; em.cmax = a.cmax;
+    em.zb = a.zb; em.p = p; em.L = L;
     em.exact = exact;
     em.lo_chk = 24 * a.c_lo + a.eps;
     em.hi_chk = em.r - 2;
     em.allz = true; em.allo = true; em.sticky = false; em.decided = false;
-    em.rbit = 0; em.tcarry = 0; em.buf = 0; em.nb = 0; em.tl = 0; em.excess = false;
-    done = product<W>(zrow, bcol, a.Db, exact ? 0 : a.c_lo, a.cmax, em);
+    em.rbit = 0; em.tcarry = 0; em.tl = 0; em.excess = false;
+    em.setup();
+    if (SPLIT && !exact) {
+      // lanes accumulate disjoint column blocks; lane 0 normalises and rounds
+      const int c_start = a.c_lo;
+      const int nb = (a.cmax - c_start) / W + 1;
+      for (int b = lane; b < nb; b += 32) {
+        double acc[W + 1];
+        block_accumulate<W, BS>(zrow, bcol, a.Db, c_start + b * W, acc);
+#pragma unroll
+        for (int w = 0; w <= W; w++) blk[b * (W + 1) + w] = acc[w];
+      }
+      __syncwarp();
+      bool ok = true;
+      if (lane == 0) {
+        double carry = 0.0;
+        for (int b = 0; b < nb && ok; b++) {
+          double acc[W + 1];
+#pragma unroll
+          for (int w = 0; w <= W; w++) acc[w] = blk[b * (W + 1) + w];
+          ok = block_emit<W>(acc, carry, c_start + b * W, em);
+        }
+        if (ok) ok = em.finish(carry);
+      }
+      done = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+    } else {
+      if (!SPLIT || lane == 0) done = product<W, BS>(zrow, bcol, a.Db, exact ? 0 : a.c_lo, a.cmax, em);
+      if (SPLIT) done = __shfl_sync(0xffffffffu, done ? 1 : 0, 0) != 0;
+    }
   }
+  if (SPLIT && lane != 0) return;
   if (em.excess) atomicAdd(&a.status[4], 1);  // normalisation misprediction (must never happen)
 
-  // ---- normalise, round to nearest-even, write in place
+  // ---- normalise, round to nearest-even, write the result (coalesced)
   if (S.sub && S.cb) {  // negative (only possible when exponents are equal)
     uint32_t c = 1;
     for (int wi = 0; wi <= L + 1; wi++) {
@@ -451,10 +540,12 @@ __device__ void update_element(const UArgs& a, const double* zrow, const double*
       break;
     }
   }
+  uint32_t* O = a.o_limbs + oidx;
+  const int64_t so = a.o_count;
   if (h < 0) {  // exact cancellation -> +0
-    for (int l = 0; l < L; l++) A[(int64_t)l * stA] = 0u;
-    a.a_exp[idx] = 0;
-    a.a_cls[idx] = DS_CLS_PZERO;
+    for (int l = 0; l < L; l++) O[(int64_t)l * so] = 0u;
+    a.o_exp[oidx] = 0;
+    a.o_cls[oidx] = DS_CLS_PZERO;
     return;
   }
   int64_t e = E - 32 * (int64_t)L - 31 + h;
@@ -475,16 +566,11 @@ __device__ void update_element(const UArgs& a, const double* zrow, const double*
       if (S.get(wi)) stk = true;
     if (!stk && (rb & 31) && (S.get(rb >> 5) & ((1u << (rb & 31)) - 1u))) stk = true;
   }
+  uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
+  uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
   const int zb = a.zb, zl = zb >> 5;
   int base = off >> 5, rs = off & 31;
   uint32_t lo = S.get(base);
-  // result LSB value (for ties-to-even)
-  uint32_t carry = 0;
-  {
-    // compute inc: need the LSB of the truncated mantissa = window bit lsbw
-    uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
-    carry = rbit & ((stk ? 1u : 0u) | lsb);
-  }
   for (int l = 0; l < L; l++) {
     uint32_t hi = S.get(base + l + 1);
     uint32_t v = rs ? ((lo >> rs) | (hi << (32 - rs))) : lo;
@@ -493,50 +579,96 @@ __device__ void update_element(const UArgs& a, const double* zrow, const double*
     else if (l == zl && (zb & 31)) v &= ~((1u << (zb & 31)) - 1u);
     if (l >= zl && carry) {
       uint32_t add = (l == zl) ? (1u << (zb & 31)) : 1u;
-      uint32_t r = v + add;
-      carry = r < v ? 1u : 0u;
-      v = r;
+      uint32_t rr = v + add;
+      carry = rr < v ? 1u : 0u;
+      v = rr;
     }
-    A[(int64_t)l * stA] = v;
+    O[(int64_t)l * so] = v;
   }
   if (carry) {
-    A[(int64_t)(L - 1) * stA] = 0x80000000u;
+    O[(int64_t)(L - 1) * so] = 0x80000000u;
     e += 1;
   }
   if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&a.status[2], 1);
-  a.a_exp[idx] = (int32_t)e;
-  a.a_cls[idx] = neg ? DS_CLS_NEG : DS_CLS_POS;
+  a.o_exp[oidx] = (int32_t)e;
+  a.o_cls[oidx] = neg ? DS_CLS_NEG : DS_CLS_POS;
 }
 
 template <int W>
-__global__ void __launch_bounds__(256) k_update_dfma(UArgs a, int TR) {
+__global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
   extern __shared__ double sm[];
   if (a.status[0] >= 0) return;
-  const int Db = a.Db;
+  const int Db = a.Db, L = a.L;
   const int ZP = Db + W;
   const int BP = Db + 3 * W;
   double* zs = sm;
   double* bs = sm + TR * ZP;
+  uint32_t* Sw = (uint32_t*)(bs + BP * TC);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int col0 = blockIdx.x * TC, row0 = blockIdx.y * TR;
   const int tid = ty * TC + tx, nth = TC * TR;
-  for (int e = tid; e < TR * ZP; e += nth) {
-    int r = e / ZP, s = e - r * ZP;
-    int rr = row0 + r;
-    zs[e] = (rr < a.nrows && s < Db) ? a.zdig[(int64_t)(a.jl0 + rr) * Db + s] : 0.0;
+  const int r = row0 + ty, cc = col0 + tx;
+  const bool active = r < a.nrows && cc < a.ncols && (cc + a.col_off) != a.skip_col;
+  const int k = cc + a.col_off;
+  const int64_t oidx = (a.orow0 + r) * a.ostride + (a.o_same ? k : cc + a.ocol_off);
+  // prefetch a's limbs into the S window (slots 1..L) while the operands stage
+  if (a.mode == 0 && active) {
+    const uint32_t* A = a.o_limbs + oidx;
+    for (int l = 0; l < L; l++) cp_async4(Sw + (l + 1) * nth + tid, A + (int64_t)l * a.o_count);
   }
-  for (int e = tid; e < BP * TC; e += nth) {
-    int tt = e / TC, c = e - tt * TC;
+  {  // operand staging: warp ty loads z row ty; b digits column tx, rows strided by TR
+    const bool zrow_ok = row0 + ty < a.nrows;
+    const double* zsrc = a.zdig + (int64_t)(zrow_ok ? row0 + ty : 0) * Db;
+    for (int s = tx; s < ZP; s += TC) cp_async8z(zs + ty * ZP + s, zsrc + (s < Db ? s : 0), zrow_ok && s < Db);
+    const bool col_ok = col0 + tx < a.ncols;
+    const double* bsrc = a.bdig + (col_ok ? col0 + tx + a.col_off : 0);
+    for (int tt = ty; tt < BP; tt += TR) {
+      int t = tt - 2 * W;
+      bool ok = col_ok && t >= 0 && t < Db;
+      cp_async8z(bs + tt * TC + tx, bsrc + (int64_t)(ok ? t : 0) * a.bstride, ok);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (!active) return;
+  fused_element<W, TC, false>(a, zs + ty * ZP, bs + tx, Sw + tid, nth, r, k, oidx, nullptr);
+}
+
+// One warp per product (mode 1): the det chain (1 element per step, on the
+// critical path) and the signed-minor row (i+1 elements).
+template <int W>
+__global__ void __launch_bounds__(128) k_mul_split(UArgs a, int nbs) {
+  extern __shared__ double sm[];
+  if (a.status[0] >= 0) return;
+  const int Db = a.Db, L = a.L;
+  const int WPB = blockDim.x >> 5;
+  const int ZP = Db + W, BP = Db + 3 * W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xs = sm;
+  double* ys = xs + ZP + (ZP & 1);
+  double* blk = ys + WPB * BP;
+  uint32_t* Sw = (uint32_t*)(blk + WPB * nbs * (W + 1));
+  for (int e = threadIdx.x; e < ZP; e += blockDim.x) xs[e] = e < Db ? a.zdig[e] : 0.0;
+  const int c = blockIdx.x * WPB + warp;
+  double* yw = ys + warp * BP;
+  for (int tt = lane; tt < BP; tt += 32) {
     int t = tt - 2 * W;
-    int cc = col0 + c;
-    double v = 0.0;
-    if (cc < a.ncols && t >= 0 && t < Db) v = a.bdig[(int64_t)t * a.n + map_col(a, cc)];
-    bs[e] = v;
+    yw[tt] = (c < a.ncols && t >= 0 && t < Db) ? a.bdig[(int64_t)t * a.bstride + c + a.col_off] : 0.0;
   }
   __syncthreads();
-  const int r = row0 + ty, cc = col0 + tx;
-  if (r >= a.nrows || cc >= a.ncols) return;
-  update_element<W>(a, zs + ty * ZP, bs + tx, a.jl0 + r, map_col(a, cc));
+  if (c >= a.ncols) return;
+  const int k = c + a.col_off;
+  const int64_t oidx = a.orow0 * a.ostride + (a.o_same ? k : c + a.ocol_off);
+  fused_element<W, 1, true>(a, xs, yw, Sw + warp * (L + 2), 1, 0, k, oidx, blk + warp * nbs * (W + 1));
+}
+
+static int split_smem(int W, int Db, int L, int cmax, int c_lo, int wpb) {
+  int nbs = (cmax - c_lo) / W + 1;
+  return 8 * ((Db + W + 1) + wpb * (Db + 3 * W) + wpb * nbs * (W + 1)) + 4 * wpb * (L + 2);
+}
+
+int fused_smem(int W, int TR, int Db, int L) {
+  return 8 * (TR * (Db + W) + (Db + 3 * W) * TC) + 4 * (L + 2) * TR * TC;
 }
 
 std::string g_err;
@@ -545,14 +677,22 @@ std::string g_err;
 
 // ---------------------------------------------------------------- host API
 struct UpdateWork {
-  double* zdig;
-  double* bdig;
+  double* zdig;   // [nloc][Db] multipliers of the current step
+  double* bdig;   // [Db][n] pivot row
   double* zf;
   double* bf;
+  double* ddig;   // [Db] det
+  double* df;
+  double* edig;   // [Db][n] row i+1 (minors emission)
+  double* ef;
   int nloc;
 };
 
-static int smem_bytes(int W, int TR, int Db) { return 8 * (TR * (Db + W) + (Db + 3 * W) * TC); }
+static int pick_tr(int W, int Db, int L, int maxsm) {
+  int TR = 8;
+  while (TR > 1 && fused_smem(W, TR, Db, L) > maxsm) TR /= 2;
+  return fused_smem(W, TR, Db, L) <= maxsm ? TR : 0;
+}
 
 int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   plan->enabled = 0;
@@ -564,19 +704,24 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   plan->workspace = nullptr;
   if (getenv("DS_DISABLE_DFMA")) return DS_OK;
   int W = plan->D <= 24 ? 8 : 16;
-  int TR = 8;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  while (TR > 1 && smem_bytes(W, TR, plan->D) > maxsm) TR /= 2;
-  if (smem_bytes(W, TR, plan->D) > maxsm) return DS_OK;  // too wide: general engine
+  int TR = pick_tr(W, plan->D, plan->L, maxsm);
+  if (TR == 0) return DS_OK;  // too wide for one CTA: general engine
   plan->w = W;
   plan->tr = TR;
   plan->tc = TC;
-  plan->smem = smem_bytes(W, TR, plan->D);
+  plan->smem = fused_smem(W, TR, plan->D, plan->L);
   cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
-  cudaError_t e1 = cudaFuncSetAttribute(k_update_dfma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  cudaError_t e2 = cudaFuncSetAttribute(k_update_dfma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) return DS_CUDA;
+  cudaError_t e1 = cudaFuncSetAttribute(k_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  cudaError_t e2 = cudaFuncSetAttribute(k_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  cudaError_t e3 = cudaFuncSetAttribute(k_mul_split<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) return DS_CUDA;
+  {
+    int clo = ((p - 2) / 24 - GUARD) & ~3;
+    if (clo < 0) clo = 0;
+    if (split_smem(4, plan->D, plan->L, (2 * p - 1) / 24, clo, 4) > maxsm) return DS_OK;
+  }
   plan->enabled = 1;
   return DS_OK;
 }
@@ -584,10 +729,9 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
 void update_plan_free(UpdatePlan* plan) {
   if (plan->workspace) {
     UpdateWork* w = (UpdateWork*)plan->workspace;
-    cudaFree(w->zdig);
-    cudaFree(w->bdig);
-    cudaFree(w->zf);
-    cudaFree(w->bf);
+    double* ptrs[] = {w->zdig, w->bdig, w->zf, w->bf, w->ddig, w->df, w->edig, w->ef};
+    for (double* q : ptrs)
+      if (q) cudaFree(q);
     delete w;
     plan->workspace = nullptr;
   }
@@ -596,17 +740,42 @@ void update_plan_free(UpdatePlan* plan) {
 static int ensure_work(UpdatePlan* plan, int nloc) {
   if (plan->workspace) return DS_OK;
   UpdateWork* w = new UpdateWork();
+  memset(w, 0, sizeof(*w));
   w->nloc = nloc;
-  size_t D = plan->D;
-  if (cudaMalloc(&w->zdig, sizeof(double) * D * (size_t)(nloc > 0 ? nloc : 1)) != cudaSuccess ||
-      cudaMalloc(&w->bdig, sizeof(double) * D * plan->n) != cudaSuccess ||
-      cudaMalloc(&w->zf, sizeof(double) * (size_t)(nloc > 0 ? nloc : 1)) != cudaSuccess ||
-      cudaMalloc(&w->bf, sizeof(double) * plan->n) != cudaSuccess) {
-    delete w;
-    return DS_OOM;
-  }
+  size_t D = plan->D, nl = nloc > 0 ? nloc : 1, n = plan->n;
+  bool ok = cudaMalloc(&w->zdig, sizeof(double) * D * nl) == cudaSuccess &&
+            cudaMalloc(&w->bdig, sizeof(double) * D * n) == cudaSuccess &&
+            cudaMalloc(&w->zf, sizeof(double) * nl) == cudaSuccess &&
+            cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
+            cudaMalloc(&w->ddig, sizeof(double) * D) == cudaSuccess &&
+            cudaMalloc(&w->df, sizeof(double) * 1) == cudaSuccess &&
+            cudaMalloc(&w->edig, sizeof(double) * D * n) == cudaSuccess &&
+            cudaMalloc(&w->ef, sizeof(double) * n) == cudaSuccess;
   plan->workspace = w;
-  return DS_OK;
+  return ok ? DS_OK : DS_OOM;
+}
+
+static void base_args(UpdatePlan* plan, UArgs& a, int32_t* status) {
+  const int p = plan->p;
+  a.p = p; a.L = plan->L; a.Db = plan->D; a.zb = 32 * plan->L - p;
+  int clo = ((p - 2) / 24 - GUARD) & ~3;  // blocks start on whole limbs
+  a.c_lo = clo > 0 ? clo : 0;
+  a.cmax = (2 * p - 1) / 24;
+  int lg = 0;
+  while ((1 << lg) < plan->D) lg++;
+  a.eps = 23 + lg;
+  a.status = status;
+}
+
+static cudaError_t launch_fused(UpdatePlan* plan, const UArgs& a, int TR, cudaStream_t s) {
+  dim3 grid((a.ncols + TC - 1) / TC, (a.nrows + TR - 1) / TR);
+  dim3 block(TC, TR);
+  size_t smem = fused_smem(plan->w, TR, plan->D, plan->L);
+  if (plan->w == 8)
+    k_fused<8><<<grid, block, smem, s>>>(a, TR);
+  else
+    k_fused<16><<<grid, block, smem, s>>>(a, TR);
+  return cudaGetLastError();
 }
 
 int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
@@ -618,32 +787,57 @@ int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* 
   UpdateWork* wk = (UpdateWork*)plan->workspace;
   const int L = plan->L, p = plan->p, Db = plan->D;
   int nrows = nloc - jl0;
-  int ncols = collect_minors ? n - 1 : n - 1 - i;
+  int kstart = collect_minors ? 0 : i + 1;
+  int ncols = n - kstart;
   if (nrows <= 0 || ncols <= 0) return DS_OK;
   const uint32_t* b_limbs = (const uint32_t*)pbuf;
   const int32_t* b_exp = (const int32_t*)(pbuf + (size_t)4 * L * n);
   const uint8_t* b_cls = (const uint8_t*)(pbuf + (size_t)4 * L * n + (size_t)4 * n);
-  k_prep_digits<<<(nrows + 127) / 128, 128, 0, s>>>(z_limbs, nloc, jl0, nrows, L, p, Db, wk->zdig, Db, 1, wk->zf);
-  k_prep_digits<<<(n + 127) / 128, 128, 0, s>>>(b_limbs, n, 0, n, L, p, Db, wk->bdig, 1, n, wk->bf);
+  prep_launch(z_limbs + jl0, nloc, nrows, L, p, Db, wk->zdig, Db, 1, wk->zf, s);
+  prep_launch(b_limbs, n, n, L, p, Db, wk->bdig, 1, n, wk->bf, s);
   UArgs a;
-  a.p = p; a.L = L; a.Db = Db; a.zb = 32 * L - p; a.n = n; a.i = i; a.jl0 = jl0; a.nrows = nrows;
-  a.ncols = ncols; a.collect_minors = collect_minors;
-  int clo = (p - 2) / 24 - GUARD;
-  a.c_lo = clo > 0 ? clo : 0;
-  a.cmax = (2 * p - 1) / 24;
-  int lg = 0;
-  while ((1 << lg) < Db) lg++;
-  a.eps = 23 + lg;
-  a.a_limbs = a_limbs; a.a_exp = a_exp; a.a_cls = a_cls; a.a_count = a_count;
-  a.zdig = wk->zdig; a.bdig = wk->bdig; a.zf = wk->zf; a.bf = wk->bf;
-  a.z_exp = z_exp; a.z_cls = z_cls; a.b_exp = b_exp; a.b_cls = b_cls; a.status = status;
-  int TR = plan->tr;
-  dim3 grid((ncols + TC - 1) / TC, (nrows + TR - 1) / TR);
-  dim3 block(TC, TR);
-  if (plan->w == 8)
-    k_update_dfma<8><<<grid, block, plan->smem, s>>>(a, TR);
-  else
-    k_update_dfma<16><<<grid, block, plan->smem, s>>>(a, TR);
+  base_args(plan, a, status);
+  a.mode = 0;
+  a.nrows = nrows;
+  a.ncols = ncols;
+  a.zdig = wk->zdig; a.zf = wk->zf; a.zexp = z_exp + jl0; a.zcls = z_cls + jl0;
+  a.bdig = wk->bdig; a.bf = wk->bf; a.bexp = b_exp; a.bcls = b_cls; a.bstride = n;
+  a.col_off = kstart; a.skip_col = i; a.o_same = 1; a.ocol_off = 0;
+  a.o_limbs = a_limbs; a.o_exp = a_exp; a.o_cls = a_cls; a.o_count = a_count; a.ostride = n; a.orow0 = jl0;
+  cudaError_t e = launch_fused(plan, a, plan->tr, s);
+  *launches += 3;
+  return e == cudaSuccess ? DS_OK : DS_CUDA;
+}
+
+// out[c] = RN(x * y_c) for c in [0, count): x one real scalar (SoA count xcount,
+// element 0 at x_limbs), y_c elements of a real SoA row (plane stride ycount).
+// Used for the det chain (elim.py:214) and the signed minors (elim.py:59).
+int mul_row_launch(UpdatePlan* plan, cudaStream_t s, const uint32_t* x_limbs, int64_t xcount, const int32_t* x_exp,
+                   const uint8_t* x_cls, const uint32_t* y_limbs, int64_t ycount, const int32_t* y_exp,
+                   const uint8_t* y_cls, int count, uint32_t* o_limbs, int64_t o_count, int32_t* o_exp,
+                   uint8_t* o_cls, int32_t* status, int64_t* launches) {
+  int rc = ensure_work(plan, 1);
+  if (rc != DS_OK) return rc;
+  if (count <= 0) return DS_OK;
+  UpdateWork* wk = (UpdateWork*)plan->workspace;
+  const int L = plan->L, p = plan->p, Db = plan->D;
+  if (count > plan->n) return DS_INVALID;
+  prep_launch(x_limbs, xcount, 1, L, p, Db, wk->ddig, Db, 1, wk->df, s);
+  prep_launch(y_limbs, ycount, count, L, p, Db, wk->edig, 1, count, wk->ef, s);
+  UArgs a;
+  base_args(plan, a, status);
+  a.mode = 1;
+  a.nrows = 1;
+  a.ncols = count;
+  a.zdig = wk->ddig; a.zf = wk->df; a.zexp = x_exp; a.zcls = x_cls;
+  a.bdig = wk->edig; a.bf = wk->ef; a.bexp = y_exp; a.bcls = y_cls; a.bstride = count;
+  a.col_off = 0; a.skip_col = -1; a.o_same = 1; a.ocol_off = 0;
+  a.o_limbs = o_limbs; a.o_exp = o_exp; a.o_cls = o_cls; a.o_count = o_count; a.ostride = 0; a.orow0 = 0;
+  const int wpb = 4;
+  const int SW = 4;  // small column blocks: enough blocks to keep the 32 lanes busy
+  int nbs = (a.cmax - a.c_lo) / SW + 1;
+  size_t smem = split_smem(SW, Db, L, a.cmax, a.c_lo, wpb);
+  k_mul_split<SW><<<(count + wpb - 1) / wpb, 32 * wpb, smem, s>>>(a, nbs);
   *launches += 3;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DS_OK : DS_CUDA;
