@@ -31,7 +31,9 @@ using namespace ds;
 struct ds_ctx {
   int n, L, p, kind, ncomp, device, rank, world, nloc;
   cudaStream_t stream, own_stream;
-  cudaEvent_t ev;
+  cudaStream_t side;           // det chain + minors emission (outputs only, may lag)
+  cudaEvent_t ev, ev_piv, ev_upd;
+  double *ws_dx, *ws_dy, *ws_ex, *ws_ey;  // side-stream product workspaces
   // matrix rows owned by this rank: [ncomp][L][nloc*n] limbs
   uint32_t* a_limbs;
   int32_t* a_exp;
@@ -515,7 +517,7 @@ __global__ void k_mult_w(KArgs k, int i, int jl0, int wwords) {
 template <int K>
 __global__ void k_emit_norm_w(KArgs k, int i, int wwords) {
   extern __shared__ uint32_t wsm[];
-  if (k.status[0] >= 0) return;
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
   const int warp = threadIdx.x >> 5;
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
@@ -563,7 +565,7 @@ __global__ void k_pivot_lite(KArgs k, int i, int first) {
 
 // sig_{m-1} = det_i (elim.py:60)
 __global__ void k_emit_last(KArgs k, int i) {
-  if (k.status[0] >= 0) return;
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
   int64_t jl = (i + 1) / k.world;
   int64_t idx = jl * k.n + (i + 1);
   for (int c = 0; c < k.ncomp; c++) {
@@ -655,6 +657,14 @@ void ds_destroy(ds_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   update_plan_free(&ctx->plan);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
+  if (ctx->ws_dx) cudaFree(ctx->ws_dx);
+  if (ctx->ws_dy) cudaFree(ctx->ws_dy);
+  if (ctx->ws_ex) cudaFree(ctx->ws_ex);
+  if (ctx->ws_ey) cudaFree(ctx->ws_ey);
+  if (ctx->ev_piv) cudaEventDestroy(ctx->ev_piv);
+  if (ctx->ev_upd) cudaEventDestroy(ctx->ev_upd);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->snap_limbs) cudaFree(ctx->snap_limbs);
   if (ctx->snap_exp) cudaFree(ctx->snap_exp);
   if (ctx->snap_cls) cudaFree(ctx->snap_cls);
@@ -681,6 +691,9 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   ctx->stream = ctx->own_stream;
   CK(cudaEventCreateWithFlags(&ctx->ev, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_piv, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
   int L = ctx->L, nc = ctx->ncomp;
   ctx->a_count = (int64_t)ctx->nloc * n;
   int rc;
@@ -721,6 +734,14 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
       ds_destroy(ctx);
       return rc;
     }
+    if (ctx->plan.enabled) {
+      size_t a1 = mul_ws_doubles(&ctx->plan, 1), an = mul_ws_doubles(&ctx->plan, n);
+      if ((rc = dmalloc(ctx, &ctx->ws_dx, a1)) != DS_OK || (rc = dmalloc(ctx, &ctx->ws_dy, a1)) != DS_OK ||
+          (rc = dmalloc(ctx, &ctx->ws_ex, a1)) != DS_OK || (rc = dmalloc(ctx, &ctx->ws_ey, an)) != DS_OK) {
+        ds_destroy(ctx);
+        return rc;
+      }
+    }
   }
   CK(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
@@ -729,6 +750,7 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
 
 int ds_load(ds_ctx* ctx, const ds_soa* h) {
   CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
   int n = ctx->n, L = ctx->L;
   if (h->count != (int64_t)n * n) return DS_INVALID;
   // gather owned rows (row-cyclic) plane by plane; contiguous when world == 1
@@ -878,12 +900,16 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     k_pivot_lite<<<1, 128, 0, s>>>(k, i, first);
     ctx->launches++;
     if (!first) {
+      // det_i = RN(det_{i-1} * piv_i) on the side stream, from pivots[i]
+      CK(cudaEventRecord(ctx->ev_piv, s));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_piv, 0));
       const uint32_t* xl = ctx->det_from_cur ? ctx->cur_limbs : ctx->det_limbs + (i - 1);
       int64_t xc = ctx->det_from_cur ? 1 : n;
       const int32_t* xe = ctx->det_from_cur ? ctx->cur_exp : ctx->det_exp + (i - 1);
       const uint8_t* xk = ctx->det_from_cur ? ctx->cur_cls : ctx->det_cls + (i - 1);
-      int rc = mul_row_launch(&ctx->plan, s, xl, xc, xe, xk, pb.limbs + i, n, pb.exp + i, pb.cls + i, 1,
-                              ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i, ctx->status, &ctx->launches);
+      int rc = mul_row_launch(&ctx->plan, ctx->side, xl, xc, xe, xk, ctx->piv_limbs + i, n, ctx->piv_exp + i,
+                              ctx->piv_cls + i, 1, ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i,
+                              ctx->status, &ctx->launches, i, ctx->ws_dx, ctx->ws_dy);
       if (rc != DS_OK) { ctx->err = "det product launch failed"; return rc; }
     }
   } else {
@@ -945,15 +971,19 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     if ((series || m == n) && (i + 1) % ctx->world == ctx->rank) {
       int64_t jl = (i + 1) / ctx->world;
       if (fast) {
-        int rc = mul_row_launch(&ctx->plan, s, ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i,
+        // outputs only: run on the side stream after this step's update
+        cudaStream_t ss = ctx->side;
+        CK(cudaEventRecord(ctx->ev_upd, s));
+        CK(cudaStreamWaitEvent(ss, ctx->ev_upd, 0));
+        int rc = mul_row_launch(&ctx->plan, ss, ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i,
                                 ctx->a_limbs + jl * n, ctx->a_count, ctx->a_exp + jl * n, ctx->a_cls + jl * n, i + 1,
                                 ctx->sig_limbs + jl * n, ctx->a_count, ctx->sig_exp + jl * n, ctx->sig_cls + jl * n,
-                                ctx->status, &ctx->launches);
+                                ctx->status, &ctx->launches, i, ctx->ws_ex, ctx->ws_ey);
         if (rc != DS_OK) { ctx->err = "minor product launch failed"; return rc; }
-        k_emit_last<<<1, 128, 0, s>>>(k, i);
+        k_emit_last<<<1, 128, 0, ss>>>(k, i);
         int blocks = (m + wpb - 1) / wpb;
         size_t smem = (size_t)wpb * wwords * 4;
-        WDIV_DISPATCH(K, k_emit_norm_w, blocks, 32 * wpb, smem, s, k, i, wwords);
+        WDIV_DISPATCH(K, k_emit_norm_w, blocks, 32 * wpb, smem, ss, k, i, wwords);
         ctx->launches += 2;
       } else {
         k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
@@ -968,6 +998,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
 
 int ds_snapshot(ds_ctx* ctx, int save) {
   CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
   int nc = ctx->ncomp, L = ctx->L;
   size_t lb = sizeof(uint32_t) * nc * L * ctx->a_count, eb = sizeof(int32_t) * nc * ctx->a_count,
          cb = (size_t)nc * ctx->a_count;
@@ -1020,6 +1051,7 @@ int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
 
 int ds_status(ds_ctx* ctx, int* failed_step) {
   CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
   int32_t st[8];
   CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1087,6 +1119,7 @@ static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int3
 
 int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) {
   CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
   int rc;
   if ((rc = copy_vec(ctx, &r->pivots, ctx->piv_limbs, ctx->piv_exp, ctx->piv_cls, ctx->n, upto)) != DS_OK) return rc;
   if ((rc = copy_vec(ctx, &r->dets, ctx->det_limbs, ctx->det_exp, ctx->det_cls, ctx->n, upto)) != DS_OK) return rc;

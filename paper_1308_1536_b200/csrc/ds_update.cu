@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <string>
 
@@ -82,6 +83,7 @@ struct UArgs {
   uint8_t* o_cls;
   int64_t o_count, ostride, orow0;
   int32_t* status;
+  int step;  // skip when a zero pivot was seen at a step <= this one
 };
 
 __device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gsrc) {
@@ -242,6 +244,68 @@ struct SWin {
     if (xa)
       while (w <= L + 1) push(0u);
   }
+
+  // NL interior limbs of P -> T (funnel by orr, + carry) -> S window.
+  // Preconditions (checked by the caller): T indices and window indices in
+  // the interior, so no masking, sticky or range logic is needed.
+  template <int NL>
+  __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry) {
+    uint32_t T[NL];
+    uint32_t pp = prevP;
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+      uint32_t t = __funnelshift_r(pp, P[k], orr);
+      uint32_t s = t + tcarry;
+      tcarry = (s < t) ? 1u : 0u;
+      T[k] = s;
+      pp = P[k];
+    }
+    if (xa) {
+      // window limb w <- funnel(T_{w-1+dq}, T_{w+dq}, dr); X = a limb in slot w
+      uint32_t pt = prev;
+#pragma unroll
+      for (int k = 0; k < NL; k++) {
+        uint32_t yb = __funnelshift_r(pt, T[k], dr);
+        pt = T[k];
+        uint32_t X = S[w * nth];
+        uint32_t s;
+        if (sub) {
+          uint64_t y = (uint64_t)yb + cb;
+          s = (uint32_t)((uint64_t)X - y);
+          cb = ((uint64_t)X < y) ? 1u : 0u;
+        } else {
+          uint64_t t2 = (uint64_t)X + yb + cb;
+          s = (uint32_t)t2;
+          cb = (uint32_t)(t2 >> 32);
+        }
+        S[w * nth] = s;
+        w++;
+      }
+      prev = pt;
+      q += NL;
+    } else {
+      // window limb w <- T_{w-1} -/+ funnel(a_{w-1+dq}, a_{w+dq}, dr)
+#pragma unroll
+      for (int k = 0; k < NL; k++) {
+        uint32_t nxt = S[(w + dq + 1) * nth];  // a limb (w + dq), not yet overwritten
+        uint32_t yb = __funnelshift_r(curA, nxt, dr);
+        curA = nxt;
+        uint32_t X = T[k];
+        uint32_t s;
+        if (sub) {
+          uint64_t y = (uint64_t)yb + cb;
+          s = (uint32_t)((uint64_t)X - y);
+          cb = ((uint64_t)X < y) ? 1u : 0u;
+        } else {
+          uint64_t t2 = (uint64_t)X + yb + cb;
+          s = (uint32_t)t2;
+          cb = (uint32_t)(t2 >> 32);
+        }
+        S[w * nth] = s;
+        w++;
+      }
+    }
+  }
 };
 
 // ------------------------------------------------------------ limb consumers
@@ -255,20 +319,29 @@ struct DryTop {
     if ((bitpos >> 5) == g) top = (v >> (bitpos & 31)) & 1u;
     return true;
   }
+  template <int NL>
+  __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
+#pragma unroll
+    for (int k = 0; k < NL; k++) limb(g0 + k, P[k]);
+    return true;
+  }
   __device__ __forceinline__ bool finish(double) { return true; }
 };
 
 // Rounds P = z*b to the p-bit t (P bit r = t's LSB) and streams t's
 // left-aligned limbs T_0..T_{L-1} (+ overflow limb T_L) into the S window.
-// T_l = P bits [o + 32l, o + 32l + 32), o = r - zb, low zb bits of T_0
-// masked, the round increment added at bit zb of T_0.
+// T_q = P bits [o + 32q, o + 32q + 32) = funnel(P_{g-1}, P_g, orr) with
+// g = q + oq + 1, o = r - zb; low zb bits of T_0 masked, the round increment
+// added at bit zb of T_0.  Blocks arrive as NL = 3W/4 whole limbs; blocks
+// after the decision that lie in the interior of the T and S ranges take a
+// branch-free path (funnel shifts + carry chains in shared memory).
 struct Emit {
   SWin* S;
   int r, zb, p, L, o, oq, orr;
   bool exact;
   int lo_chk, hi_chk;  // short-product decision region [lo_chk, hi_chk]
   bool allz, allo, sticky, decided, excess;
-  uint32_t rbit, tcarry, prevP;
+  uint32_t rbit, tcarry, prevP, prevT;
   int tl, gtop, gn;
 
   __device__ __forceinline__ void setup() {
@@ -276,65 +349,96 @@ struct Emit {
     oq = o >> 5;
     orr = o & 31;
     prevP = 0;
+    prevT = 0;
     gn = 0;
-    gtop = (r + p + 31) >> 5;  // P limbs >= gtop (and bits >= r+p) must be zero
+    gtop = (r + p + 31) >> 5;
   }
 
-  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+  __device__ __forceinline__ bool decide_limb(int g, uint32_t v) {
     const int lo = 32 * g;
-    gn = g + 1;
-    if (!decided) {
-      if (lo < r) {
-        int rb = r - 1 - lo;  // round bit inside this limb?
-        if (rb >= 0 && rb < 32) rbit = (v >> rb) & 1u;
-        if (exact) {
-          uint32_t below = rb >= 32 ? v : (rb > 0 ? (v & ((1u << rb) - 1u)) : 0u);
-          if (below) sticky = true;
-        } else {
-          int a0 = lo > lo_chk ? lo : lo_chk;
-          int a1 = (lo + 31) < hi_chk ? (lo + 31) : hi_chk;
-          if (a1 >= a0) {
-            int len = a1 - a0 + 1;
-            uint32_t m = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
-            uint32_t bits = (v >> (a0 - lo)) & m;
-            allz &= bits == 0u;
-            allo &= bits == m;
-          }
+    if (lo < r) {
+      int rb = r - 1 - lo;
+      if (rb >= 0 && rb < 32) rbit = (v >> rb) & 1u;
+      if (exact) {
+        uint32_t below = rb >= 32 ? v : (rb > 0 ? (v & ((1u << rb) - 1u)) : 0u);
+        if (below) sticky = true;
+      } else {
+        int a0 = lo > lo_chk ? lo : lo_chk;
+        int a1 = (lo + 31) < hi_chk ? (lo + 31) : hi_chk;
+        if (a1 >= a0) {
+          int len = a1 - a0 + 1;
+          uint32_t m = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+          uint32_t bits = (v >> (a0 - lo)) & m;
+          allz &= bits == 0u;
+          allo &= bits == m;
         }
-      }
-      if (r >= lo && r < lo + 32) {  // limb holding t's LSB: decide
-        uint32_t lsb = (v >> (r - lo)) & 1u;
-        if (exact) {
-          tcarry = rbit & ((sticky ? 1u : 0u) | lsb);
-        } else {
-          if (allz || allo) return false;  // undecided: rerun with the full product
-          tcarry = rbit;
-        }
-        decided = true;
       }
     }
-    // T limb l = funnel(P_{oq+l}, P_{oq+l+1}) >> orr
-    int l = orr ? g - oq - 1 : g - oq;
-    if (l >= 0 && l < L) {
-      uint32_t t = orr ? ((prevP >> orr) | (v << (32 - orr))) : v;
-      if (l == 0 && zb) t &= ~((1u << zb) - 1u);
-      uint32_t add = (l == 0) ? (tcarry << zb) : tcarry;
+    if (r >= lo && r < lo + 32) {  // limb holding t's LSB: decide
+      uint32_t lsb = (v >> (r - lo)) & 1u;
+      if (exact) {
+        tcarry = rbit & ((sticky ? 1u : 0u) | lsb);
+      } else {
+        if (allz || allo) return false;  // undecided: rerun with the full product
+        tcarry = rbit;
+      }
+      decided = true;
+    }
+    return true;
+  }
+
+  // general path for one P limb
+  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+    gn = g + 1;
+    if (!decided && !decide_limb(g, v)) return false;
+    int q = g - oq - 1;
+    if (q >= 0 && q < L) {
+      uint32_t t = __funnelshift_r(prevP, v, orr);
+      uint32_t add = tcarry;
+      if (q == 0) {
+        if (zb) t &= ~((1u << zb) - 1u);
+        add <<= zb;
+      }
       uint32_t s = t + add;
       tcarry = (s < t) ? 1u : 0u;
       S->push(s);
-      tl = l + 1;
-    } else if (l >= L) {
-      // bits at and above r + p must be zero
-      uint32_t hiw = (l == L && orr) ? ((prevP >> orr) | (v << (32 - orr))) : v;
-      if (hiw) excess = true;
+      tl = q + 1;
+    } else if (q >= L) {
+      if (__funnelshift_r(prevP, v, orr)) excess = true;  // bits >= r + p must be zero
     }
     prevP = v;
     return true;
   }
 
+  template <int NL>
+  __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
+    const int q0 = g0 - oq - 1;
+    // interior fast path: decided, T indices [q0, q0+NL) inside [1, L), and the
+    // S window indices produced are inside [1, L]
+    bool interior = decided && q0 >= 1 && q0 + NL <= L;
+    if (interior) {
+      if (S->xa) {
+        int w0 = q0 - S->dq;
+        interior = w0 >= 1 && w0 + NL <= S->L;
+      } else {
+        interior = !S->yzero && (q0 + 1 + S->dq + NL) <= S->L;  // a limbs read stay inside [0, L)
+      }
+    }
+    if (!interior) {
+#pragma unroll
+      for (int k = 0; k < NL; k++)
+        if (!limb(g0 + k, P[k])) return false;
+      return true;
+    }
+    gn = g0 + NL;
+    S->fast_block<NL>(prevP, P, orr, tcarry);
+    prevP = P[NL - 1];
+    tl = q0 + NL;
+    return true;
+  }
+
   __device__ __forceinline__ bool finish(double carry) {
     if (carry != 0.0) excess = true;
-    // P's remaining limbs are zero: flush the last T limbs
     for (int guard = 0; tl < L && guard < L + 4; guard++) limb(gn, 0u);
     if (tl != L) excess = true;
     S->push(tcarry);  // overflow limb T_L (t rounded up to 2^p)
@@ -400,14 +504,15 @@ __device__ __forceinline__ bool block_emit(double (&acc)[W + 1], double& carry, 
   }
   carry = acc[W];
   const int g0 = (3 * c0) >> 2;
+  uint32_t P[3 * W / 4];
 #pragma unroll
   for (int k = 0; k < W / 4; k++) {
     uint32_t d0 = dg[4 * k], d1 = dg[4 * k + 1], d2 = dg[4 * k + 2], d3 = dg[4 * k + 3];
-    if (!cons.limb(g0 + 3 * k, d0 | (d1 << 24))) return false;
-    if (!cons.limb(g0 + 3 * k + 1, (d1 >> 8) | (d2 << 16))) return false;
-    if (!cons.limb(g0 + 3 * k + 2, (d2 >> 16) | (d3 << 8))) return false;
+    P[3 * k] = d0 | (d1 << 24);
+    P[3 * k + 1] = (d1 >> 8) | (d2 << 16);
+    P[3 * k + 2] = (d2 >> 16) | (d3 << 8);
   }
-  return true;
+  return cons.block(g0, P);
 }
 
 // P = sum_c col_c 2^(24c) for columns c >= c_start, streamed low -> high as
@@ -568,22 +673,29 @@ __device__ void fused_element(const UArgs& a, const double* zrow, const double* 
   }
   uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
   uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
-  const int zb = a.zb, zl = zb >> 5;
-  int base = off >> 5, rs = off & 31;
+  const int zb = a.zb;  // < 32: only limb 0 holds bits below the LSB
+  const int base = off >> 5, rs = off & 31;
   uint32_t lo = S.get(base);
-  for (int l = 0; l < L; l++) {
-    uint32_t hi = S.get(base + l + 1);
-    uint32_t v = rs ? ((lo >> rs) | (hi << (32 - rs))) : lo;
+  {
+    uint32_t hi = S.get(base + 1);
+    uint32_t v = __funnelshift_r(lo, hi, rs);
     lo = hi;
-    if (l < zl) v = 0;
-    else if (l == zl && (zb & 31)) v &= ~((1u << (zb & 31)) - 1u);
-    if (l >= zl && carry) {
-      uint32_t add = (l == zl) ? (1u << (zb & 31)) : 1u;
-      uint32_t rr = v + add;
-      carry = rr < v ? 1u : 0u;
-      v = rr;
-    }
-    O[(int64_t)l * so] = v;
+    if (zb) v &= ~((1u << zb) - 1u);
+    uint32_t add = carry << zb;
+    uint32_t rr = v + add;
+    carry = rr < v ? 1u : 0u;
+    O[0] = rr;
+  }
+  // S.get(base + l + 1) for l >= 1 stays inside the window: base + L <= L + 1
+  const uint32_t* Wp = Sw + (base + 2) * nth;
+#pragma unroll 4
+  for (int l = 1; l < L; l++) {
+    uint32_t hi = (base + l + 1 <= L + 1) ? Wp[(l - 1) * nth] : 0u;
+    uint32_t v = __funnelshift_r(lo, hi, rs);
+    lo = hi;
+    uint32_t rr = v + carry;
+    carry = rr < v ? 1u : 0u;
+    O[(int64_t)l * so] = rr;
   }
   if (carry) {
     O[(int64_t)(L - 1) * so] = 0x80000000u;
@@ -597,7 +709,7 @@ __device__ void fused_element(const UArgs& a, const double* zrow, const double* 
 template <int W>
 __global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
   extern __shared__ double sm[];
-  if (a.status[0] >= 0) return;
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int Db = a.Db, L = a.L;
   const int ZP = Db + W;
   const int BP = Db + 3 * W;
@@ -639,7 +751,7 @@ __global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
 template <int W>
 __global__ void __launch_bounds__(128) k_mul_split(UArgs a, int nbs) {
   extern __shared__ double sm[];
-  if (a.status[0] >= 0) return;
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int Db = a.Db, L = a.L;
   const int WPB = blockDim.x >> 5;
   const int ZP = Db + W, BP = Db + 3 * W;
@@ -688,6 +800,9 @@ struct UpdateWork {
   int nloc;
 };
 
+// per-context side-stream workspaces for mul_row_launch: digits + topf
+size_t mul_ws_doubles(const UpdatePlan* plan, int count) { return (size_t)plan->D * count + count + 8; }
+
 static int pick_tr(int W, int Db, int L, int maxsm) {
   int TR = 8;
   while (TR > 1 && fused_smem(W, TR, Db, L) > maxsm) TR /= 2;
@@ -703,7 +818,11 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   plan->device = device;
   plan->workspace = nullptr;
   if (getenv("DS_DISABLE_DFMA")) return DS_OK;
-  int W = plan->D <= 24 ? 8 : 16;
+  int W = plan->D <= 24 ? 8 : 16;  // W = 32 measured slower (corner waste (W-1)/Db)
+  if (const char* ew = getenv("DS_FUSED_W")) {  // tuning override: 8 / 16 / 32
+    int w = atoi(ew);
+    if (w == 8 || w == 16 || w == 32) W = w;
+  }
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int TR = pick_tr(W, plan->D, plan->L, maxsm);
@@ -715,6 +834,7 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e1 = cudaFuncSetAttribute(k_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   cudaError_t e2 = cudaFuncSetAttribute(k_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   cudaError_t e3 = cudaFuncSetAttribute(k_mul_split<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) return DS_CUDA;
   {
@@ -773,8 +893,10 @@ static cudaError_t launch_fused(UpdatePlan* plan, const UArgs& a, int TR, cudaSt
   size_t smem = fused_smem(plan->w, TR, plan->D, plan->L);
   if (plan->w == 8)
     k_fused<8><<<grid, block, smem, s>>>(a, TR);
-  else
+  else if (plan->w == 16)
     k_fused<16><<<grid, block, smem, s>>>(a, TR);
+  else
+    k_fused<32><<<grid, block, smem, s>>>(a, TR);
   return cudaGetLastError();
 }
 
@@ -804,6 +926,7 @@ int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* 
   a.bdig = wk->bdig; a.bf = wk->bf; a.bexp = b_exp; a.bcls = b_cls; a.bstride = n;
   a.col_off = kstart; a.skip_col = i; a.o_same = 1; a.ocol_off = 0;
   a.o_limbs = a_limbs; a.o_exp = a_exp; a.o_cls = a_cls; a.o_count = a_count; a.ostride = n; a.orow0 = jl0;
+  a.step = i;
   cudaError_t e = launch_fused(plan, a, plan->tr, s);
   *launches += 3;
   return e == cudaSuccess ? DS_OK : DS_CUDA;
@@ -815,22 +938,29 @@ int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* 
 int mul_row_launch(UpdatePlan* plan, cudaStream_t s, const uint32_t* x_limbs, int64_t xcount, const int32_t* x_exp,
                    const uint8_t* x_cls, const uint32_t* y_limbs, int64_t ycount, const int32_t* y_exp,
                    const uint8_t* y_cls, int count, uint32_t* o_limbs, int64_t o_count, int32_t* o_exp,
-                   uint8_t* o_cls, int32_t* status, int64_t* launches) {
+                   uint8_t* o_cls, int32_t* status, int64_t* launches, int step, double* wsx, double* wsy) {
   int rc = ensure_work(plan, 1);
   if (rc != DS_OK) return rc;
   if (count <= 0) return DS_OK;
   UpdateWork* wk = (UpdateWork*)plan->workspace;
   const int L = plan->L, p = plan->p, Db = plan->D;
   if (count > plan->n) return DS_INVALID;
-  prep_launch(x_limbs, xcount, 1, L, p, Db, wk->ddig, Db, 1, wk->df, s);
-  prep_launch(y_limbs, ycount, count, L, p, Db, wk->edig, 1, count, wk->ef, s);
+  // workspaces: the det chain and the minors emission use separate buffers so
+  // they can run on the side stream without racing each other
+  double* xd = wsx ? wsx : wk->ddig;
+  double* yd = wsy ? wsy : wk->edig;
+  double* xf = xd + Db;  // topf slots after the digits
+  double* yf = yd + (size_t)Db * count;
+  prep_launch(x_limbs, xcount, 1, L, p, Db, xd, Db, 1, xf, s);
+  prep_launch(y_limbs, ycount, count, L, p, Db, yd, 1, count, yf, s);
   UArgs a;
   base_args(plan, a, status);
   a.mode = 1;
   a.nrows = 1;
   a.ncols = count;
-  a.zdig = wk->ddig; a.zf = wk->df; a.zexp = x_exp; a.zcls = x_cls;
-  a.bdig = wk->edig; a.bf = wk->ef; a.bexp = y_exp; a.bcls = y_cls; a.bstride = count;
+  a.zdig = xd; a.zf = xf; a.zexp = x_exp; a.zcls = x_cls;
+  a.bdig = yd; a.bf = yf; a.bexp = y_exp; a.bcls = y_cls; a.bstride = count;
+  a.step = step;
   a.col_off = 0; a.skip_col = -1; a.o_same = 1; a.ocol_off = 0;
   a.o_limbs = o_limbs; a.o_exp = o_exp; a.o_cls = o_cls; a.o_count = o_count; a.ostride = 0; a.orow0 = 0;
   const int wpb = 4;

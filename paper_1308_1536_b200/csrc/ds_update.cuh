@@ -21,4 +21,5 @@ int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* 
 int mul_row_launch(UpdatePlan* plan, cudaStream_t s, const uint32_t* x_limbs, int64_t xcount, const int32_t* x_exp,
                    const uint8_t* x_cls, const uint32_t* y_limbs, int64_t ycount, const int32_t* y_exp,
                    const uint8_t* y_cls, int count, uint32_t* o_limbs, int64_t o_count, int32_t* o_exp,
-                   uint8_t* o_cls, int32_t* status, int64_t* launches);
+                   uint8_t* o_cls, int32_t* status, int64_t* launches, int step, double* wsx, double* wsy);
+size_t mul_ws_doubles(const UpdatePlan* plan, int count);
