@@ -53,16 +53,54 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dist", action="store_true",
+                    help="use the torch.distributed (NCCL) step loop even at world size 1 (testing)")
+    ap.add_argument("--family", default="beta", choices=["beta", "random"],
+                    help="beta: Artless-method beta matrix (genmat.beta_matrix, Eq. 9); random: random_uniform")
     return ap.parse_args()
+
+
+ZEROS = os.path.join(ROOT, "data", "zeta_zeros_4096.txt")
+
+
+def gamma_cache_path(n: int, p: int) -> str:
+    return os.path.join(ROOT, "data", f"beta_gammas_p{p}_N{n}.npz")
+
+
+def build_input(args, pinned: bool):
+    """(SoA matrix, description, seconds).  beta: bit-identical to
+    genmat.beta_matrix(load_zeros(zeros, Precision(p), n), n, SpougeGamma(),
+    Precision(p)) (tests/test_hostgen.py), built by the multi-threaded C
+    builder from the cached column Gammas when present."""
+    import numpy as np
+    t0 = time.perf_counter()
+    if args.family == "beta":
+        from paper_1308_1536_b200 import hostgen
+        from paper_1308_1536_b200.soa import SoA
+        gammas = None
+        cp = gamma_cache_path(args.n, args.prec)
+        if os.path.exists(cp):
+            z = np.load(cp)
+            gammas = SoA(2, int(z["L"]), int(z["count"]), np.ascontiguousarray(z["limbs"]),
+                         np.ascontiguousarray(z["exp"]), np.ascontiguousarray(z["cls"]))
+        A = hostgen.beta_matrix_soa(ZEROS, args.n, args.prec, pinned=pinned, gammas=gammas)
+        desc = (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
+                f"@{args.prec}b, zeros data/zeta_zeros_4096.txt" + (", cached column Gammas" if gammas else ""))
+    else:
+        from paper_1308_1536_b200.synth import random_uniform_soa
+        A = random_uniform_soa(args.n, args.prec, 2000, pinned=pinned)
+        desc = f"N={args.n} random_uniform real matrix @{args.prec}b (SURVEY 8d config 3')"
+    return A, desc, time.perf_counter() - t0
 
 
 def work_limb_macs(n: int, L: int, complex_: bool = False) -> float:
     return n * (n - 1) ** 2 / 2 * L * L * (4 if complex_ else 1)
 
 
-def workload(args) -> dict:
-    return {"workload": f"N={args.n} random_uniform real matrix @{args.prec}b: all leading minors + "
-                        f"last-column signed/normalized minors for every size (SURVEY 8d config 3')",
+def workload(args, desc: str = "") -> dict:
+    return {"workload": f"{desc}: all leading minors + last-column signed/normalized minors for every size "
+                        f"(BASELINE config 3)",
+            "family": args.family,
             "n": args.n, "prec_bits": args.prec, "limbs": (args.prec + 31) // 32, "kind": "real",
             "collect_minors": True, "series": True,
             "l2": "inputs larger than L2 (matrix %.1f GB)" % (args.n * args.n * (4 * ((args.prec + 31) // 32) + 5) / 1e9)}
@@ -115,35 +153,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(n: int, p: int, seconds: float, A=None):
+def cpu_reference(n: int, p: int, seconds: float, A):
     """Time the reference hot loop (oracle = elim.py:37-53 over MPFR) on a
-    bounded sample: pivot steps i = 0, 1, ... applied to all later rows of a
-    full-width matrix until ~`seconds` of wall time; all host threads."""
+    bounded sample of the workload: pivot row 0 applied to the next `rows`
+    full-width rows of A, repeated for steps i = 0, 1, ... until ~`seconds`
+    of wall time; all host threads."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-
     import oracle
-    from paper_1308_1536_b200.synth import random_uniform_soa
+    from paper_1308_1536_b200.soa import SoA
     L = (p + 31) // 32
     threads = len(os.sched_getaffinity(0))
-    rows_per_call = max(threads * 4, 64)
-    A = random_uniform_soa(rows_per_call + 1, p, 3) if A is None else A
-    # a full-width sample: pivot row + rows_per_call rows of width n
-    from paper_1308_1536_b200.soa import SoA
-    big = random_uniform_soa(1, p, 5)  # placeholder for shape
+    rows_per_call = min(max(threads * 4, 64), n - 1)
     prow = SoA(1, L, n)
     rows = SoA(1, L, rows_per_call * n)
-    src = random_uniform_soa(int(np.ceil(np.sqrt((rows_per_call + 1) * n))) + 1, p, 11)
-    prow.limbs[:] = src.limbs[:, :, :n]
-    prow.exp[:] = src.exp[:, :n]
-    prow.cls[:] = src.cls[:, :n]
-    rows.limbs[:] = src.limbs[:, :, n:n + rows_per_call * n]
-    rows.exp[:] = src.exp[:, n:n + rows_per_call * n]
-    rows.cls[:] = src.cls[:, n:n + rows_per_call * n]
-    del big
-    total_t, total_macs, calls = 0.0, 0.0, 0
-    i = 0
+    prow.limbs[:] = A.limbs[:, :, :n]
+    prow.exp[:] = A.exp[:, :n]
+    prow.cls[:] = A.cls[:, :n]
+    rows.limbs[:] = A.limbs[:, :, n:n + rows_per_call * n]
+    rows.exp[:] = A.exp[:, n:n + rows_per_call * n]
+    rows.cls[:] = A.cls[:, n:n + rows_per_call * n]
+    total_t, total_macs, calls, i = 0.0, 0.0, 0, 0
     while total_t < seconds and i < n - 1:
+        # step i touches all n-1 columns of every sampled row (L and U slots)
         dt = oracle.time_apply_pivot_rows(n, p, "real", i, prow, rows, rows_per_call, threads, True)
         total_t += dt
         total_macs += rows_per_call * (n - 1)
@@ -151,8 +182,9 @@ def cpu_reference(n: int, p: int, seconds: float, A=None):
         i += 1
     rate = total_macs * L * L / total_t
     return {"value": rate, "unit": "limb-MAC/s", "cores": threads, "kind": "port",
-            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}) of elim.py:37-53 "
-                      f"over MPFR 4.2.1, {total_macs:.3g} MACs in {total_t:.2f}s on {threads} threads",
+            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}) of the workload matrix, "
+                      f"elim.py:37-53 restated over MPFR 4.2.1 (oracle/ds_oracle.c), {total_macs:.3g} MACs in "
+                      f"{total_t:.2f}s on {threads} threads",
             "seconds_to_all_minors_extrapolated": work_limb_macs(n, L) / rate}
 
 
@@ -162,12 +194,13 @@ def run_reference(args):
         return
     L = (args.prec + 31) // 32
     per = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+    A, desc, _ = build_input(args, pinned=False)
     for _ in range(args.warmup):
-        cpu_reference(args.n, args.prec, per / 4)
+        cpu_reference(args.n, args.prec, per / 4, A)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference(args.n, args.prec, per))
+        vals.append(cpu_reference(args.n, args.prec, per, A))
     wall = time.perf_counter() - t0
     rate = sum(v["value"] for v in vals) / len(vals)
     base = vals[-1]
@@ -175,7 +208,7 @@ def run_reference(args):
            "value": rate, "unit": "limb-MAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "mpfr (u64 limbs)", "data": "synthetic", "impl": "reference",
-           "config": workload(args),
+           "config": workload(args, desc),
            "seconds_to_all_minors": work_limb_macs(args.n, L) / rate,
            "cpu_baseline": {"value": rate, "unit": "limb-MAC/s", "cores": base["cores"], "kind": "port",
                             "sample": base["sample"]},
@@ -194,19 +227,19 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_1308_1536_b200.engine import DeviceElimination, HostResults
-    from paper_1308_1536_b200.synth import random_uniform_soa
 
     n, p = args.n, args.prec
     L = (p + 31) // 32
-    A = random_uniform_soa(n, p, 2000, pinned=True)  # identical on every rank
+    A, desc, gen_s = build_input(args, pinned=True)  # identical on every rank
     eng = DeviceElimination(n, p, "real", local, rank, world)
     stream = torch.cuda.current_stream()
     pivot = None
-    if world > 1:
+    if use_dist:
         from paper_1308_1536_b200.parexec import dist_run
         _, pbytes = eng.pivot_buffer()
         pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{local}")
@@ -219,7 +252,7 @@ def main():
             eng.snapshot(False)
         else:
             eng.load(A)
-        if world == 1:
+        if not use_dist:
             if resident:
                 eng.run_resident(True, True, 0, n)
             else:
@@ -294,14 +327,15 @@ def main():
         cpu = None
         if not args.no_cpu:
             try:
-                cpu = cpu_reference(n, p, args.cpu_seconds)
+                cpu = cpu_reference(n, p, args.cpu_seconds, A)
             except Exception as exc:  # never fail the GPU line on the baseline
                 cpu = {"error": repr(exc)}
         out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
                "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "f64 (exact 24-bit digit products) + u32 limbs", "data": "synthetic",
-               "config": workload(args), "seconds_to_all_minors": ms / 1e3,
+               "dtype": "f64 (exact 24-bit digit products) + u32 limbs", "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
+               "config": workload(args, desc), "seconds_to_all_minors": ms / 1e3,
+               "input_generation_s": gen_s,
                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
                "clocks": clk.summary(), "parallelism": f"row-cyclic x{world}"}
         print(json.dumps(out), flush=True)

@@ -1,0 +1,85 @@
+"""Fast host builders (libds_hostgen.so) that produce benchmark-size inputs
+directly in the ds SoA format.
+
+beta_matrix_soa reproduces genmat.beta_matrix (reference genmat.py:156-190,
+Artless Eq. 9) bit for bit -- same MPFR/MPC operation sequence and working
+precisions -- in multi-threaded C with Gamma(1/4 - i t/2) memoised per column.
+This is input generation (the reference builds inputs through gmpy2 the same
+way); the elimination itself never runs on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .soa import SoA, ds_soa
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libds_hostgen.so")
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"{LIB_PATH} missing: run make -C paper_1308_1536_b200/csrc")
+        L = ctypes.CDLL(LIB_PATH)
+        L.dsh_beta_matrix.restype = ctypes.c_int
+        L.dsh_beta_matrix.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
+                                      ctypes.c_int, ctypes.POINTER(ds_soa), ctypes.POINTER(ds_soa)]
+        L.dsh_beta_gammas.restype = ctypes.c_int
+        L.dsh_beta_gammas.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
+                                      ctypes.c_int, ctypes.POINTER(ds_soa)]
+        _lib = L
+    return _lib
+
+
+def read_zero_tokens(path: str, count: int) -> list:
+    """First `count` zero ordinates of a zeros file as decimal strings
+    (the tokens load_zeros parses, genmat.py:50-60)."""
+    out = []
+    with open(path) as f:
+        for line in f:
+            tok = line.strip()
+            if not tok or tok.startswith("#"):
+                continue
+            out.append(tok)
+            if len(out) == count:
+                break
+    if len(out) < count:
+        from .errors import InsufficientZeros
+        raise InsufficientZeros(f"{path} holds {len(out)} zeros, need {count}")
+    return out
+
+
+def beta_gammas_soa(zeros_path: str, N: int, prec_bits: int, nthreads: int = 0, guard_bits: int = 64) -> SoA:
+    """Gamma(1/4 - i gamma_j / 2) at prec + guard bits for j < N (complex SoA):
+    the column-only, expensive part of beta_entry (genmat.py:171)."""
+    lib = _load()
+    toks = read_zero_tokens(zeros_path, N)
+    arr = (ctypes.c_char_p * N)(*[t.encode() for t in toks])
+    out = SoA(2, (prec_bits + guard_bits + 31) // 32, N)
+    c = out.c()
+    if lib.dsh_beta_gammas(N, prec_bits, arr, guard_bits, nthreads, ctypes.byref(c)) != 0:
+        from .errors import GammaEvaluationFailed
+        raise GammaEvaluationFailed("Spouge Gamma did not stabilise")
+    return out
+
+
+def beta_matrix_soa(zeros_path: str, N: int, prec_bits: int, nthreads: int = 0, guard_bits: int = 64,
+                    pinned: bool = False, gammas: SoA | None = None) -> SoA:
+    lib = _load()
+    toks = read_zero_tokens(zeros_path, N)
+    arr = (ctypes.c_char_p * N)(*[t.encode() for t in toks])
+    out = SoA(1, (prec_bits + 31) // 32, N * N, pinned=pinned)
+    c = out.c()
+    g = None
+    if gammas is not None:
+        assert gammas.ncomp == 2 and gammas.L == (prec_bits + guard_bits + 31) // 32 and gammas.count >= N
+        g = ctypes.byref(gammas.c())
+    rc = lib.dsh_beta_matrix(N, prec_bits, arr, guard_bits, nthreads, ctypes.byref(c), g)
+    if rc != 0:
+        from .errors import GammaEvaluationFailed
+        raise GammaEvaluationFailed("Spouge Gamma did not stabilise")
+    return out
