@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=2000)
-    ap.add_argument("--prec", type=int, default=4096)
+    ap.add_argument("--dim", dest="n", type=int, default=2000)
+    ap.add_argument("--bits", dest="prec", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

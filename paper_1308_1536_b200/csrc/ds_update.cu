@@ -262,34 +262,40 @@ struct SWin {
     }
     if (xa) {
       // window limb w <- funnel(T_{w-1+dq}, T_{w+dq}, dr); X = a limb in slot w
+      uint32_t X[NL];
+#pragma unroll
+      for (int k = 0; k < NL; k++) X[k] = S[(w + k) * nth];  // all loads first (ILP)
       uint32_t pt = prev;
 #pragma unroll
       for (int k = 0; k < NL; k++) {
         uint32_t yb = __funnelshift_r(pt, T[k], dr);
         pt = T[k];
-        uint32_t X = S[w * nth];
         uint32_t s;
         if (sub) {
           uint64_t y = (uint64_t)yb + cb;
-          s = (uint32_t)((uint64_t)X - y);
-          cb = ((uint64_t)X < y) ? 1u : 0u;
+          s = (uint32_t)((uint64_t)X[k] - y);
+          cb = ((uint64_t)X[k] < y) ? 1u : 0u;
         } else {
-          uint64_t t2 = (uint64_t)X + yb + cb;
+          uint64_t t2 = (uint64_t)X[k] + yb + cb;
           s = (uint32_t)t2;
           cb = (uint32_t)(t2 >> 32);
         }
-        S[w * nth] = s;
-        w++;
+        X[k] = s;
       }
+#pragma unroll
+      for (int k = 0; k < NL; k++) S[(w + k) * nth] = X[k];
+      w += NL;
       prev = pt;
       q += NL;
     } else {
       // window limb w <- T_{w-1} -/+ funnel(a_{w-1+dq}, a_{w+dq}, dr)
+      uint32_t Av[NL];
+#pragma unroll
+      for (int k = 0; k < NL; k++) Av[k] = S[(w + k + dq + 1) * nth];  // a limbs (w+k+dq): loads first
 #pragma unroll
       for (int k = 0; k < NL; k++) {
-        uint32_t nxt = S[(w + dq + 1) * nth];  // a limb (w + dq), not yet overwritten
-        uint32_t yb = __funnelshift_r(curA, nxt, dr);
-        curA = nxt;
+        uint32_t yb = __funnelshift_r(curA, Av[k], dr);
+        curA = Av[k];
         uint32_t X = T[k];
         uint32_t s;
         if (sub) {
@@ -301,9 +307,11 @@ struct SWin {
           s = (uint32_t)t2;
           cb = (uint32_t)(t2 >> 32);
         }
-        S[w * nth] = s;
-        w++;
+        T[k] = s;
       }
+#pragma unroll
+      for (int k = 0; k < NL; k++) S[(w + k) * nth] = T[k];
+      w += NL;
     }
   }
 };
@@ -706,7 +714,7 @@ __device__ void fused_element(const UArgs& a, const double* zrow, const double* 
   a.o_cls[oidx] = neg ? DS_CLS_NEG : DS_CLS_POS;
 }
 
-template <int W>
+template <int W, int TCc>
 __global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
   extern __shared__ double sm[];
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
@@ -715,10 +723,10 @@ __global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
   const int BP = Db + 3 * W;
   double* zs = sm;
   double* bs = sm + TR * ZP;
-  uint32_t* Sw = (uint32_t*)(bs + BP * TC);
+  uint32_t* Sw = (uint32_t*)(bs + BP * TCc);
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int col0 = blockIdx.x * TC, row0 = blockIdx.y * TR;
-  const int tid = ty * TC + tx, nth = TC * TR;
+  const int col0 = blockIdx.x * TCc, row0 = blockIdx.y * TR;
+  const int tid = ty * TCc + tx, nth = TCc * TR;
   const int r = row0 + ty, cc = col0 + tx;
   const bool active = r < a.nrows && cc < a.ncols && (cc + a.col_off) != a.skip_col;
   const int k = cc + a.col_off;
@@ -731,19 +739,19 @@ __global__ void __launch_bounds__(256) k_fused(UArgs a, int TR) {
   {  // operand staging: warp ty loads z row ty; b digits column tx, rows strided by TR
     const bool zrow_ok = row0 + ty < a.nrows;
     const double* zsrc = a.zdig + (int64_t)(zrow_ok ? row0 + ty : 0) * Db;
-    for (int s = tx; s < ZP; s += TC) cp_async8z(zs + ty * ZP + s, zsrc + (s < Db ? s : 0), zrow_ok && s < Db);
+    for (int s = tx; s < ZP; s += TCc) cp_async8z(zs + ty * ZP + s, zsrc + (s < Db ? s : 0), zrow_ok && s < Db);
     const bool col_ok = col0 + tx < a.ncols;
     const double* bsrc = a.bdig + (col_ok ? col0 + tx + a.col_off : 0);
     for (int tt = ty; tt < BP; tt += TR) {
       int t = tt - 2 * W;
       bool ok = col_ok && t >= 0 && t < Db;
-      cp_async8z(bs + tt * TC + tx, bsrc + (int64_t)(ok ? t : 0) * a.bstride, ok);
+      cp_async8z(bs + tt * TCc + tx, bsrc + (int64_t)(ok ? t : 0) * a.bstride, ok);
     }
   }
   cp_async_wait_all();
   __syncthreads();
   if (!active) return;
-  fused_element<W, TC, false>(a, zs + ty * ZP, bs + tx, Sw + tid, nth, r, k, oidx, nullptr);
+  fused_element<W, TCc, false>(a, zs + ty * ZP, bs + tx, Sw + tid, nth, r, k, oidx, nullptr);
 }
 
 // One warp per product (mode 1): the det chain (1 element per step, on the
@@ -779,8 +787,8 @@ static int split_smem(int W, int Db, int L, int cmax, int c_lo, int wpb) {
   return 8 * ((Db + W + 1) + wpb * (Db + 3 * W) + wpb * nbs * (W + 1)) + 4 * wpb * (L + 2);
 }
 
-int fused_smem(int W, int TR, int Db, int L) {
-  return 8 * (TR * (Db + W) + (Db + 3 * W) * TC) + 4 * (L + 2) * TR * TC;
+int fused_smem(int W, int TR, int Db, int L, int tc = TC) {
+  return 8 * (TR * (Db + W) + (Db + 3 * W) * tc) + 4 * (L + 2) * TR * tc;
 }
 
 std::string g_err;
@@ -827,14 +835,25 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int TR = pick_tr(W, plan->D, plan->L, maxsm);
   if (TR == 0) return DS_OK;  // too wide for one CTA: general engine
+  int tc = TC;
+  int smsm = 0;  // shared memory per SM
+  cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  // two independent 16-column CTAs per SM desynchronise the warps' epilogues
+  // (one 256-thread CTA runs all its warps in lockstep phases)
+  if (fused_smem(W, 8, plan->D, plan->L, 16) * 2 + 2048 <= smsm && !getenv("DS_FUSED_TC32")) {
+    tc = 16;
+    TR = 8;
+  }
   plan->w = W;
   plan->tr = TR;
-  plan->tc = TC;
-  plan->smem = fused_smem(W, TR, plan->D, plan->L);
+  plan->tc = tc;
+  plan->smem = fused_smem(W, TR, plan->D, plan->L, tc);
   cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
-  cudaError_t e1 = cudaFuncSetAttribute(k_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  cudaError_t e2 = cudaFuncSetAttribute(k_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-  if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  cudaError_t e1 = cudaFuncSetAttribute(k_fused<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_fused<8, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  cudaError_t e2 = cudaFuncSetAttribute(k_fused<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k_fused<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k_fused<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   cudaError_t e3 = cudaFuncSetAttribute(k_mul_split<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) return DS_CUDA;
   {
@@ -888,15 +907,18 @@ static void base_args(UpdatePlan* plan, UArgs& a, int32_t* status) {
 }
 
 static cudaError_t launch_fused(UpdatePlan* plan, const UArgs& a, int TR, cudaStream_t s) {
-  dim3 grid((a.ncols + TC - 1) / TC, (a.nrows + TR - 1) / TR);
-  dim3 block(TC, TR);
-  size_t smem = fused_smem(plan->w, TR, plan->D, plan->L);
-  if (plan->w == 8)
-    k_fused<8><<<grid, block, smem, s>>>(a, TR);
-  else if (plan->w == 16)
-    k_fused<16><<<grid, block, smem, s>>>(a, TR);
-  else
-    k_fused<32><<<grid, block, smem, s>>>(a, TR);
+  const int tc = plan->tc;
+  dim3 grid((a.ncols + tc - 1) / tc, (a.nrows + TR - 1) / TR);
+  dim3 block(tc, TR);
+  size_t smem = fused_smem(plan->w, TR, plan->D, plan->L, tc);
+  if (tc == 16) {
+    if (plan->w == 8) k_fused<8, 16><<<grid, block, smem, s>>>(a, TR);
+    else k_fused<16, 16><<<grid, block, smem, s>>>(a, TR);
+  } else {
+    if (plan->w == 8) k_fused<8, 32><<<grid, block, smem, s>>>(a, TR);
+    else if (plan->w == 16) k_fused<16, 32><<<grid, block, smem, s>>>(a, TR);
+    else k_fused<32, 32><<<grid, block, smem, s>>>(a, TR);
+  }
   return cudaGetLastError();
 }
 

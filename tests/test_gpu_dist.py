@@ -68,8 +68,9 @@ def test_torchrun_process_transport(name, tmp_path):
 def test_bench_under_torchrun_small():
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
-                        "--steps", "1", "--warmup", "1", "--n", "96", "--prec", "512", "--family", "random",
-                        "--cpu-seconds", "1", "--dist"], check=True, timeout=600, cwd=ROOT, capture_output=True, text=True)
+                        "--steps", "1", "--warmup", "1", "--dim", "96", "--bits", "512", "--family", "random",
+                        "--cpu-seconds", "1", "--dist"], timeout=600, cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     d = json.loads(line)
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
