@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed (NCCL) step loop even at world size 1 (testing)")
+    ap.add_argument("--gen-budget", type=float, default=420.0,
+                    help="max seconds of host time to build the Artless input before falling back to random")
     ap.add_argument("--family", default="beta", choices=["beta", "random"],
                     help="beta: Artless-method beta matrix (genmat.beta_matrix, Eq. 9); random: random_uniform")
     return ap.parse_args()
@@ -67,7 +69,7 @@ def gamma_cache_path(n: int, p: int) -> str:
     return os.path.join(ROOT, "data", f"beta_gammas_p{p}_N{n}.npz")
 
 
-def build_input(args, pinned: bool):
+def build_input(args, pinned: bool, rank: int = 0, world: int = 1):
     """(SoA matrix, description, seconds).  beta: bit-identical to
     genmat.beta_matrix(load_zeros(zeros, Precision(p), n), n, SpougeGamma(),
     Precision(p)) (tests/test_hostgen.py), built by the multi-threaded C
@@ -83,10 +85,25 @@ def build_input(args, pinned: bool):
             z = np.load(cp)
             gammas = SoA(2, int(z["L"]), int(z["count"]), np.ascontiguousarray(z["limbs"]),
                          np.ascontiguousarray(z["exp"]), np.ascontiguousarray(z["cls"]))
-        A = hostgen.beta_matrix_soa(ZEROS, args.n, args.prec, pinned=pinned, gammas=gammas)
-        desc = (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
-                f"@{args.prec}b, zeros data/zeta_zeros_4096.txt" + (", cached column Gammas" if gammas else ""))
-    else:
+        # each rank builds only the rows it owns (row-cyclic); host threads shared by the local ranks
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        threads = max(1, len(os.sched_getaffinity(0)) // local_world)
+        bb = hostgen.BetaBuilder(ZEROS, args.n, args.prec, gammas=gammas, pinned=pinned, nthreads=threads,
+                                 row0=rank, rstep=world)
+        probe = max(1, min(args.n, 2 * threads))
+        bb.fill(probe)
+        # later columns (larger ordinates) cost more per entry: 1.3x margin
+        est = 1.3 * (time.perf_counter() - t0) * args.n / probe
+        if est <= args.gen_budget:
+            bb.fill(args.n)
+            A = bb.out
+            desc = (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
+                    f"@{args.prec}b, zeros data/zeta_zeros_4096.txt" + (", cached column Gammas" if gammas else ""))
+            return A, desc, time.perf_counter() - t0
+        print(f"[bench] beta matrix generation would take ~{est:.0f}s > --gen-budget {args.gen_budget:.0f}s "
+              f"on this host: using random_uniform (same shape, same work)", file=sys.stderr)
+        args.family = "random"
+    if args.family == "random":
         from paper_1308_1536_b200.synth import random_uniform_soa
         A = random_uniform_soa(args.n, args.prec, 2000, pinned=pinned)
         desc = f"N={args.n} random_uniform real matrix @{args.prec}b (SURVEY 8d config 3')"
@@ -235,7 +252,7 @@ def main():
 
     n, p = args.n, args.prec
     L = (p + 31) // 32
-    A, desc, gen_s = build_input(args, pinned=True)  # identical on every rank
+    A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world)  # this rank's rows
     eng = DeviceElimination(n, p, "real", local, rank, world)
     stream = torch.cuda.current_stream()
     pivot = None
@@ -325,7 +342,7 @@ def main():
     out = None
     if rank == 0:
         cpu = None
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # rank 0 at N=1 only
             try:
                 cpu = cpu_reference(n, p, args.cpu_seconds, A)
             except Exception as exc:  # never fail the GPU line on the baseline

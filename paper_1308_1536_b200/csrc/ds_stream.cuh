@@ -1,0 +1,406 @@
+// ds_stream.cuh -- the per-element rounding stream shared by the fused DFMA
+// update (ds_update.cu) and the tensor-core update (ds_tc.cu):
+//   product limbs (low -> high) -> Emit (round to the p-bit t, short-product
+//   decision) -> SWin (exact aligned a -/+ t window with guard limb + sticky,
+//   in shared memory) -> round_write (normalise, RN, coalesced store).
+#pragma once
+#include <stdint.h>
+#include "../../include/detseries_b200.h"
+
+namespace dss {
+
+// ------------------------------------------------------------ S window
+// Exact aligned sum S = |X| -/+ |Y| of a and t on a window of L+2 limbs held
+// in SHARED memory (limb w at S[w*nth]): limb 0 = guard, limbs 1..L = X's
+// mantissa positions, limb L+1 = carry.  a's limbs were prefetched into
+// limbs 1..L with cp.async while the product ran.  X is the operand with the
+// larger exponent; Y is shifted right by dq limbs + dr bits; Y bits below the
+// window become the sticky bit (effective subtraction borrows one guard ulp
+// when sticky -- the standard round/sticky trick).
+struct SWin {
+  uint32_t* S;
+  int nth;
+  int L;
+  bool xa;     // X = a (Y = t) or X = t (Y = a)
+  bool sub;    // effective subtraction
+  bool yzero;  // Y == 0 (a == 0, or a pure product)
+  int dq, dr;
+  uint32_t prev;
+  int q, w;
+  uint32_t cb;
+  bool sticky;
+  uint32_t curA;
+
+  __device__ __forceinline__ uint32_t get(int wi) const {
+    return (wi >= 0 && wi <= L + 1) ? S[wi * nth] : 0u;
+  }
+  __device__ __forceinline__ void set(int wi, uint32_t v) { S[wi * nth] = v; }
+  // a limb l (0 <= l < L) lives in window slot l + 1 until overwritten
+  __device__ __forceinline__ uint32_t aload(int l) const { return (l >= 0 && l < L) ? S[(l + 1) * nth] : 0u; }
+
+  __device__ __forceinline__ void emit(uint32_t X, uint32_t Yb) {
+    uint32_t s;
+    if (sub) {
+      uint64_t y = (uint64_t)Yb + cb + ((w == 0 && sticky) ? 1u : 0u);
+      s = (uint32_t)((uint64_t)X - y);
+      cb = ((uint64_t)X < y) ? 1u : 0u;
+    } else {
+      uint64_t t = (uint64_t)X + Yb + cb;
+      s = (uint32_t)t;
+      cb = (uint32_t)(t >> 32);
+    }
+    S[w * nth] = s;
+    w++;
+  }
+
+  __device__ __forceinline__ uint32_t abits(int wi) {
+    uint32_t nxt = aload(wi + dq);
+    uint32_t v = dr ? ((curA >> dr) | (nxt << (32 - dr))) : curA;
+    curA = nxt;
+    return v;
+  }
+
+  __device__ void init(int L_, bool xa_, bool sub_, bool yzero_, int64_t shift) {
+    L = L_; xa = xa_; sub = sub_; yzero = yzero_;
+    if (shift > 32 * (int64_t)(L + 3)) shift = 32 * (int64_t)(L + 3);
+    dq = (int)(shift >> 5);
+    dr = (int)(shift & 31);
+    prev = 0; q = 0; w = 0; cb = 0; sticky = false; curA = 0;
+    if (xa) {
+      S[0] = 0u;
+      S[(L + 1) * nth] = 0u;
+      return;
+    }
+    if (yzero) {
+      emit(0u, 0u);
+      return;
+    }
+    int64_t below = 32 * (int64_t)(dq - 1) + dr;  // a bits [0, below) are under the window
+    for (int l = 0; l < L && (int64_t)l * 32 < below; l++) {
+      uint32_t v = aload(l);
+      int64_t lim = below - 32 * (int64_t)l;
+      if (lim < 32) v &= (1u << lim) - 1u;
+      if (v) sticky = true;
+    }
+    curA = aload(dq - 1);
+    emit(0u, abits(0));
+  }
+
+  __device__ __forceinline__ void push(uint32_t T) {
+    if (xa) {
+      int wq = q - dq;
+      if (wq < 0) {
+        if (q >= 1 && prev) sticky = true;
+      } else {
+        if (wq == 0 && dr > 0 && (prev & ((1u << dr) - 1u))) sticky = true;
+        uint32_t Yb = dr ? ((prev >> dr) | (T << (32 - dr))) : prev;
+        emit((wq >= 1 && wq <= L) ? S[wq * nth] : 0u, Yb);
+      }
+      prev = T;
+      q++;
+    } else {
+      emit(T, yzero ? 0u : abits(w));
+    }
+  }
+
+  __device__ void finish() {
+    if (xa)
+      while (w <= L + 1) push(0u);
+  }
+
+  // NL interior limbs of P -> T (funnel by orr, + carry) -> S window.
+  // Preconditions (checked by the caller): T indices and window indices in
+  // the interior, so no masking, sticky or range logic is needed.
+  template <int NL>
+  __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry) {
+    uint32_t T[NL];
+    uint32_t pp = prevP;
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+      uint32_t t = __funnelshift_r(pp, P[k], orr);
+      uint32_t s = t + tcarry;
+      tcarry = (s < t) ? 1u : 0u;
+      T[k] = s;
+      pp = P[k];
+    }
+    if (xa) {
+      // window limb w <- funnel(T_{w-1+dq}, T_{w+dq}, dr); X = a limb in slot w
+      uint32_t X[NL];
+#pragma unroll
+      for (int k = 0; k < NL; k++) X[k] = S[(w + k) * nth];  // all loads first (ILP)
+      uint32_t pt = prev;
+#pragma unroll
+      for (int k = 0; k < NL; k++) {
+        uint32_t yb = __funnelshift_r(pt, T[k], dr);
+        pt = T[k];
+        uint32_t s;
+        if (sub) {
+          uint64_t y = (uint64_t)yb + cb;
+          s = (uint32_t)((uint64_t)X[k] - y);
+          cb = ((uint64_t)X[k] < y) ? 1u : 0u;
+        } else {
+          uint64_t t2 = (uint64_t)X[k] + yb + cb;
+          s = (uint32_t)t2;
+          cb = (uint32_t)(t2 >> 32);
+        }
+        X[k] = s;
+      }
+#pragma unroll
+      for (int k = 0; k < NL; k++) S[(w + k) * nth] = X[k];
+      w += NL;
+      prev = pt;
+      q += NL;
+    } else {
+      // window limb w <- T_{w-1} -/+ funnel(a_{w-1+dq}, a_{w+dq}, dr)
+      uint32_t Av[NL];
+#pragma unroll
+      for (int k = 0; k < NL; k++) Av[k] = S[(w + k + dq + 1) * nth];  // a limbs (w+k+dq): loads first
+#pragma unroll
+      for (int k = 0; k < NL; k++) {
+        uint32_t yb = __funnelshift_r(curA, Av[k], dr);
+        curA = Av[k];
+        uint32_t X = T[k];
+        uint32_t s;
+        if (sub) {
+          uint64_t y = (uint64_t)yb + cb;
+          s = (uint32_t)((uint64_t)X - y);
+          cb = ((uint64_t)X < y) ? 1u : 0u;
+        } else {
+          uint64_t t2 = (uint64_t)X + yb + cb;
+          s = (uint32_t)t2;
+          cb = (uint32_t)(t2 >> 32);
+        }
+        T[k] = s;
+      }
+#pragma unroll
+      for (int k = 0; k < NL; k++) S[(w + k) * nth] = T[k];
+      w += NL;
+    }
+  }
+};
+
+// ------------------------------------------------------------ limb consumers
+// The product arrives low -> high as 32-bit limbs of P (blocks of W digits
+// starting at a column c0 = 0 mod 4 are exactly 3W/4 whole limbs).
+// Top-bit probe (exact dry product): is bit 2p-1 of P set?
+struct DryTop {
+  int bitpos;
+  int top;
+  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+    if ((bitpos >> 5) == g) top = (v >> (bitpos & 31)) & 1u;
+    return true;
+  }
+  template <int NL>
+  __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
+#pragma unroll
+    for (int k = 0; k < NL; k++) limb(g0 + k, P[k]);
+    return true;
+  }
+  __device__ __forceinline__ bool finish(double) { return true; }
+};
+
+// Rounds P = z*b to the p-bit t (P bit r = t's LSB) and streams t's
+// left-aligned limbs T_0..T_{L-1} (+ overflow limb T_L) into the S window.
+// T_q = P bits [o + 32q, o + 32q + 32) = funnel(P_{g-1}, P_g, orr) with
+// g = q + oq + 1, o = r - zb; low zb bits of T_0 masked, the round increment
+// added at bit zb of T_0.  Blocks arrive as NL = 3W/4 whole limbs; blocks
+// after the decision that lie in the interior of the T and S ranges take a
+// branch-free path (funnel shifts + carry chains in shared memory).
+struct Emit {
+  SWin* S;
+  int r, zb, p, L, o, oq, orr;
+  bool exact;
+  bool onesided;       // omitted low part E >= 0 (unsigned digits) instead of |E| < 2^eps
+  int lo_chk, hi_chk;  // short-product decision region [lo_chk, hi_chk]
+  bool allz, allo, sticky, decided, excess;
+  uint32_t rbit, tcarry, prevP, prevT;
+  int tl, gtop, gn;
+
+  __device__ __forceinline__ void setup() {
+    o = r - zb;
+    oq = o >> 5;
+    orr = o & 31;
+    prevP = 0;
+    prevT = 0;
+    gn = 0;
+    gtop = (r + p + 31) >> 5;
+  }
+
+  __device__ __forceinline__ bool decide_limb(int g, uint32_t v) {
+    const int lo = 32 * g;
+    if (lo < r) {
+      int rb = r - 1 - lo;
+      if (rb >= 0 && rb < 32) rbit = (v >> rb) & 1u;
+      if (exact) {
+        uint32_t below = rb >= 32 ? v : (rb > 0 ? (v & ((1u << rb) - 1u)) : 0u);
+        if (below) sticky = true;
+      } else {
+        int a0 = lo > lo_chk ? lo : lo_chk;
+        int a1 = (lo + 31) < hi_chk ? (lo + 31) : hi_chk;
+        if (a1 >= a0) {
+          int len = a1 - a0 + 1;
+          uint32_t m = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+          uint32_t bits = (v >> (a0 - lo)) & m;
+          allz &= bits == 0u;
+          allo &= bits == m;
+        }
+      }
+    }
+    if (r >= lo && r < lo + 32) {  // limb holding t's LSB: decide
+      uint32_t lsb = (v >> (r - lo)) & 1u;
+      if (exact) {
+        tcarry = rbit & ((sticky ? 1u : 0u) | lsb);
+      } else {
+        if (onesided ? (allo || (rbit && allz)) : (allz || allo)) return false;  // undecided
+        tcarry = rbit;
+      }
+      decided = true;
+    }
+    return true;
+  }
+
+  // general path for one P limb
+  __device__ __forceinline__ bool limb(int g, uint32_t v) {
+    gn = g + 1;
+    if (!decided && !decide_limb(g, v)) return false;
+    int q = g - oq - 1;
+    if (q >= 0 && q < L) {
+      uint32_t t = __funnelshift_r(prevP, v, orr);
+      uint32_t add = tcarry;
+      if (q == 0) {
+        if (zb) t &= ~((1u << zb) - 1u);
+        add <<= zb;
+      }
+      uint32_t s = t + add;
+      tcarry = (s < t) ? 1u : 0u;
+      S->push(s);
+      tl = q + 1;
+    } else if (q >= L) {
+      if (__funnelshift_r(prevP, v, orr)) excess = true;  // bits >= r + p must be zero
+    }
+    prevP = v;
+    return true;
+  }
+
+  template <int NL>
+  __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
+    const int q0 = g0 - oq - 1;
+    // interior fast path: decided, T indices [q0, q0+NL) inside [1, L), and the
+    // S window indices produced are inside [1, L]
+    bool interior = decided && q0 >= 1 && q0 + NL <= L;
+    if (interior) {
+      if (S->xa) {
+        int w0 = q0 - S->dq;
+        interior = w0 >= 1 && w0 + NL <= S->L;
+      } else {
+        interior = !S->yzero && (q0 + 1 + S->dq + NL) <= S->L;  // a limbs read stay inside [0, L)
+      }
+    }
+    if (!interior) {
+#pragma unroll
+      for (int k = 0; k < NL; k++)
+        if (!limb(g0 + k, P[k])) return false;
+      return true;
+    }
+    gn = g0 + NL;
+    S->fast_block<NL>(prevP, P, orr, tcarry);
+    prevP = P[NL - 1];
+    tl = q0 + NL;
+    return true;
+  }
+
+  __device__ __forceinline__ bool finish(double carry) {
+    if (carry != 0.0) excess = true;
+    for (int guard = 0; tl < L && guard < L + 4; guard++) limb(gn, 0u);
+    if (tl != L) excess = true;
+    S->push(tcarry);  // overflow limb T_L (t rounded up to 2^p)
+    S->finish();
+    return true;
+  }
+};
+
+
+// Normalise the S window, round to nearest-even at p bits and write the
+// left-aligned result limbs O[l*so] (coalesced across a warp), exponent and
+// class.  E is the exponent of the window's X operand.
+__device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,
+                                            int64_t so, int32_t* oexp, uint8_t* ocls, int32_t* status) {
+  uint32_t* Sw = S.S;
+  const int nth = S.nth;
+  // ---- normalise, round to nearest-even, write the result (coalesced)
+  if (S.sub && S.cb) {  // negative (only possible when exponents are equal)
+    uint32_t c = 1;
+    for (int wi = 0; wi <= L + 1; wi++) {
+      uint64_t v = (uint64_t)(uint32_t)~S.get(wi) + c;
+      S.set(wi, (uint32_t)v);
+      c = (uint32_t)(v >> 32);
+    }
+    neg ^= 1;
+  }
+  int h = -1;
+  for (int wi = L + 1; wi >= 0; wi--) {
+    uint32_t v = S.get(wi);
+    if (v) {
+      h = 32 * wi + 31 - __clz(v);
+      break;
+    }
+  }
+  if (h < 0) {  // exact cancellation -> +0
+    for (int l = 0; l < L; l++) O[(int64_t)l * so] = 0u;
+    *oexp = 0;
+    *ocls = DS_CLS_PZERO;
+    return;
+  }
+  int64_t e = E - 32 * (int64_t)L - 31 + h;
+  int off = h - 32 * L + 1;
+  if (off < 0) {  // massive cancellation: move the window up by whole limbs
+    int qs = (-off + 31) / 32;
+    for (int wi = L + 1; wi >= 0; wi--) S.set(wi, S.get(wi - qs));
+    h += 32 * qs;
+    off += 32 * qs;
+  }
+  int lsbw = h - p + 1;
+  uint32_t rbit = 0;
+  bool stk = S.sticky;
+  if (lsbw - 1 >= 0) {
+    int rb = lsbw - 1;
+    rbit = (S.get(rb >> 5) >> (rb & 31)) & 1u;
+    for (int wi = 0; wi < (rb >> 5) && !stk; wi++)
+      if (S.get(wi)) stk = true;
+    if (!stk && (rb & 31) && (S.get(rb >> 5) & ((1u << (rb & 31)) - 1u))) stk = true;
+  }
+  uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
+  uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
+  const int base = off >> 5, rs = off & 31;
+  uint32_t lo = S.get(base);
+  {
+    uint32_t hi = S.get(base + 1);
+    uint32_t v = __funnelshift_r(lo, hi, rs);
+    lo = hi;
+    if (zb) v &= ~((1u << zb) - 1u);
+    uint32_t add = carry << zb;
+    uint32_t rr = v + add;
+    carry = rr < v ? 1u : 0u;
+    O[0] = rr;
+  }
+  // S.get(base + l + 1) for l >= 1 stays inside the window: base + L <= L + 1
+  const uint32_t* Wp = Sw + (base + 2) * nth;
+#pragma unroll 4
+  for (int l = 1; l < L; l++) {
+    uint32_t hi = (base + l + 1 <= L + 1) ? Wp[(l - 1) * nth] : 0u;
+    uint32_t v = __funnelshift_r(lo, hi, rs);
+    lo = hi;
+    uint32_t rr = v + carry;
+    carry = rr < v ? 1u : 0u;
+    O[(int64_t)l * so] = rr;
+  }
+  if (carry) {
+    O[(int64_t)(L - 1) * so] = 0x80000000u;
+    e += 1;
+  }
+  if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&status[2], 1);
+  *oexp = (int32_t)e;
+  *ocls = neg ? DS_CLS_NEG : DS_CLS_POS;
+}
+
+}  // namespace dss

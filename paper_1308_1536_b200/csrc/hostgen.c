@@ -184,13 +184,23 @@ int dsh_beta_gammas(int N, long p, const char **zeros, int guard_bits, int nthre
 
 /* gammas: optional precomputed Gamma values (complex ds SoA, count >= N, at
  * precision p + guard_bits, from dsh_beta_gammas); NULL computes them. */
+int dsh_beta_matrix_cols(int N, long p, const char **zeros, int guard_bits, int nthreads, ds_soa *out,
+                         const ds_soa *gammas, int j0, int j1, int row0, int rstep);
+
 int dsh_beta_matrix(int N, long p, const char **zeros, int guard_bits, int nthreads, ds_soa *out,
                     const ds_soa *gammas) {
+  return dsh_beta_matrix_cols(N, p, zeros, guard_bits, nthreads, out, gammas, 0, N, 0, 1);
+}
+
+/* columns [j0, j1) and rows row0, row0 + rstep, ... only (a rank of the
+ * row-cyclic layout builds just the rows it owns) */
+int dsh_beta_matrix_cols(int N, long p, const char **zeros, int guard_bits, int nthreads, ds_soa *out,
+                         const ds_soa *gammas, int j0, int j1, int row0, int rstep) {
   const long work = p + guard_bits;
   const int L = (int)((p + 31) / 32);
   int failed = 0;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : omp_get_max_threads())
-  for (int j = 0; j < N; j++) {
+  for (int j = j0; j < j1; j++) {
     mpfr_t tp, tt, pi, lp, A, lnn, val, outp, ztmp;
     mpc_t I, z, g, v, w2, pref, pAg, u, e, npow, den, term, four, half, tmpc;
     mpfr_init2(tp, p);
@@ -239,7 +249,7 @@ int dsh_beta_matrix(int N, long p, const char **zeros, int guard_bits, int nthre
     mpc_set_d(half, 0.5, RNN);
     mpc_sub(u, half, v, RNN);
     mpc_set_ui(four, 4, RNN);
-    for (int n = 1; n <= N; n++) {
+    for (int n = 1 + row0; n <= N; n += rstep) {
       mpfr_set_ui(lnn, (unsigned long)n, RN);
       mpfr_log(lnn, lnn, RN);                          /* log(mpfr(n)) */
       mpc_set_fr(tmpc, lnn, RNN);

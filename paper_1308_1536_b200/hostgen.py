@@ -28,6 +28,10 @@ def _load():
         L.dsh_beta_matrix.restype = ctypes.c_int
         L.dsh_beta_matrix.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(ds_soa), ctypes.POINTER(ds_soa)]
+        L.dsh_beta_matrix_cols.restype = ctypes.c_int
+        L.dsh_beta_matrix_cols.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
+                                           ctypes.c_int, ctypes.POINTER(ds_soa), ctypes.POINTER(ds_soa), ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.dsh_beta_gammas.restype = ctypes.c_int
         L.dsh_beta_gammas.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(ds_soa)]
@@ -83,3 +87,33 @@ def beta_matrix_soa(zeros_path: str, N: int, prec_bits: int, nthreads: int = 0, 
         from .errors import GammaEvaluationFailed
         raise GammaEvaluationFailed("Spouge Gamma did not stabilise")
     return out
+
+
+class BetaBuilder:
+    """Incremental builder: fill column ranges of the N x N beta matrix (so a
+    caller can time the first chunk and decide whether to continue)."""
+
+    def __init__(self, zeros_path: str, N: int, prec_bits: int, gammas: SoA | None = None, nthreads: int = 0,
+                 guard_bits: int = 64, pinned: bool = False, row0: int = 0, rstep: int = 1):
+        self.lib = _load()
+        self.N, self.p, self.guard, self.nthreads = N, prec_bits, guard_bits, nthreads
+        toks = read_zero_tokens(zeros_path, N)
+        self._arr = (ctypes.c_char_p * N)(*[t.encode() for t in toks])
+        self.out = SoA(1, (prec_bits + 31) // 32, N * N, pinned=pinned)
+        self._c = self.out.c()
+        self._g = gammas
+        self._gc = gammas.c() if gammas is not None else None
+        self.done = 0
+        self.row0, self.rstep = row0, rstep
+
+    def fill(self, j1: int):
+        j1 = min(j1, self.N)
+        if j1 <= self.done:
+            return
+        g = ctypes.byref(self._gc) if self._gc is not None else None
+        rc = self.lib.dsh_beta_matrix_cols(self.N, self.p, self._arr, self.guard, self.nthreads,
+                                           ctypes.byref(self._c), g, self.done, j1, self.row0, self.rstep)
+        if rc != 0:
+            from .errors import GammaEvaluationFailed
+            raise GammaEvaluationFailed("Spouge Gamma did not stabilise")
+        self.done = j1
