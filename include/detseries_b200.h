@@ -158,6 +158,12 @@ int ds_snapshot(ds_ctx *ctx, int save);
  * (rows * cols * L^2, x4 for complex), then clears the counters. */
 int ds_profile(ds_ctx *ctx, int enable);
 int ds_profile_read(ds_ctx *ctx, double *update_ms, int64_t *launches, double *limb_macs);
+/* Internal engine counters (observability; no reference counterpart):
+ * out[0] = elements the tensor-core update handed to the exact fallback
+ * (short product undecided / normalisation uncertain), out[1] = 1 if the
+ * tensor-core update engine is active, out[2] = 1 if the DFMA engine is.
+ * Writes min(n, 3) values. */
+int ds_counters(ds_ctx *ctx, int64_t *out, int n);
 
 /* Last error message of this context (or of the last failed ds_create when
  * ctx is NULL). */

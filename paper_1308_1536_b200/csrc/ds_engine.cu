@@ -22,6 +22,7 @@
 
 #include "ds_mp.cuh"
 #include "ds_update.cuh"
+#include "ds_tc.cuh"
 #include "ds_warpdiv.cuh"
 
 using namespace ds;
@@ -74,6 +75,7 @@ struct ds_ctx {
   double prof_work;
   // fused update engine workspace
   UpdatePlan plan;
+  TcPlan tc;  // tensor-core update (tcgen05 kind::i8), preferred when enabled
   int64_t launches;
   int host_have_det;   // a det chain value exists (first step sets det = piv)
   int det_from_cur;    // next det product reads the ds_set_det seed in `cur`
@@ -657,6 +659,7 @@ void ds_destroy(ds_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   update_plan_free(&ctx->plan);
+  tc_plan_free(&ctx->tc);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ws_dx) cudaFree(ctx->ws_dx);
   if (ctx->ws_dy) cudaFree(ctx->ws_dy);
@@ -735,6 +738,12 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
       return rc;
     }
     if (ctx->plan.enabled) {
+      rc = tc_plan_init(&ctx->tc, n, ctx->nloc, ctx->p, device);
+      if (rc != DS_OK) {
+        ctx->err = "tensor-core update plan: device allocation or attribute failed";
+        ds_destroy(ctx);
+        return rc;
+      }
       size_t a1 = mul_ws_doubles(&ctx->plan, 1), an = mul_ws_doubles(&ctx->plan, n);
       if ((rc = dmalloc(ctx, &ctx->ws_dx, a1)) != DS_OK || (rc = dmalloc(ctx, &ctx->ws_dy, a1)) != DS_OK ||
           (rc = dmalloc(ctx, &ctx->ws_ex, a1)) != DS_OK || (rc = dmalloc(ctx, &ctx->ws_ey, an)) != DS_OK) {
@@ -951,9 +960,13 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
       ctx->prof_work += (double)nrows * ncols_u * (double)L * L * (ctx->kind == DS_KIND_COMPLEX ? 4.0 : 1.0);
     }
     if (fast) {
-      int rc = update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
-                             ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
-                             ctx->status, &ctx->launches);
+      int rc = ctx->tc.enabled
+                   ? tc_update_launch(&ctx->tc, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
+                                      ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
+                                      ctx->status, &ctx->launches)
+                   : update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
+                                   ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
+                                   ctx->status, &ctx->launches);
       if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
     } else {
       int kfirst = collect_minors ? 0 : i + 1;
@@ -1049,6 +1062,17 @@ int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
   return DS_OK;
 }
 
+int ds_counters(ds_ctx* ctx, int64_t* out, int n) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
+  int32_t st[8];
+  CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int64_t v[3] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.enabled && !ctx->tc.enabled) ? 1 : 0};
+  for (int q = 0; q < n && q < 3; q++) out[q] = v[q];
+  return DS_OK;
+}
+
 int ds_status(ds_ctx* ctx, int* failed_step) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
@@ -1059,6 +1083,10 @@ int ds_status(ds_ctx* ctx, int* failed_step) {
   if (st[2] != 0) {
     ctx->err = "exponent left the MPFR default range";
     return DS_OVERFLOW;
+  }
+  if (st[4] != 0 || st[5] != 0) {  // internal consistency counters: must stay zero
+    ctx->err = st[4] ? "update engine: normalisation misprediction" : "tensor-core update: fallback list overflow";
+    return DS_CUDA;
   }
   return DS_OK;
 }

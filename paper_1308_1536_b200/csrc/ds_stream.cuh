@@ -17,9 +17,20 @@ namespace dss {
 // larger exponent; Y is shifted right by dq limbs + dr bits; Y bits below the
 // window become the sticky bit (effective subtraction borrows one guard ulp
 // when sticky -- the standard round/sticky trick).
+// shared-memory accesses by 32-bit shared address (LDS/STS; the window
+// pointer would otherwise be generic after inlining through the structs)
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
 struct SWin {
-  uint32_t* S;
-  int nth;
+  uint32_t sa;  // shared address of window limb 0 of this thread
+  uint32_t sb;  // byte stride between window limbs (4 * threads sharing the window array)
   int L;
   bool xa;     // X = a (Y = t) or X = t (Y = a)
   bool sub;    // effective subtraction
@@ -31,12 +42,17 @@ struct SWin {
   bool sticky;
   uint32_t curA;
 
-  __device__ __forceinline__ uint32_t get(int wi) const {
-    return (wi >= 0 && wi <= L + 1) ? S[wi * nth] : 0u;
+  __device__ __forceinline__ void base(uint32_t* S, int nth) {
+    sa = (uint32_t)__cvta_generic_to_shared(S);
+    sb = 4u * (uint32_t)nth;
   }
-  __device__ __forceinline__ void set(int wi, uint32_t v) { S[wi * nth] = v; }
+  __device__ __forceinline__ uint32_t at(int wi) const { return sa + (uint32_t)wi * sb; }
+  __device__ __forceinline__ uint32_t get(int wi) const {
+    return (wi >= 0 && wi <= L + 1) ? lds32(at(wi)) : 0u;
+  }
+  __device__ __forceinline__ void set(int wi, uint32_t v) { sts32(at(wi), v); }
   // a limb l (0 <= l < L) lives in window slot l + 1 until overwritten
-  __device__ __forceinline__ uint32_t aload(int l) const { return (l >= 0 && l < L) ? S[(l + 1) * nth] : 0u; }
+  __device__ __forceinline__ uint32_t aload(int l) const { return (l >= 0 && l < L) ? lds32(at(l + 1)) : 0u; }
 
   __device__ __forceinline__ void emit(uint32_t X, uint32_t Yb) {
     uint32_t s;
@@ -49,7 +65,7 @@ struct SWin {
       s = (uint32_t)t;
       cb = (uint32_t)(t >> 32);
     }
-    S[w * nth] = s;
+    set(w, s);
     w++;
   }
 
@@ -67,8 +83,8 @@ struct SWin {
     dr = (int)(shift & 31);
     prev = 0; q = 0; w = 0; cb = 0; sticky = false; curA = 0;
     if (xa) {
-      S[0] = 0u;
-      S[(L + 1) * nth] = 0u;
+      set(0, 0u);
+      set(L + 1, 0u);
       return;
     }
     if (yzero) {
@@ -94,7 +110,7 @@ struct SWin {
       } else {
         if (wq == 0 && dr > 0 && (prev & ((1u << dr) - 1u))) sticky = true;
         uint32_t Yb = dr ? ((prev >> dr) | (T << (32 - dr))) : prev;
-        emit((wq >= 1 && wq <= L) ? S[wq * nth] : 0u, Yb);
+        emit((wq >= 1 && wq <= L) ? lds32(at(wq)) : 0u, Yb);
       }
       prev = T;
       q++;
@@ -127,7 +143,7 @@ struct SWin {
       // window limb w <- funnel(T_{w-1+dq}, T_{w+dq}, dr); X = a limb in slot w
       uint32_t X[NL];
 #pragma unroll
-      for (int k = 0; k < NL; k++) X[k] = S[(w + k) * nth];  // all loads first (ILP)
+      for (int k = 0; k < NL; k++) X[k] = lds32(at(w + k));  // all loads first (ILP)
       uint32_t pt = prev;
 #pragma unroll
       for (int k = 0; k < NL; k++) {
@@ -146,7 +162,7 @@ struct SWin {
         X[k] = s;
       }
 #pragma unroll
-      for (int k = 0; k < NL; k++) S[(w + k) * nth] = X[k];
+      for (int k = 0; k < NL; k++) sts32(at(w + k), X[k]);
       w += NL;
       prev = pt;
       q += NL;
@@ -154,7 +170,7 @@ struct SWin {
       // window limb w <- T_{w-1} -/+ funnel(a_{w-1+dq}, a_{w+dq}, dr)
       uint32_t Av[NL];
 #pragma unroll
-      for (int k = 0; k < NL; k++) Av[k] = S[(w + k + dq + 1) * nth];  // a limbs (w+k+dq): loads first
+      for (int k = 0; k < NL; k++) Av[k] = lds32(at(w + k + dq + 1));  // a limbs (w+k+dq): loads first
 #pragma unroll
       for (int k = 0; k < NL; k++) {
         uint32_t yb = __funnelshift_r(curA, Av[k], dr);
@@ -173,7 +189,7 @@ struct SWin {
         T[k] = s;
       }
 #pragma unroll
-      for (int k = 0; k < NL; k++) S[(w + k) * nth] = T[k];
+      for (int k = 0; k < NL; k++) sts32(at(w + k), T[k]);
       w += NL;
     }
   }
@@ -325,24 +341,27 @@ struct Emit {
 // class.  E is the exponent of the window's X operand.
 __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,
                                             int64_t so, int32_t* oexp, uint8_t* ocls, int32_t* status) {
-  uint32_t* Sw = S.S;
-  const int nth = S.nth;
+  const uint32_t sb = S.sb;
   // ---- normalise, round to nearest-even, write the result (coalesced)
   if (S.sub && S.cb) {  // negative (only possible when exponents are equal)
     uint32_t c = 1;
-    for (int wi = 0; wi <= L + 1; wi++) {
-      uint64_t v = (uint64_t)(uint32_t)~S.get(wi) + c;
-      S.set(wi, (uint32_t)v);
-      c = (uint32_t)(v >> 32);
+    uint32_t ad = S.at(0);
+    for (int wi = 0; wi <= L + 1; wi++, ad += sb) {
+      uint32_t v = ~lds32(ad) + c;
+      c = (c && v == 0u) ? 1u : 0u;
+      sts32(ad, v);
     }
     neg ^= 1;
   }
   int h = -1;
-  for (int wi = L + 1; wi >= 0; wi--) {
-    uint32_t v = S.get(wi);
-    if (v) {
-      h = 32 * wi + 31 - __clz(v);
-      break;
+  {
+    uint32_t ad = S.at(L + 1);
+    for (int wi = L + 1; wi >= 0; wi--, ad -= sb) {
+      uint32_t v = lds32(ad);
+      if (v) {
+        h = 32 * wi + 31 - __clz(v);
+        break;
+      }
     }
   }
   if (h < 0) {  // exact cancellation -> +0
@@ -371,10 +390,15 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
   }
   uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
   uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
+  // 0 <= off <= 33 here, so base = off >> 5 is 0 or 1 and the window limbs
+  // base + l + 1 (l < L) stay inside [0, L + 1]
   const int base = off >> 5, rs = off & 31;
-  uint32_t lo = S.get(base);
+  uint32_t ad = S.at(base);
+  uint32_t lo = lds32(ad);
+  ad += sb;
   {
-    uint32_t hi = S.get(base + 1);
+    uint32_t hi = lds32(ad);
+    ad += sb;
     uint32_t v = __funnelshift_r(lo, hi, rs);
     lo = hi;
     if (zb) v &= ~((1u << zb) - 1u);
@@ -383,16 +407,17 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
     carry = rr < v ? 1u : 0u;
     O[0] = rr;
   }
-  // S.get(base + l + 1) for l >= 1 stays inside the window: base + L <= L + 1
-  const uint32_t* Wp = Sw + (base + 2) * nth;
+  uint32_t* Op = O + so;
 #pragma unroll 4
   for (int l = 1; l < L; l++) {
-    uint32_t hi = (base + l + 1 <= L + 1) ? Wp[(l - 1) * nth] : 0u;
+    uint32_t hi = lds32(ad);
+    ad += sb;
     uint32_t v = __funnelshift_r(lo, hi, rs);
     lo = hi;
     uint32_t rr = v + carry;
     carry = rr < v ? 1u : 0u;
-    O[(int64_t)l * so] = rr;
+    *Op = rr;
+    Op += so;
   }
   if (carry) {
     O[(int64_t)(L - 1) * so] = 0x80000000u;

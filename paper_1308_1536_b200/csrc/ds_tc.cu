@@ -1,0 +1,530 @@
+// ds_tc.cu -- the update a_jk <- RN(a_jk - RN(z_j * b_k)) (elim.py:49-52) with
+// the mantissa products on the 5th-generation tensor cores.
+//
+// z_j * b_k = sum_c col_c 2^(8c),  col_c = sum_s B_k[s] Z_j[c - s]  over the
+// unsigned 8-bit digits (bytes) of the left-aligned mantissas.  For 128
+// consecutive columns k of the pivot row and one row j this is one int8 GEMM
+//     D[k][c] = sum_s B[k][s] * T_j[s][c],   T_j[s][c] = Z_j[c - s]  (Toeplitz)
+// computed by tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32) into TMEM:
+// M = 128 columns k (TMEM lanes), N = 176 output digit columns per tile, K =
+// 32 digits per instruction.  Only digit columns c >= c_lo are formed (short
+// product: the omitted part E is >= 0 and < D8*2^8 units of 2^(8 c_lo)); the
+// rounding of z*b is decided from the computed columns unless the bits under
+// the round bit are all ones (or a possible tie), in which case the element is
+// handed to the exact general engine through a fallback list (probability
+// ~2^-40 on non-exact data).
+//
+// CTA roles (256 threads; one CTA = 128 columns x RBR rows):
+//   warps 0-3  epilogue: thread = column k = TMEM lane, so a warp touches 32
+//              consecutive a_jk of one row (coalesced in the plane-major SoA);
+//              tcgen05.ld of 16 digit columns at a time, carry propagation
+//              into 8-bit digits, 4 digits = one 32-bit limb of P, then the
+//              shared rounding stream (ds_stream.cuh: round to t, exact
+//              a -/+ t window in shared memory with a's limbs prefetched by
+//              cp.async, RN, store).
+//   warps 4-7  producers: per row, 16 pre-shifted copies of the row's reversed
+//              digits; per MMA, a K-major Toeplitz tile in a shared-memory ring
+//              (one LDS.128 + STS.128 per 16-byte chunk); one elected thread
+//              issues the MMAs and commits to mbarriers.
+// The pivot-row digits of the CTA's 128 columns stay in shared memory
+// (canonical no-swizzle K-major layout) for all its rows.  TMEM holds two
+// 176-column accumulator buffers (the epilogue of one tile overlaps the MMAs
+// of the next).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../../include/detseries_b200.h"
+#include "ds_mp.cuh"
+#include "ds_stream.cuh"
+#include "ds_tc.cuh"
+
+namespace {
+
+using namespace dss;
+
+constexpr int TM = 128;      // columns per CTA (TMEM lanes)
+constexpr int TN = 176;      // output digit columns per MMA tile
+constexpr int KS = 32;       // digits per MMA K step
+constexpr int NSLOT = 6;     // B-tile ring
+constexpr int NPROD = 128;   // producer threads
+constexpr int RBR = 8;       // rows per CTA
+
+struct TcArgs {
+  int p, L, zb, D8p, nks, ntiles, c_lo, eps;
+  int nrows, ncols, kstart, skip_col, n;
+  int jl0;
+  const uint8_t* zbytes;   // [nrows][D8p]
+  const uint8_t* bbytes;   // [n][D8p]
+  const double* zf;        // [nrows]
+  const double* bf;        // [n]
+  const int32_t* zexp;     // z meta, offset by jl0
+  const uint8_t* zcls;
+  const int32_t* bexp;     // pivot row meta
+  const uint8_t* bcls;
+  uint32_t* a_limbs;
+  int32_t* a_exp;
+  uint8_t* a_cls;
+  int64_t a_count;
+  int32_t* status;
+  int step;
+  int* fb_count;           // fallback list
+  int2* fb_list;
+  int fb_cap;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
+// the phase completes instead of spinning through issue slots
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(1000000));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc));
+}
+__device__ __forceinline__ void cp4(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_wait_all() {
+  asm volatile("cp.async.commit_group;");
+  asm volatile("cp.async.wait_group 0;");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count));
+}
+
+// ---------------------------------------------------------------- prep
+// bytes of the left-aligned mantissa (= the 32-bit limbs, little-endian),
+// zero padded to D8p; one thread per (element, limb)
+__global__ void k_tc_bytes(const uint32_t* src, int64_t count, int num, int L, int D8p, uint8_t* dst, double* topf) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int W = D8p / 4;
+  if (t >= (int64_t)num * W) return;
+  int e = (int)(t / W), l = (int)(t % W);
+  uint32_t v = l < L ? src[(int64_t)l * count + e] : 0u;
+  ((uint32_t*)(dst + (int64_t)e * D8p))[l] = v;
+  if (l == 0) {
+    uint64_t top = ((uint64_t)src[(int64_t)(L - 1) * count + e] << 32) | src[(int64_t)(L - 2) * count + e];
+    topf[e] = (double)top * 0x1p-63;
+  }
+}
+
+// ---------------------------------------------------------------- main
+struct Smem {
+  uint8_t* As;    // nks * TM * KS: pivot-row digits of the CTA's 128 columns (K-major)
+  uint8_t* Bs;    // NSLOT * TN * KS: Toeplitz tiles of the current row's digits
+  uint8_t* rbq;   // 16 * RBL: shifted copies of the reversed row digits
+  uint32_t* Sw;   // (L + 2) * TM: per-column S windows
+  uint32_t* zw;   // ZWL bytes: the current row's digits with zero padding
+};
+
+// Roles: TMEM lane = column k (128 consecutive columns of the pivot row), so
+// the epilogue warp's 32 lanes touch 32 consecutive a_jk of one row (coalesced
+// 128-byte accesses in the plane-major SoA); the CTA walks RB rows j.  z*b is
+// symmetric, so A = pivot-row digits (staged once) and B = Toeplitz(z_j).
+__global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_empty[NSLOT];
+  __shared__ __align__(8) uint64_t bar_tfull[2];
+  __shared__ __align__(8) uint64_t bar_tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nks = a.nks, ntiles = a.ntiles, L = a.L;
+  const int T0 = a.c_lo + ntiles * TN - 1;  // largest digit index a tile can ask for
+  const int zbase = (T0 - RBL - 48) & ~3;   // zw[v] = Z[zbase + v]
+  const int ZWL = RBL + 96;
+  Smem s;
+  s.As = smem;
+  s.Bs = s.As + nks * TM * KS;
+  s.rbq = s.Bs + NSLOT * TN * KS;
+  s.Sw = (uint32_t*)(s.rbq + 16 * RBL);
+  s.zw = s.Sw + (L + 2) * TM;
+  const int kbase = a.kstart + blockIdx.x * TM;
+  const int row0 = blockIdx.y * RB;
+  const int nrow_cta = min(RB, a.nrows - row0);
+
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; i++) mbar_init(&bar_empty[i], 1);
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&bar_tfull[i], 1);
+      mbar_init(&bar_tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // pivot-row digits -> As (canonical K-major: [ks][half][lanegroup][lane%8][16B])
+  for (int c = tid; c < TM * nks * 2; c += 256) {
+    int r = c / (nks * 2), q = c % (nks * 2);
+    int ks = q >> 1, h = q & 1;
+    uint8_t* dst = s.As + ks * TM * KS + h * TM * 16 + (r >> 3) * 128 + (r & 7) * 16;
+    if (kbase + r < a.n) cp16(dst, a.bbytes + (int64_t)(kbase + r) * a.D8p + ks * KS + h * 16);
+    else *(uint4*)dst = make_uint4(0, 0, 0, 0);
+  }
+  cp_wait_all();
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp >= 4) {
+    // =================================================== producers + MMA issuer
+    const int ptid = tid - 128;
+    int it = 0;  // B-slot iteration counter
+    for (int ri = 0; ri < nrow_cta; ri++) {
+      const uint8_t* zrow = a.zbytes + (int64_t)(row0 + ri) * a.D8p;
+      named_sync(1, NPROD);  // the previous row's tiles no longer read rbq / zw
+      // zero-padded window of the row's digits (word granular: D8p, zbase = 0 mod 4)
+      for (int v = ptid; v < ZWL / 4; v += NPROD) {
+        int t = zbase + 4 * v;
+        s.zw[v] = (t >= 0 && t < a.D8p) ? *(const uint32_t*)(zrow + t) : 0u;
+      }
+      named_sync(1, NPROD);
+      // rbq[q][y] = rb[y + q],  rb[x] = Z[T0 - x]: chunk (q, y0) = reversed
+      // Z[u .. u+16), u = T0 - y0 - q - 15  (funnel-shifted words + byte reversal)
+      for (int c = ptid; c < RBL; c += NPROD) {
+        int q = c / (RBL / 16), y0 = (c % (RBL / 16)) * 16;
+        int off = T0 - y0 - q - 15 - zbase;
+        const uint32_t* wp = s.zw + (off >> 2);
+        int sh = 8 * (off & 3);
+        uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+        uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
+        uint32_t x2 = __funnelshift_r(w2, w3, sh), x3 = __funnelshift_r(w3, w4, sh);
+        *(uint4*)(s.rbq + q * RBL + y0) =
+            make_uint4(__byte_perm(x3, 0, 0x0123), __byte_perm(x2, 0, 0x0123), __byte_perm(x1, 0, 0x0123),
+                       __byte_perm(x0, 0, 0x0123));
+      }
+      named_sync(1, NPROD);
+      for (int t = 0; t < ntiles; t++) {
+        const int gt = ri * ntiles + t;  // CTA-wide tile counter
+        const int buf = gt & 1;
+        const int c0 = a.c_lo + t * TN;
+        int s_lo = c0 - (a.D8p - 1);
+        if (s_lo < 0) s_lo = 0;
+        int s_hi = c0 + TN - 1;
+        if (s_hi > a.D8p - 1) s_hi = a.D8p - 1;
+        const int ks0 = s_lo / KS, ks1 = s_hi / KS;
+        for (int ks = ks0; ks <= ks1; ks++, it++) {
+          const int slot = it % NSLOT;
+          mbar_wait(&bar_empty[slot], ((it / NSLOT) & 1) ^ 1);
+          uint8_t* B = s.Bs + slot * TN * KS;
+          // chunk (n, h): bytes kk = 16h..16h+15 of row n -> rb[x0 .. x0+16),
+          // x0 = T0 - c0 - n + 32 ks + 16 h
+          for (int c = ptid; c < TN * 2; c += NPROD) {
+            int n = c >> 1, h = c & 1;
+            int x0 = T0 - c0 - n + KS * ks + 16 * h;
+            uint4 v = *(const uint4*)(s.rbq + (x0 & 15) * RBL + (x0 & ~15));
+            *(uint4*)(B + h * TN * 16 + (n >> 3) * 128 + (n & 7) * 16) = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;");
+          named_sync(1, NPROD);
+          if (ptid == 0) {
+            if (ks == ks0 && gt >= 2) mbar_wait(&bar_tempty[buf], ((gt >> 1) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            uint64_t ad = umma_desc(smem_u32(s.As + ks * TM * KS), TM * 16, 128);
+            uint64_t bd = umma_desc(smem_u32(B), TN * 16, 128);
+            uint32_t acc = ks > ks0 ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + buf * TN),
+                "l"(ad), "l"(bd), "r"(idesc_i8(TM, TN)), "r"(acc));
+            umma_commit(&bar_empty[slot]);
+            if (ks == ks1) umma_commit(&bar_tfull[buf]);
+          }
+        }
+      }
+    }
+  } else {
+    // =================================================== epilogue (lane = column)
+    const int r = tid;
+    const int k = kbase + r;
+    const bool col_ok = k < a.n && k != a.skip_col;
+    uint32_t* Sw = s.Sw + r;  // window limb w at Sw[w * TM]
+    for (int ri = 0; ri < nrow_cta; ri++) {
+      const int zr = row0 + ri;  // row index relative to jl0
+      const int jl = a.jl0 + zr;
+      const int64_t idx = (int64_t)jl * a.n + k;
+      // ---- element setup (mirrors ds_update.cu fused_element)
+      bool process = false, fallback = false;
+      int neg = 0, norm = 0;
+      int64_t E = 0, d = 0;
+      bool xa = false, sub = false, za = false;
+      if (col_ok) {
+        uint8_t cz = a.zcls[zr], cb = a.bcls[k], ca = a.a_cls[idx];
+        za = ca >= DS_CLS_PZERO;
+        int sa = ca & 1, st = (cz & 1) ^ (cb & 1);
+        if (cz >= DS_CLS_PZERO || cb >= DS_CLS_PZERO) {
+          if (za) a.a_cls[idx] = (sa && !st) ? DS_CLS_NZERO : DS_CLS_PZERO;
+        } else {
+          int32_t ea = za ? 0 : a.a_exp[idx];
+          double pr = a.zf[zr] * a.bf[k];
+          norm = pr >= 2.0 ? 1 : 0;
+          bool confident = fabs(pr - 2.0) > 0x1p-42;
+          int64_t ebase = (int64_t)a.zexp[zr] + a.bexp[k];
+          if (!za && (int64_t)ea - (ebase - 1) >= (int64_t)a.p + 3) {
+            // a dominates whatever the normalisation: unchanged
+          } else if (!confident) {
+            fallback = true;
+          } else {
+            int64_t et = ebase - (norm ? 0 : 1);
+            d = za ? -(int64_t)(1 << 30) : (int64_t)ea - et;
+            if (za || d < (int64_t)a.p + 2) {
+              xa = !za && d >= 0;
+              sub = !za && (sa == st);
+              neg = xa ? sa : (st ^ 1);
+              E = xa ? ea : et;
+              process = true;
+            }
+          }
+        }
+      }
+      // prefetch a's limbs into the window (slots 1..L): coalesced across the warp
+      if (process && !za) {
+        const uint32_t* A = a.a_limbs + idx;
+#pragma unroll 4
+        for (int l = 0; l < L; l++) cp4(Sw + (l + 1) * TM, A + (int64_t)l * a.a_count);
+      }
+      cp_wait_all();
+      SWin S;
+      S.base(Sw, TM);
+      Emit em;
+      if (process) {
+        S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
+        em.S = &S;
+        em.r = (norm ? a.p : a.p - 1) + 2 * a.zb;  // t's LSB in P' = M_z * M_b
+        em.zb = a.zb;
+        em.p = a.p;
+        em.L = L;
+        em.exact = false;
+        em.onesided = true;
+        em.lo_chk = 8 * a.c_lo + a.eps;
+        em.hi_chk = em.r - 2;
+        em.allz = true; em.allo = true; em.sticky = false; em.decided = false;
+        em.rbit = 0; em.tcarry = 0; em.tl = 0; em.excess = false;
+        em.setup();
+      }
+      bool ok = true;
+      uint32_t carry = 0;
+      for (int t = 0; t < ntiles; t++) {
+        const int gt = ri * ntiles + t;
+        const int buf = gt & 1;
+        mbar_wait(&bar_tfull[buf], (gt >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + buf * TN;
+#pragma unroll 1
+        for (int cb = 0; cb < TN; cb += 16) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15])
+              : "r"(taddr + cb));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (process && ok) {
+            // limb g = sum_j v[4g+j] 2^(8j) + carry (< 2^51): 4 wide multiply-adds,
+            // low word = the limb, high word = the carry into the next limb
+            uint32_t P[4];
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+              uint64_t acc = (uint64_t)v[4 * g] + carry;
+              acc += (uint64_t)v[4 * g + 1] * 256u;
+              acc += (uint64_t)v[4 * g + 2] * 65536u;
+              acc += (uint64_t)v[4 * g + 3] * 16777216u;
+              P[g] = (uint32_t)acc;
+              carry = (uint32_t)(acc >> 32);
+            }
+            const int g0 = (a.c_lo + t * TN + cb) >> 2;
+            ok = em.block<4>(g0, P);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_tempty[buf]);
+      }
+      if (process && ok) {
+        em.finish(carry ? 1.0 : 0.0);
+        if (em.excess) ok = false;
+      }
+      if (process && !ok) fallback = true;
+      if (process && ok) {
+        round_write(S, neg, E, L, a.p, a.zb, a.a_limbs + idx, a.a_count, a.a_exp + idx, a.a_cls + idx, a.status);
+      } else if (fallback) {
+        int slot = atomicAdd(a.fb_count, 1);
+        if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
+        else atomicAdd(&a.status[5], 1);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// exact general-engine update of the listed elements (undecided short
+// products / uncertain normalisation): mul_rn then add_rn (ds_mp.cuh)
+__global__ void k_tc_fallback(TcArgs a, const uint32_t* z_limbs, int64_t z_count, const uint32_t* b_limbs,
+                              uint32_t* scratch, int64_t sthreads) {
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  int cnt = *a.fb_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && cnt > 0) atomicAdd(&a.status[6], cnt);
+  if (cnt > a.fb_cap) cnt = a.fb_cap;
+  const int L = a.L;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x) {
+    int2 e = a.fb_list[q];
+    int jl = e.x, k = e.y;
+    int64_t idx = (int64_t)jl * a.n + k;
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ds::Ptr tmp{scratch + tid, sthreads};
+    ds::Ptr tv = tmp, work = tmp.off(2 * (int64_t)L + 4), res = work.off(2 * (int64_t)L + 4);
+    ds::Val z{ds::CPtr{z_limbs + jl, z_count}, a.zexp[jl - a.jl0], a.zcls[jl - a.jl0]};
+    ds::Val b{ds::CPtr{b_limbs + k, a.n}, a.bexp[k], a.bcls[k]};
+    int32_t te;
+    uint8_t tc;
+    ds::mul_rn(tv, &te, &tc, z, b, L, a.p, work);
+    ds::Val t{ds::CPtr{tv.p, tv.s}, te, tc};
+    ds::Val av{ds::CPtr{a.a_limbs + idx, a.a_count}, a.a_exp[idx], a.a_cls[idx]};
+    int32_t re;
+    uint8_t rc;
+    if (!ds::add_rn(res, &re, &rc, av, t, true, L, a.p, work)) atomicAdd(&a.status[2], 1);
+    for (int l = 0; l < L; l++) a.a_limbs[(int64_t)l * a.a_count + idx] = res[l];
+    a.a_exp[idx] = re;
+    a.a_cls[idx] = rc;
+  }
+}
+
+size_t tc_smem(int nks, int L, int D8p, int RBL) {
+  return (size_t)nks * TM * KS + (size_t)NSLOT * TN * KS + 16 * (size_t)RBL + 4 * (size_t)(L + 2) * TM + RBL + 96;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host
+struct TcWork {
+  uint8_t* zbytes;
+  uint8_t* bbytes;
+  double* zf;
+  double* bf;
+  int* fb_count;
+  int2* fb_list;
+  uint32_t* scratch;
+  int64_t sthreads;
+  int fb_cap;
+};
+
+int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
+  memset(plan, 0, sizeof(*plan));
+  if (getenv("DS_DISABLE_TC")) return DS_OK;
+  plan->p = p;
+  plan->L = (p + 31) / 32;
+  plan->D8p = ((4 * plan->L + KS - 1) / KS) * KS;
+  plan->nks = plan->D8p / KS;
+  int zb = 32 * plan->L - p;
+  int lg = 0;
+  while ((1 << lg) < plan->D8p) lg++;
+  plan->eps = 9 + lg;
+  // t's LSB in P' is at r' >= p - 1 + 2 zb; keep >= 32 decision bits above eps
+  int rmin = p - 1 + 2 * zb;
+  int clo = (rmin - 2 - 32 - plan->eps) / 8;
+  clo &= ~3;
+  if (clo < 0) clo = 0;
+  plan->c_lo = clo;
+  plan->ntiles = (2 * plan->D8p - clo + TN - 1) / TN;
+  plan->RBL = ((plan->ntiles * TN + KS * plan->nks + 32) + 15) & ~15;
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  size_t smem = tc_smem(plan->nks, plan->L, plan->D8p, plan->RBL) + 1024;
+  if ((int)smem > maxsm - 2048 || p < 256) return DS_OK;  // not applicable: other engines
+  if (cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DS_CUDA;
+  plan->smem = smem;
+  TcWork* w = new TcWork();
+  memset(w, 0, sizeof(*w));
+  w->fb_cap = 1 << 16;
+  w->sthreads = 64 * 128;
+  bool ok = cudaMalloc(&w->zbytes, (size_t)plan->D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
+            cudaMalloc(&w->bbytes, (size_t)plan->D8p * n) == cudaSuccess &&
+            cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
+            cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
+            cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
+            cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)plan->L + 96)) == cudaSuccess;
+  plan->work = w;
+  if (!ok) return DS_OOM;
+  plan->enabled = 1;
+  return DS_OK;
+}
+
+void tc_plan_free(TcPlan* plan) {
+  TcWork* w = (TcWork*)plan->work;
+  if (!w) return;
+  void* ptrs[] = {w->zbytes, w->bbytes, w->zf, w->bf, w->fb_count, w->fb_list, w->scratch};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete w;
+  plan->work = nullptr;
+}
+
+int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
+                     int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
+                     const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
+                     int64_t* launches) {
+  TcWork* w = (TcWork*)plan->work;
+  const int L = plan->L;
+  const int nrows = nloc - jl0;
+  const int kstart = collect_minors ? 0 : i + 1;
+  const int ncols = n - kstart;
+  if (nrows <= 0 || ncols <= 0) return DS_OK;
+  const uint32_t* b_limbs = (const uint32_t*)pbuf;
+  const int32_t* b_exp = (const int32_t*)(pbuf + (size_t)4 * L * n);
+  const uint8_t* b_cls = (const uint8_t*)(pbuf + (size_t)4 * L * n + (size_t)4 * n);
+  const int W4 = plan->D8p / 4;
+  k_tc_bytes<<<(unsigned)(((int64_t)nrows * W4 + 255) / 256), 256, 0, s>>>(z_limbs + jl0, nloc, nrows, L, plan->D8p,
+                                                                          w->zbytes, w->zf);
+  k_tc_bytes<<<(unsigned)(((int64_t)n * W4 + 255) / 256), 256, 0, s>>>(b_limbs, n, n, L, plan->D8p, w->bbytes, w->bf);
+  cudaMemsetAsync(w->fb_count, 0, sizeof(int), s);
+  TcArgs a;
+  a.p = plan->p; a.L = L; a.zb = 32 * L - plan->p; a.D8p = plan->D8p; a.nks = plan->nks; a.ntiles = plan->ntiles;
+  a.c_lo = plan->c_lo; a.eps = plan->eps;
+  a.nrows = nrows; a.ncols = ncols; a.kstart = kstart; a.skip_col = i; a.n = n; a.jl0 = jl0;
+  a.zbytes = w->zbytes; a.bbytes = w->bbytes; a.zf = w->zf; a.bf = w->bf;
+  a.zexp = z_exp + jl0; a.zcls = z_cls + jl0; a.bexp = b_exp; a.bcls = b_cls;
+  a.a_limbs = a_limbs; a.a_exp = a_exp; a.a_cls = a_cls; a.a_count = a_count;
+  a.status = status; a.step = i;
+  a.fb_count = w->fb_count; a.fb_list = w->fb_list; a.fb_cap = w->fb_cap;
+  dim3 grid((ncols + TM - 1) / TM, (nrows + RBR - 1) / RBR);
+  k_update_tc<<<grid, 256, plan->smem, s>>>(a, plan->RBL, RBR);
+  k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
+  *launches += 4;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DS_OK : DS_CUDA;
+}

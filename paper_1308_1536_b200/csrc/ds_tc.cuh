@@ -1,0 +1,19 @@
+// ds_tc.cuh -- interface of the tensor-core (tcgen05 kind::i8) real update (ds_tc.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+struct TcPlan {
+  int enabled;
+  int p, L, D8p, nks;  // precision, 32-bit limbs, 8-bit digits (padded to the MMA K), K steps
+  int c_lo, ntiles, eps, RBL;
+  size_t smem;
+  void* work;
+};
+
+int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device);
+void tc_plan_free(TcPlan* plan);
+int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
+                     int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
+                     const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
+                     int64_t* launches);

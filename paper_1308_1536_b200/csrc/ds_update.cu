@@ -282,8 +282,7 @@ __device__ void fused_element(const UArgs& a, const double* zrow, const double* 
 
   const int lane = threadIdx.x & 31;
   SWin S;
-  S.S = Sw;
-  S.nth = nth;
+  S.base(Sw, nth);
   Emit em;
   bool done = false;
   for (int attempt = 0; attempt < 2 && !done; attempt++) {
@@ -401,6 +400,15 @@ __global__ void __launch_bounds__(128) k_mul_split(UArgs a, int nbs) {
   fused_element<W, 1, true>(a, xs, yw, Sw + warp * (L + 2), 1, 0, k, oidx, blk + warp * nbs * (W + 1));
 }
 
+// highest digit column of z*b that can be nonzero: P < 2^(2p) needs columns
+// <= (2p-1)/24, but when p = 0 mod 24 the balanced top digit d_{D-1} (the
+// borrow of u_{D-2} >= 2^23) can be 1 and its column 2D-2 must be summed too
+// (it cancels the -1 carry out of the column below).
+static int top_column(int p) {
+  int D = (p + 23) / 24 + 1;
+  return p % 24 == 0 ? 2 * D - 2 : (2 * p - 1) / 24;
+}
+
 static int split_smem(int W, int Db, int L, int cmax, int c_lo, int wpb) {
   int nbs = (cmax - c_lo) / W + 1;
   return 8 * ((Db + W + 1) + wpb * (Db + 3 * W) + wpb * nbs * (W + 1)) + 4 * wpb * (L + 2);
@@ -478,7 +486,7 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   {
     int clo = ((p - 2) / 24 - GUARD) & ~3;
     if (clo < 0) clo = 0;
-    if (split_smem(4, plan->D, plan->L, (2 * p - 1) / 24, clo, 4) > maxsm) return DS_OK;
+    if (split_smem(4, plan->D, plan->L, top_column(p), clo, 4) > maxsm) return DS_OK;
   }
   plan->enabled = 1;
   return DS_OK;
@@ -518,7 +526,7 @@ static void base_args(UpdatePlan* plan, UArgs& a, int32_t* status) {
   a.p = p; a.L = plan->L; a.Db = plan->D; a.zb = 32 * plan->L - p;
   int clo = ((p - 2) / 24 - GUARD) & ~3;  // blocks start on whole limbs
   a.c_lo = clo > 0 ? clo : 0;
-  a.cmax = (2 * p - 1) / 24;
+  a.cmax = top_column(p);
   int lg = 0;
   while ((1 << lg) < plan->D) lg++;
   a.eps = 23 + lg;

@@ -164,6 +164,12 @@ class DeviceElimination:
                "ds_profile_read", self.rank)
         return ms.value, n.value, w.value
 
+    def counters(self) -> dict:
+        """Internal engine counters (ds_counters): tensor-core fallback elements, active update engine."""
+        out = (ctypes.c_int64 * 3)()
+        _check(self.lib.ds_counters(self.ctx, out, 3), self.ctx, "ds_counters", self.rank)
+        return {"tc_fallback_elements": int(out[0]), "tc_engine": bool(out[1]), "dfma_engine": bool(out[2])}
+
     def stream(self) -> int:
         return self.lib.ds_stream(self.ctx) or 0
 

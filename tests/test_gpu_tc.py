@@ -1,0 +1,63 @@
+"""Tensor-core update (ds_tc.cu, tcgen05 kind::i8) against the oracle and
+against the DFMA update engine (ds_update.cu, selected with DS_DISABLE_TC):
+several 128-row tiles, many columns per CTA (TMEM double-buffer reuse), the
+column range with and without collected minors, ragged tails."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from _util import first_mismatch, results_digest
+from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+from paper_1308_1536_b200.synth import random_uniform_soa
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_run(A, n, p, steps, minors, env=None):
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        with DeviceElimination(n, p, "real") as eng:
+            eng.load(A)
+            res = HostResults.alloc(n, 1, eng.L, minors)
+            eng.run(minors, True, 0, steps, res)
+            fin = A.copy()
+            eng.fetch(fin)
+            return res, fin
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,p,steps", [(150, 4096, 3), (261, 1024, 5), (140, 2000, 4), (130, 333, 6)])
+def test_tc_matches_oracle(n, p, steps):
+    A = random_uniform_soa(n, p, seed=n + p)
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res_o = HostResults.alloc(n, 1, ref.L, True)
+    ref.run(True, True, 0, steps, res_o)
+    fin_o = A.copy()
+    ref.fetch(fin_o)
+    res_d, fin_d = _device_run(A, n, p, steps, True)
+    mism = first_mismatch(fin_o, fin_d, p)
+    assert not mism, mism
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+@pytest.mark.parametrize("minors", [True, False])
+@pytest.mark.parametrize("n,p,steps", [(600, 4096, 40), (1000, 1024, 200)])
+def test_tc_matches_dfma_engine(n, p, steps, minors):
+    A = random_uniform_soa(n, p, seed=7 * n + p)
+    res_t, fin_t = _device_run(A, n, p, steps, minors)
+    res_f, fin_f = _device_run(A, n, p, steps, minors, env={"DS_DISABLE_TC": "1"})
+    assert np.array_equal(fin_t.cls, fin_f.cls)
+    assert np.array_equal(fin_t.exp, fin_f.exp)
+    assert np.array_equal(fin_t.limbs, fin_f.limbs)
+    assert results_digest(res_f, fin_f, n, p, steps) == results_digest(res_t, fin_t, n, p, steps)

@@ -1,9 +1,13 @@
-"""Quick timing probe of full eliminations on one GPU (not the bench)."""
+"""Quick timing probe of full eliminations on one GPU (not the bench).
+
+usage: python tools/probe_perf.py 1000@4096 2000@4096 ...
+Prints wall time, update-kernel time (profile events), the engine counters
+(tensor-core fallback elements, which update engine ran)."""
 import sys
 import time
 
 sys.path.insert(0, ".")
-import torch  # noqa: E402
+import torch  # noqa: E402,F401
 
 from paper_1308_1536_b200.engine import DeviceElimination, HostResults  # noqa: E402
 from paper_1308_1536_b200.synth import random_uniform_soa  # noqa: E402
@@ -15,9 +19,12 @@ for spec in sys.argv[1:]:
     with DeviceElimination(n, p, "real") as eng:
         res = HostResults.alloc(n, 1, L, True)
         eng.load(A)
+        eng.profile(True)
         t0 = time.perf_counter()
         rc, done = eng.run(True, True, 0, n, res)
         t1 = time.perf_counter()
+        ms, nl, w = eng.profile_read()
         work = n * (n - 1) ** 2 / 2 * L * L
         print(f"n={n} p={p} done={done} wall={t1 - t0:.3f}s (incl. results D2H) "
-              f"limb-MAC/s={work / (t1 - t0):.3e} launches={eng.launches()}", flush=True)
+              f"limb-MAC/s={work / (t1 - t0):.3e} update={ms / 1e3:.3f}s ({w / (ms * 1e-3):.3e}/s over {nl} launches) "
+              f"launches={eng.launches()} {eng.counters()}", flush=True)
