@@ -28,6 +28,45 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
+// s = x + y + cy over N limbs (low -> high) with the PTX carry chain;
+// cy (0/1) in, carry out.  Chains of 4 and 2 limbs, the carry handed over in
+// a register between them.
+__device__ __forceinline__ void addc4(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %4, 0xffffffff;\n\t"
+      "addc.cc.u32 %0, %5, %9;\n\t"
+      "addc.cc.u32 %1, %6, %10;\n\t"
+      "addc.cc.u32 %2, %7, %11;\n\t"
+      "addc.cc.u32 %3, %8, %12;\n\t"
+      "addc.u32 %4, 0, 0;\n\t}"
+      : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "+r"(cy)
+      : "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]));
+}
+__device__ __forceinline__ void addc2(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %2, 0xffffffff;\n\t"
+      "addc.cc.u32 %0, %3, %5;\n\t"
+      "addc.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %2, 0, 0;\n\t}"
+      : "=r"(s[0]), "=r"(s[1]), "+r"(cy)
+      : "r"(x[0]), "r"(x[1]), "r"(y[0]), "r"(y[1]));
+}
+__device__ __forceinline__ void addc1(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %1, 0xffffffff;\n\t"
+      "addc.cc.u32 %0, %2, %3;\n\t"
+      "addc.u32 %1, 0, 0;\n\t}"
+      : "=r"(s[0]), "+r"(cy)
+      : "r"(x[0]), "r"(y[0]));
+}
+template <int N>
+__device__ __forceinline__ void addc_n(uint32_t (&s)[N], const uint32_t (&x)[N], const uint32_t (&y)[N], uint32_t& cy) {
+#pragma unroll
+  for (int k = 0; k + 4 <= N; k += 4) addc4(s + k, x + k, y + k, cy);
+  if (N & 2) addc2(s + (N & ~3), x + (N & ~3), y + (N & ~3), cy);
+  if (N & 1) addc1(s + (N - 1), x + (N - 1), y + (N - 1), cy);
+}
+
 struct SWin {
   uint32_t sa;  // shared address of window limb 0 of this thread
   uint32_t sb;  // byte stride between window limbs (4 * threads sharing the window array)
@@ -127,70 +166,47 @@ struct SWin {
   // NL interior limbs of P -> T (funnel by orr, + carry) -> S window.
   // Preconditions (checked by the caller): T indices and window indices in
   // the interior, so no masking, sticky or range logic is needed.
+  // One branch-free path for both operand orders (lanes of a warp differ in
+  // xa / sub): X -/+ Y as X + (Y ^ m) + carry with PTX carry chains
+  // (subtraction = add of the complement; the borrow is 1 - carry).
   template <int NL>
   __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry) {
-    uint32_t T[NL];
+    uint32_t T[NL], Z[NL];
     uint32_t pp = prevP;
 #pragma unroll
     for (int k = 0; k < NL; k++) {
-      uint32_t t = __funnelshift_r(pp, P[k], orr);
-      uint32_t s = t + tcarry;
-      tcarry = (s < t) ? 1u : 0u;
-      T[k] = s;
+      T[k] = __funnelshift_r(pp, P[k], orr);
+      Z[k] = 0u;
       pp = P[k];
     }
+    addc_n<NL>(T, T, Z, tcarry);
+    // X = a (slot w+k) or T;  Y stream = T (xa) or a limbs (slot w+k+dq+1)
+    const uint32_t ad0 = at(w + (xa ? 0 : dq + 1));
+    uint32_t Ld[NL];
+#pragma unroll
+    for (int k = 0; k < NL; k++) Ld[k] = lds32(ad0 + (uint32_t)k * sb);  // all loads first (ILP)
+    const uint32_t m = sub ? 0xffffffffu : 0u;
+    uint32_t yp = xa ? prev : curA;
+    uint32_t X[NL], Y[NL];
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+      uint32_t yh = xa ? T[k] : Ld[k];
+      Y[k] = __funnelshift_r(yp, yh, dr) ^ m;
+      yp = yh;
+      X[k] = xa ? Ld[k] : T[k];
+    }
+    uint32_t cy = sub ? (cb ^ 1u) : cb;
+    addc_n<NL>(X, X, Y, cy);
+    cb = sub ? (cy ^ 1u) : cy;
+    const uint32_t adw = at(w);
+#pragma unroll
+    for (int k = 0; k < NL; k++) sts32(adw + (uint32_t)k * sb, X[k]);
+    w += NL;
     if (xa) {
-      // window limb w <- funnel(T_{w-1+dq}, T_{w+dq}, dr); X = a limb in slot w
-      uint32_t X[NL];
-#pragma unroll
-      for (int k = 0; k < NL; k++) X[k] = lds32(at(w + k));  // all loads first (ILP)
-      uint32_t pt = prev;
-#pragma unroll
-      for (int k = 0; k < NL; k++) {
-        uint32_t yb = __funnelshift_r(pt, T[k], dr);
-        pt = T[k];
-        uint32_t s;
-        if (sub) {
-          uint64_t y = (uint64_t)yb + cb;
-          s = (uint32_t)((uint64_t)X[k] - y);
-          cb = ((uint64_t)X[k] < y) ? 1u : 0u;
-        } else {
-          uint64_t t2 = (uint64_t)X[k] + yb + cb;
-          s = (uint32_t)t2;
-          cb = (uint32_t)(t2 >> 32);
-        }
-        X[k] = s;
-      }
-#pragma unroll
-      for (int k = 0; k < NL; k++) sts32(at(w + k), X[k]);
-      w += NL;
-      prev = pt;
+      prev = yp;
       q += NL;
     } else {
-      // window limb w <- T_{w-1} -/+ funnel(a_{w-1+dq}, a_{w+dq}, dr)
-      uint32_t Av[NL];
-#pragma unroll
-      for (int k = 0; k < NL; k++) Av[k] = lds32(at(w + k + dq + 1));  // a limbs (w+k+dq): loads first
-#pragma unroll
-      for (int k = 0; k < NL; k++) {
-        uint32_t yb = __funnelshift_r(curA, Av[k], dr);
-        curA = Av[k];
-        uint32_t X = T[k];
-        uint32_t s;
-        if (sub) {
-          uint64_t y = (uint64_t)yb + cb;
-          s = (uint32_t)((uint64_t)X - y);
-          cb = ((uint64_t)X < y) ? 1u : 0u;
-        } else {
-          uint64_t t2 = (uint64_t)X + yb + cb;
-          s = (uint32_t)t2;
-          cb = (uint32_t)(t2 >> 32);
-        }
-        T[k] = s;
-      }
-#pragma unroll
-      for (int k = 0; k < NL; k++) sts32(at(w + k), T[k]);
-      w += NL;
+      curA = yp;
     }
   }
 };
@@ -408,8 +424,26 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
     O[0] = rr;
   }
   uint32_t* Op = O + so;
-#pragma unroll 4
-  for (int l = 1; l < L; l++) {
+  int l = 1;
+  for (; l + 4 <= L; l += 4) {
+    uint32_t h4[4], v4[4];
+    const uint32_t z4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 4; k++) h4[k] = lds32(ad + (uint32_t)k * sb);
+    ad += 4 * sb;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      v4[k] = __funnelshift_r(lo, h4[k], rs);
+      lo = h4[k];
+    }
+    addc4(v4, v4, z4, carry);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      *Op = v4[k];
+      Op += so;
+    }
+  }
+  for (; l < L; l++) {
     uint32_t hi = lds32(ad);
     ad += sb;
     uint32_t v = __funnelshift_r(lo, hi, rs);
