@@ -45,14 +45,16 @@ namespace {
 using namespace dss;
 
 constexpr int TM = 128;      // columns per CTA (TMEM lanes)
-constexpr int TN = 176;      // output digit columns per MMA tile
 constexpr int KS = 32;       // digits per MMA K step
-constexpr int NSLOT = 6;     // B-tile ring
-constexpr int NPROD = 128;   // producer threads
-constexpr int RBR = 8;       // rows per CTA
+constexpr int NEPI = 256;    // epilogue threads: two groups of 4 warps (alternate rows)
+constexpr int NPIPE = 64;    // producer threads per pipeline (2 warps; one per row parity)
+constexpr int NTHREADS = NEPI + 2 * NPIPE;
+constexpr int RBR = 16;      // rows per CTA
 
 struct TcArgs {
   int p, L, zb, D8p, nks, ntiles, c_lo, eps;
+  int tn;                  // output digit columns per MMA tile (N)
+  int br;                  // Toeplitz bank rows: ntiles * tn + 32 (nks - 1)
   int nrows, ncols, kstart, skip_col, n;
   int jl0;
   const uint8_t* zbytes;   // [nrows][D8p]
@@ -134,142 +136,153 @@ __global__ void k_tc_bytes(const uint32_t* src, int64_t count, int num, int L, i
 }
 
 // ---------------------------------------------------------------- main
-struct Smem {
-  uint8_t* As;    // nks * TM * KS: pivot-row digits of the CTA's 128 columns (K-major)
-  uint8_t* Bs;    // NSLOT * TN * KS: Toeplitz tiles of the current row's digits
-  uint8_t* rbq;   // 16 * RBL: shifted copies of the reversed row digits
-  uint32_t* Sw;   // (L + 2) * TM: per-column S windows
-  uint32_t* zw;   // ZWL bytes: the current row's digits with zero padding
-};
+__device__ __forceinline__ void bar_pipe(int id, int count) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count));
+}
 
-// Roles: TMEM lane = column k (128 consecutive columns of the pivot row), so
-// the epilogue warp's 32 lanes touch 32 consecutive a_jk of one row (coalesced
-// 128-byte accesses in the plane-major SoA); the CTA walks RB rows j.  z*b is
-// symmetric, so A = pivot-row digits (staged once) and B = Toeplitz(z_j).
-__global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB) {
+// Roles (384 threads; one CTA = 128 consecutive columns k x RBR rows j):
+//   warps 0-7   epilogue, two groups (warps 0-3: even rows, 4-7: odd rows);
+//               thread = column k = TMEM lane 32 (warp % 4) + lane, so a
+//               warp touches 32 consecutive a_jk of one row (coalesced).
+//   warps 8-9   pipeline 0 (even rows), warps 10-11 pipeline 1 (odd rows):
+//               per row, the Toeplitz bank of z_j's digits in the canonical
+//               K-major layout -- bank row r <-> m = m_min + r holds bytes
+//               k = 0..31 = Z[m - k] -- so the B tile of (tile t, K step ks)
+//               is bank rows [t*tn + 32 (nks-1-ks), +tn): a descriptor offset
+//               (8-row aligned), no per-MMA copies.  Lane 0 of warps 8 / 10
+//               issues the pipeline's MMAs.
+// TMEM: accumulators [0, 4 tn) = (group, double buffer) x tn columns; the
+// pivot-row digits (MMA A operand, lane = column k, 4 digits per 32-bit
+// column) at [4 tn, 4 tn + 8 nks).
+__global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_empty[NSLOT];
-  __shared__ __align__(8) uint64_t bar_tfull[2];
-  __shared__ __align__(8) uint64_t bar_tempty[2];
+  __shared__ __align__(8) uint64_t bar_bank_empty[2];
+  __shared__ __align__(8) uint64_t bar_tfull[2][2];
+  __shared__ __align__(8) uint64_t bar_tempty[2][2];
   __shared__ uint32_t tmem_base_sh;
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nks = a.nks, ntiles = a.ntiles, L = a.L;
-  const int T0 = a.c_lo + ntiles * TN - 1;  // largest digit index a tile can ask for
-  const int zbase = (T0 - RBL - 48) & ~3;   // zw[v] = Z[zbase + v]
-  const int ZWL = RBL + 96;
-  Smem s;
-  s.As = smem;
-  s.Bs = s.As + nks * TM * KS;
-  s.rbq = s.Bs + NSLOT * TN * KS;
-  s.Sw = (uint32_t*)(s.rbq + 16 * RBL);
-  s.zw = s.Sw + (L + 2) * TM;
+  const int nks = a.nks, ntiles = a.ntiles, L = a.L, TN = a.tn, BR = a.br;
+  const int m_min = a.c_lo - KS * (nks - 1);
+  const int zbase = (m_min - 32) & ~3;  // zw[v] = Z[zbase + v]
+  const int ZWL = ((BR + 64) + 15) & ~15;
+  uint8_t* bank0 = smem;                              // 2 banks of BR * 32 bytes
+  uint32_t* Swin = (uint32_t*)(smem + 2 * BR * KS);   // NEPI windows of L + 2 limbs
+  uint8_t* zw0 = (uint8_t*)(Swin + (L + 2) * NEPI);    // 2 x ZWL bytes
   const int kbase = a.kstart + blockIdx.x * TM;
-  const int row0 = blockIdx.y * RB;
-  const int nrow_cta = min(RB, a.nrows - row0);
+  const int row0 = blockIdx.y * RBR;
+  const int nrow_cta = min(RBR, a.nrows - row0);
+  const uint32_t ACOL = 4 * TN;
 
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; i++) mbar_init(&bar_empty[i], 1);
-    for (int i = 0; i < 2; i++) {
-      mbar_init(&bar_tfull[i], 1);
-      mbar_init(&bar_tempty[i], 4);
+    for (int g = 0; g < 2; g++) {
+      mbar_init(&bar_bank_empty[g], 1);
+      for (int b = 0; b < 2; b++) {
+        mbar_init(&bar_tfull[g][b], 1);
+        mbar_init(&bar_tempty[g][b], 4);
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  if (warp == 4) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // pivot-row digits -> As (canonical K-major: [ks][half][lanegroup][lane%8][16B])
-  for (int c = tid; c < TM * nks * 2; c += 256) {
-    int r = c / (nks * 2), q = c % (nks * 2);
-    int ks = q >> 1, h = q & 1;
-    uint8_t* dst = s.As + ks * TM * KS + h * TM * 16 + (r >> 3) * 128 + (r & 7) * 16;
-    if (kbase + r < a.n) cp16(dst, a.bbytes + (int64_t)(kbase + r) * a.D8p + ks * KS + h * 16);
-    else *(uint4*)dst = make_uint4(0, 0, 0, 0);
-  }
-  cp_wait_all();
-  asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_sh;
-
-  if (warp >= 4) {
-    // =================================================== producers + MMA issuer
-    const int ptid = tid - 128;
-    int it = 0;  // B-slot iteration counter
-    for (int ri = 0; ri < nrow_cta; ri++) {
-      const uint8_t* zrow = a.zbytes + (int64_t)(row0 + ri) * a.D8p;
-      named_sync(1, NPROD);  // the previous row's tiles no longer read rbq / zw
-      // zero-padded window of the row's digits (word granular: D8p, zbase = 0 mod 4)
-      for (int v = ptid; v < ZWL / 4; v += NPROD) {
-        int t = zbase + 4 * v;
-        s.zw[v] = (t >= 0 && t < a.D8p) ? *(const uint32_t*)(zrow + t) : 0u;
+  // pivot-row digits of the CTA's columns -> TMEM (group-0 threads, lane = column)
+  if (tid < TM) {
+    const int k = kbase + tid;
+    const uint4* src = (const uint4*)(a.bbytes + (int64_t)(k < a.n ? k : 0) * a.D8p);
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + ACOL;
+    for (int c = 0; c < a.D8p / 4; c += 8) {
+      uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
+      if (k < a.n) {
+        u0 = src[c / 4];
+        u1 = src[c / 4 + 1];
       }
-      named_sync(1, NPROD);
-      // rbq[q][y] = rb[y + q],  rb[x] = Z[T0 - x]: chunk (q, y0) = reversed
-      // Z[u .. u+16), u = T0 - y0 - q - 15  (funnel-shifted words + byte reversal)
-      for (int c = ptid; c < RBL; c += NPROD) {
-        int q = c / (RBL / 16), y0 = (c % (RBL / 16)) * 16;
-        int off = T0 - y0 - q - 15 - zbase;
-        const uint32_t* wp = s.zw + (off >> 2);
-        int sh = 8 * (off & 3);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + c), "r"(u0.x),
+                   "r"(u0.y), "r"(u0.z), "r"(u0.w), "r"(u1.x), "r"(u1.y), "r"(u1.z), "r"(u1.w));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  if (tid >= NEPI) {
+    // =================================================== pipelines: banks + MMAs
+    const int pp = (tid - NEPI) / NPIPE;  // row parity
+    const int ptid = (tid - NEPI) % NPIPE;
+    uint8_t* bank = bank0 + pp * BR * KS;
+    uint8_t* zw = zw0 + pp * ZWL;
+    const uint32_t bank_sa = smem_u32(bank);
+    const bool issuer = ptid == 0;
+    int q = 0;  // row counter of this pipeline
+    for (int ri = pp; ri < nrow_cta; ri += 2, q++) {
+      if (q >= 1) mbar_wait(&bar_bank_empty[pp], (q - 1) & 1);  // MMAs of row ri-2 completed
+      const uint8_t* zrow = a.zbytes + (int64_t)(row0 + ri) * a.D8p;
+      for (int v = ptid; v < ZWL / 4; v += NPIPE) {
+        int t = zbase + 4 * v;
+        ((uint32_t*)zw)[v] = (t >= 0 && t < a.D8p) ? *(const uint32_t*)(zrow + t) : 0u;
+      }
+      bar_pipe(1 + pp, NPIPE);
+      // chunk (r, h): bytes k = 16h .. 16h+15 of bank row r = reversed Z[u .. u+16),
+      // u = m_min + r - 16h - 15
+      for (int c = ptid; c < 2 * BR; c += NPIPE) {
+        const int h = c >= BR ? 1 : 0, r = c - h * BR;
+        const int off = m_min + r - 16 * h - 15 - zbase;
+        const uint32_t* wp = (const uint32_t*)zw + (off >> 2);
+        const int sh = 8 * (off & 3);
         uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
         uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
         uint32_t x2 = __funnelshift_r(w2, w3, sh), x3 = __funnelshift_r(w3, w4, sh);
-        *(uint4*)(s.rbq + q * RBL + y0) =
+        *(uint4*)(bank + h * BR * 16 + (r >> 3) * 128 + (r & 7) * 16) =
             make_uint4(__byte_perm(x3, 0, 0x0123), __byte_perm(x2, 0, 0x0123), __byte_perm(x1, 0, 0x0123),
                        __byte_perm(x0, 0, 0x0123));
       }
-      named_sync(1, NPROD);
-      for (int t = 0; t < ntiles; t++) {
-        const int gt = ri * ntiles + t;  // CTA-wide tile counter
-        const int buf = gt & 1;
-        const int c0 = a.c_lo + t * TN;
-        int s_lo = c0 - (a.D8p - 1);
-        if (s_lo < 0) s_lo = 0;
-        int s_hi = c0 + TN - 1;
-        if (s_hi > a.D8p - 1) s_hi = a.D8p - 1;
-        const int ks0 = s_lo / KS, ks1 = s_hi / KS;
-        for (int ks = ks0; ks <= ks1; ks++, it++) {
-          const int slot = it % NSLOT;
-          mbar_wait(&bar_empty[slot], ((it / NSLOT) & 1) ^ 1);
-          uint8_t* B = s.Bs + slot * TN * KS;
-          // chunk (n, h): bytes kk = 16h..16h+15 of row n -> rb[x0 .. x0+16),
-          // x0 = T0 - c0 - n + 32 ks + 16 h
-          for (int c = ptid; c < TN * 2; c += NPROD) {
-            int n = c >> 1, h = c & 1;
-            int x0 = T0 - c0 - n + KS * ks + 16 * h;
-            uint4 v = *(const uint4*)(s.rbq + (x0 & 15) * RBL + (x0 & ~15));
-            *(uint4*)(B + h * TN * 16 + (n >> 3) * 128 + (n & 7) * 16) = v;
-          }
-          asm volatile("fence.proxy.async.shared::cta;");
-          named_sync(1, NPROD);
-          if (ptid == 0) {
-            if (ks == ks0 && gt >= 2) mbar_wait(&bar_tempty[buf], ((gt >> 1) - 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            uint64_t ad = umma_desc(smem_u32(s.As + ks * TM * KS), TM * 16, 128);
-            uint64_t bd = umma_desc(smem_u32(B), TN * 16, 128);
+      asm volatile("fence.proxy.async.shared::cta;");
+      bar_pipe(1 + pp, NPIPE);
+      if (issuer) {
+        for (int t = 0; t < ntiles; t++) {
+          const int gt = q * ntiles + t;  // tile counter of this group
+          const int buf = gt & 1;
+          if (gt >= 2) mbar_wait(&bar_tempty[pp][buf], ((gt >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const int c0 = a.c_lo + t * TN;
+          int s_lo = c0 - (a.D8p - 1);
+          if (s_lo < 0) s_lo = 0;
+          int s_hi = c0 + TN - 1;
+          if (s_hi > a.D8p - 1) s_hi = a.D8p - 1;
+          const int ks0 = s_lo / KS, ks1 = s_hi / KS;
+          const uint32_t dcol = tmem + (uint32_t)((2 * pp + buf) * TN);
+          for (int ks = ks0; ks <= ks1; ks++) {
+            const int r0 = t * TN + KS * (nks - 1 - ks);  // multiple of 8
+            uint64_t bd = umma_desc(bank_sa + (uint32_t)(r0 >> 3) * 128u, (uint32_t)BR * 16u, 128);
             uint32_t acc = ks > ks0 ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + buf * TN),
-                "l"(ad), "l"(bd), "r"(idesc_i8(TM, TN)), "r"(acc));
-            umma_commit(&bar_empty[slot]);
-            if (ks == ks1) umma_commit(&bar_tfull[buf]);
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dcol),
+                "r"(tmem + ACOL + 8 * ks), "l"(bd), "r"(idesc_i8(TM, TN)), "r"(acc));
           }
+          umma_commit(&bar_tfull[pp][buf]);
         }
+        umma_commit(&bar_bank_empty[pp]);
       }
+      __syncwarp();
     }
   } else {
-    // =================================================== epilogue (lane = column)
-    const int r = tid;
+    // =================================================== epilogue
+    const int grp = warp >> 2, qw = warp & 3;
+    const int r = qw * 32 + lane;  // TMEM lane = column within the CTA
     const int k = kbase + r;
     const bool col_ok = k < a.n && k != a.skip_col;
-    uint32_t* Sw = s.Sw + r;  // window limb w at Sw[w * TM]
-    for (int ri = 0; ri < nrow_cta; ri++) {
+    uint32_t* Sw = Swin + tid;  // window limb w at Sw[w * NEPI]
+    int q = 0;
+    for (int ri = grp; ri < nrow_cta; ri += 2, q++) {
       const int zr = row0 + ri;  // row index relative to jl0
       const int jl = a.jl0 + zr;
       const int64_t idx = (int64_t)jl * a.n + k;
@@ -311,11 +324,11 @@ __global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB)
       if (process && !za) {
         const uint32_t* A = a.a_limbs + idx;
 #pragma unroll 4
-        for (int l = 0; l < L; l++) cp4(Sw + (l + 1) * TM, A + (int64_t)l * a.a_count);
+        for (int l = 0; l < L; l++) cp4(Sw + (l + 1) * NEPI, A + (int64_t)l * a.a_count);
       }
       cp_wait_all();
       SWin S;
-      S.base(Sw, TM);
+      S.base(Sw, NEPI);
       Emit em;
       if (process) {
         S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
@@ -335,11 +348,11 @@ __global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB)
       bool ok = true;
       uint32_t carry = 0;
       for (int t = 0; t < ntiles; t++) {
-        const int gt = ri * ntiles + t;
+        const int gt = q * ntiles + t;
         const int buf = gt & 1;
-        mbar_wait(&bar_tfull[buf], (gt >> 1) & 1);
+        mbar_wait(&bar_tfull[grp][buf], (gt >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + buf * TN;
+        const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((2 * grp + buf) * TN);
 #pragma unroll 1
         for (int cb = 0; cb < TN; cb += 16) {
           uint32_t v[16];
@@ -369,7 +382,7 @@ __global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB)
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_tempty[buf]);
+        if (lane == 0) mbar_arrive(&bar_tempty[grp][buf]);
       }
       if (process && ok) {
         em.finish(carry ? 1.0 : 0.0);
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(256, 1) k_update_tc(TcArgs a, int RBL, int RB)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // exact general-engine update of the listed elements (undecided short
@@ -422,8 +435,9 @@ __global__ void k_tc_fallback(TcArgs a, const uint32_t* z_limbs, int64_t z_count
   }
 }
 
-size_t tc_smem(int nks, int L, int D8p, int RBL) {
-  return (size_t)nks * TM * KS + (size_t)NSLOT * TN * KS + 16 * (size_t)RBL + 4 * (size_t)(L + 2) * TM + RBL + 96;
+size_t tc_smem(int L, int br) {
+  const size_t zwl = ((br + 64) + 15) & ~15;
+  return 2 * (size_t)br * KS + 4 * (size_t)(L + 2) * NEPI + 2 * zwl;
 }
 
 }  // namespace
@@ -458,12 +472,17 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   clo &= ~3;
   if (clo < 0) clo = 0;
   plan->c_lo = clo;
-  plan->ntiles = (2 * plan->D8p - clo + TN - 1) / TN;
-  plan->RBL = ((plan->ntiles * TN + KS * plan->nks + 32) + 15) & ~15;
+  // TMEM: 4 accumulator buffers of tn columns + 8 nks columns of A <= 512
+  int tn = ((512 - 8 * plan->nks) / 4) & ~15;
+  if (tn > 256) tn = 256;
+  if (tn < 32 || p < 256) return DS_OK;  // not applicable: other engines
+  plan->tn = tn;
+  plan->ntiles = (2 * plan->D8p - clo + tn - 1) / tn;
+  plan->br = plan->ntiles * tn + KS * (plan->nks - 1);
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  size_t smem = tc_smem(plan->nks, plan->L, plan->D8p, plan->RBL) + 1024;
-  if ((int)smem > maxsm - 2048 || p < 256) return DS_OK;  // not applicable: other engines
+  size_t smem = tc_smem(plan->L, plan->br) + 1024;
+  if ((int)smem > maxsm - 2048) return DS_OK;  // not applicable: other engines
   if (cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DS_CUDA;
   plan->smem = smem;
@@ -521,8 +540,10 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   a.a_limbs = a_limbs; a.a_exp = a_exp; a.a_cls = a_cls; a.a_count = a_count;
   a.status = status; a.step = i;
   a.fb_count = w->fb_count; a.fb_list = w->fb_list; a.fb_cap = w->fb_cap;
+  a.tn = plan->tn;
+  a.br = plan->br;
   dim3 grid((ncols + TM - 1) / TM, (nrows + RBR - 1) / RBR);
-  k_update_tc<<<grid, 256, plan->smem, s>>>(a, plan->RBL, RBR);
+  k_update_tc<<<grid, NTHREADS, plan->smem, s>>>(a);
   k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
   *launches += 4;
   cudaError_t e = cudaGetLastError();

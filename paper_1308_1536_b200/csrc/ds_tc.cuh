@@ -6,7 +6,8 @@
 struct TcPlan {
   int enabled;
   int p, L, D8p, nks;  // precision, 32-bit limbs, 8-bit digits (padded to the MMA K), K steps
-  int c_lo, ntiles, eps, RBL;
+  int c_lo, ntiles, eps;
+  int tn, br;          // MMA N per tile, Toeplitz bank rows
   size_t smem;
   void* work;
 };

@@ -120,6 +120,85 @@ __global__ void __launch_bounds__(128) k_conv(const uint8_t* Z, const uint8_t* b
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
+
+// Variant: A (Z digits) in TENSOR MEMORY (written by tcgen05.st, lane = row,
+// K bytes packed 4 per 32-bit column), B from shared memory.
+__global__ void __launch_bounds__(128) k_conv_ta(const uint8_t* Z, const uint8_t* b, int D8, int c0, int32_t* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int nks = D8 / KS;
+  uint8_t* Bs = sm;  // nks * (N * 32) bytes
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < N * D8; e += blockDim.x) {
+    int n = e / D8, s = e % D8;
+    int ks = s / KS, kk = s % KS;
+    int t = c0 + n - s;
+    Bs[ks * N * KS + kmaj_off(n, kk, N)] = (t >= 0 && t < D8) ? b[t] : 0;
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mbar)), "r"(1));
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  const uint32_t abase = tmem + 256;  // A in columns [256, 256 + D8/4)
+  // row r = tid writes its D8 bytes as D8/4 words, 8 columns per st
+  for (int c = 0; c < D8 / 4; c += 8) {
+    uint32_t w[8];
+    for (int q = 0; q < 8; q++) {
+      const uint8_t* zp = Z + tid * D8 + 4 * (c + q);
+      w[q] = zp[0] | (zp[1] << 8) | (zp[2] << 16) | ((uint32_t)zp[3] << 24);
+    }
+    uint32_t ta = abase + ((uint32_t)(warp * 32) << 16) + c;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]));
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;");
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t idesc = instr_desc_i8(M, N);
+  if (tid == 0) {
+    for (int ks = 0; ks < nks; ks++) {
+      uint32_t b_addr = (uint32_t)__cvta_generic_to_shared(Bs + ks * N * KS);
+      uint64_t bdesc = smem_desc(b_addr, N * 16, 128);
+      uint32_t acc = ks > 0 ? 1u : 0u;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+          "r"(abase + ks * 8), "l"(bdesc), "r"(idesc), "r"(acc));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&mbar)));
+  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"((uint32_t)__cvta_generic_to_shared(&mbar)), "r"(0));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  for (int cb = 0; cb < N; cb += 16) {
+    uint32_t v[16];
+    uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    int row = warp * 32 + lane;
+    for (int q = 0; q < 16; q++) out[row * N + cb + q] = (int32_t)v[q];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 int main(int argc, char** argv) {
   const int D8 = argc > 1 ? atoi(argv[1]) : 512;
   const int c0 = argc > 2 ? atoi(argv[2]) : D8 - 16;
@@ -156,6 +235,20 @@ int main(int argc, char** argv) {
       }
     }
   printf("D8=%d c0=%d mismatches=%ld\n", D8, c0, bad);
+  {
+    size_t smem2 = (size_t)(D8 / KS) * N * KS;
+    CK(cudaFuncSetAttribute(k_conv_ta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    CK(cudaMemset(dout, 0, sizeof(int32_t) * M * N));
+    k_conv_ta<<<1, 128, smem2>>>(dZ, db, D8, c0, dout);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    std::vector<int32_t> out2(M * N);
+    CK(cudaMemcpy(out2.data(), dout, sizeof(int32_t) * M * N, cudaMemcpyDeviceToHost));
+    long bad2 = 0;
+    for (int i = 0; i < M * N; i++) if (out2[i] != out[i]) { if (bad2 < 5) printf("TA mismatch %d: %d vs %d\n", i, out2[i], out[i]); bad2++; }
+    printf("A-in-TMEM variant: mismatches vs smem-A result=%ld\n", bad2);
+    bad += bad2;
+  }
   // timing: many reps of the MMA chain in one CTA per SM
   int reps = 200;
   cudaEvent_t e0, e1;
