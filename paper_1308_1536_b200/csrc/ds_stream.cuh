@@ -247,7 +247,10 @@ struct Emit {
   bool allz, allo, sticky, decided, excess;
   uint32_t rbit, tcarry, prevP, prevT;
   int tl, gtop, gn;
+  int glo, ghi;  // blocks starting at limb g0 in [glo, ghi] are interior (see block)
 
+  // call after S->init; NL = limbs per block the producer delivers
+  template <int NL>
   __device__ __forceinline__ void setup() {
     o = r - zb;
     oq = o >> 5;
@@ -256,6 +259,19 @@ struct Emit {
     prevT = 0;
     gn = 0;
     gtop = (r + p + 31) >> 5;
+    // interior: T indices q0 = g0 - oq - 1 with [q0, q0+NL) inside [1, L), and
+    // the S window slots inside [1, L]:  xa: q0 - dq >= 1, q0 - dq + NL <= L;
+    // otherwise a limbs read up to q0 + dq + NL stay below L
+    int qlo = 1, qhi = L - NL;
+    if (S->xa) {
+      qlo = 1 + S->dq;
+    } else if (S->yzero) {
+      qhi = 0;
+    } else {
+      qhi = L - NL - 1 - S->dq;
+    }
+    glo = qlo + oq + 1;
+    ghi = qhi + oq + 1;
   }
 
   __device__ __forceinline__ bool decide_limb(int g, uint32_t v) {
@@ -317,18 +333,8 @@ struct Emit {
   template <int NL>
   __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
     const int q0 = g0 - oq - 1;
-    // interior fast path: decided, T indices [q0, q0+NL) inside [1, L), and the
-    // S window indices produced are inside [1, L]
-    bool interior = decided && q0 >= 1 && q0 + NL <= L;
-    if (interior) {
-      if (S->xa) {
-        int w0 = q0 - S->dq;
-        interior = w0 >= 1 && w0 + NL <= S->L;
-      } else {
-        interior = !S->yzero && (q0 + 1 + S->dq + NL) <= S->L;  // a limbs read stay inside [0, L)
-      }
-    }
-    if (!interior) {
+    // interior fast path (bounds from setup<NL>)
+    if (!(decided && g0 >= glo && g0 <= ghi)) {
 #pragma unroll
       for (int k = 0; k < NL; k++)
         if (!limb(g0 + k, P[k])) return false;

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
         em.hi_chk = em.r - 2;
         em.allz = true; em.allo = true; em.sticky = false; em.decided = false;
         em.rbit = 0; em.tcarry = 0; em.tl = 0; em.excess = false;
-        em.setup();
+        em.setup<8>();
       }
       bool ok = true;
       uint32_t carry = 0;
@@ -354,21 +354,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((2 * grp + buf) * TN);
 #pragma unroll 1
-        for (int cb = 0; cb < TN; cb += 16) {
-          uint32_t v[16];
+        for (int cb = 0; cb < TN; cb += 32) {
+          uint32_t v[32];
           asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                "=r"(v[15])
+                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
               : "r"(taddr + cb));
           asm volatile("tcgen05.wait::ld.sync.aligned;");
           if (process && ok) {
             // limb g = sum_j v[4g+j] 2^(8j) + carry (< 2^51): 4 wide multiply-adds,
             // low word = the limb, high word = the carry into the next limb
-            uint32_t P[4];
+            uint32_t P[8];
 #pragma unroll
-            for (int g = 0; g < 4; g++) {
+            for (int g = 0; g < 8; g++) {
               uint64_t acc = (uint64_t)v[4 * g] + carry;
               acc += (uint64_t)v[4 * g + 1] * 256u;
               acc += (uint64_t)v[4 * g + 2] * 65536u;
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
               carry = (uint32_t)(acc >> 32);
             }
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
-            ok = em.block<4>(g0, P);
+            ok = em.block<8>(g0, P);
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -473,7 +476,7 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   if (clo < 0) clo = 0;
   plan->c_lo = clo;
   // TMEM: 4 accumulator buffers of tn columns + 8 nks columns of A <= 512
-  int tn = ((512 - 8 * plan->nks) / 4) & ~15;
+  int tn = ((512 - 8 * plan->nks) / 4) & ~31;  // multiple of the 32-column epilogue chunk
   if (tn > 256) tn = 256;
   if (tn < 32 || p < 256) return DS_OK;  // not applicable: other engines
   plan->tn = tn;

@@ -297,7 +297,7 @@ __device__ void fused_element(const UArgs& a, const double* zrow, const double* 
     em.hi_chk = em.r - 2;
     em.allz = true; em.allo = true; em.sticky = false; em.decided = false;
     em.rbit = 0; em.tcarry = 0; em.tl = 0; em.excess = false;
-    em.setup();
+    em.setup<3 * W / 4>();
     if (SPLIT && !exact) {
       // lanes accumulate disjoint column blocks; lane 0 normalises and rounds
       const int c_start = a.c_lo;

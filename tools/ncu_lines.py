@@ -1,0 +1,49 @@
+"""Per-region instruction / stall-sample totals of one ncu capture of k_update_tc
+(source page with -lineinfo).  usage: ncu_lines.py REPORT [top]"""
+import collections
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(src.splitlines()))
+out = []
+fname = None
+for r in rows:
+    if r and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if len(r) > 8 and r[0].isdigit() and r[2] == "-":
+        try:
+            out.append((int(r[7]), int(r[4]), fname, int(r[0]), r[1][:80]))
+        except ValueError:
+            pass
+REG = {"ds_tc.cu": [(0, "tc helpers"), (150, "tc setup"), (217, "pipelines"), (278, "epi setup+prefetch"),
+                    (350, "epi tiles"), (391, "epi tail")],
+       "ds_stream.cuh": [(0, "stream helpers"), (70, "swin access"), (118, "swin init/push/finish"),
+                         (173, "swin fast_block"), (241, "emit"), (358, "round_write")]}
+
+
+def region(f, line):
+    name = f
+    for start, nm in REG.get(f, []):
+        if line >= start:
+            name = nm
+    return name
+
+
+agg = collections.defaultdict(lambda: [0, 0])
+for n, s, f, line, _ in out:
+    k = region(f, line)
+    agg[k][0] += n
+    agg[k][1] += s
+T = sum(v[0] for v in agg.values()) or 1
+S = sum(v[1] for v in agg.values()) or 1
+for k, v in sorted(agg.items(), key=lambda x: -x[1][0]):
+    print(f"{k:24s} inst {v[0] / 1e6:7.2f}M ({100 * v[0] / T:4.1f}%)  samples {v[1]:6d} ({100 * v[1] / S:4.1f}%)")
+if top:
+    for o in sorted(out, key=lambda o: -o[1])[:top]:
+        print(o)
