@@ -109,12 +109,12 @@ class DeviceElimination:
         _check(self.lib.ds_set_det(self.ctx, ctypes.byref(s)), self.ctx, "ds_set_det", self.rank)
 
     # -- serial engine -----------------------------------------------------
-    def run(self, collect_minors: bool, series: bool, start: int, stop: int, res: HostResults):
-        """Steps [start, stop) on the device; returns (rc, steps_done)."""
-        r = res.c()
+    def run(self, collect_minors: bool, series: bool, start: int, stop: int, res: HostResults | None):
+        """Steps [start, stop) on the device; returns (rc, steps_done).  res=None leaves
+        the outputs in HBM (fetch them later with results())."""
         done = ctypes.c_int(0)
-        rc = self.lib.ds_run(self.ctx, int(collect_minors), int(series), start, stop, ctypes.byref(r),
-                             ctypes.byref(done))
+        rp = ctypes.byref(res.c()) if res is not None else None
+        rc = self.lib.ds_run(self.ctx, int(collect_minors), int(series), start, stop, rp, ctypes.byref(done))
         _check(rc, self.ctx, "ds_run", self.rank)
         return rc, done.value
 

@@ -17,14 +17,18 @@ for spec in sys.argv[1:]:
     A = random_uniform_soa(n, p, 1)
     L = (p + 31) // 32
     with DeviceElimination(n, p, "real") as eng:
-        res = HostResults.alloc(n, 1, L, True)
+        res = HostResults.alloc(n, 1, L, True, pinned=True)
         eng.load(A)
         eng.profile(True)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rc, done = eng.run(True, True, 0, n, res)
+        rc, done = eng.run(True, True, 0, n, None)
+        torch.cuda.synchronize()
         t1 = time.perf_counter()
+        eng.results(n, res)
+        t2 = time.perf_counter()
         ms, nl, w = eng.profile_read()
         work = n * (n - 1) ** 2 / 2 * L * L
-        print(f"n={n} p={p} done={done} wall={t1 - t0:.3f}s (incl. results D2H) "
+        print(f"n={n} p={p} done={done} device={t1 - t0:.3f}s results-D2H={t2 - t1:.3f}s "
               f"limb-MAC/s={work / (t1 - t0):.3e} update={ms / 1e3:.3f}s ({w / (ms * 1e-3):.3e}/s over {nl} launches) "
               f"launches={eng.launches()} {eng.counters()}", flush=True)
