@@ -698,7 +698,8 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   CK(cudaEventCreateWithFlags(&ctx->ev_piv, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
   int L = ctx->L, nc = ctx->ncomp;
-  ctx->a_count = (int64_t)ctx->nloc * n;
+  // plane stride padded to 32 elements (128 B): keeps every limb plane 16-byte aligned for the tile tensor map
+  ctx->a_count = (((int64_t)ctx->nloc * n) + 31) & ~(int64_t)31;
   int rc;
 #define AL(ptr, cnt) if ((rc = dmalloc(ctx, &ptr, (size_t)(cnt))) != DS_OK) { ds_destroy(ctx); return rc; }
   AL(ctx->a_limbs, (int64_t)nc * L * ctx->a_count);

@@ -359,35 +359,49 @@ struct Emit {
 
 
 // Normalise the S window, round to nearest-even at p bits and write the
-// left-aligned result limbs O[l*so] (coalesced across a warp), exponent and
-// class.  E is the exponent of the window's X operand.
-__device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,
-                                            int64_t so, int32_t* oexp, uint8_t* ocls, int32_t* status) {
+// left-aligned result limbs, exponent and class.  E is the exponent of the
+// window's X operand.  INPLACE: result limb l goes to window slot l + 1 (the
+// slots a's limbs were loaded into; a tile store writes them back), else to
+// O[l*so] in global memory (coalesced across a warp).
+// A negative window (X < Y: only possible when the exponents are equal) is
+// negated on the fly: -S = ~S + 1, where the +1 only reaches the limbs up to
+// the lowest nonzero one (z0); above it -S_w = ~S_w.
+template <bool INPLACE>
+__device__ __forceinline__ void round_out(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,
+                                          int64_t so, int32_t* oexp, uint8_t* ocls, int32_t* status) {
   const uint32_t sb = S.sb;
-  // ---- normalise, round to nearest-even, write the result (coalesced)
-  if (S.sub && S.cb) {  // negative (only possible when exponents are equal)
-    uint32_t c = 1;
-    uint32_t ad = S.at(0);
-    for (int wi = 0; wi <= L + 1; wi++, ad += sb) {
-      uint32_t v = ~lds32(ad) + c;
-      c = (c && v == 0u) ? 1u : 0u;
-      sts32(ad, v);
-    }
+  // ---- sign: a negative window is read as ~slot (mneg); the limbs up to the
+  // lowest nonzero one z0 are fixed up so that ~slot = -S there too:
+  // slot z0 <- S_z0 - 1 (= ~(-S_z0)), slots below <- ~0 (-S_w = 0)
+  uint32_t mneg = 0u;
+  if (S.sub && S.cb) {
     neg ^= 1;
-  }
-  int h = -1;
-  {
-    uint32_t ad = S.at(L + 1);
-    for (int wi = L + 1; wi >= 0; wi--, ad -= sb) {
-      uint32_t v = lds32(ad);
+    mneg = 0xffffffffu;
+    int z0 = 0;
+    while (z0 <= L + 1) {
+      uint32_t v = lds32(S.at(z0));
       if (v) {
-        h = 32 * wi + 31 - __clz(v);
+        sts32(S.at(z0), v - 1u);
         break;
       }
+      sts32(S.at(z0), 0xffffffffu);
+      z0++;
+    }
+  }
+  auto get = [&](int w) -> uint32_t { return (w >= 0 && w <= L + 1) ? (lds32(S.at(w)) ^ mneg) : 0u; };
+  int h = -1;
+  for (int wi = L + 1; wi >= 0; wi--) {
+    uint32_t v = get(wi);
+    if (v) {
+      h = 32 * wi + 31 - __clz(v);
+      break;
     }
   }
   if (h < 0) {  // exact cancellation -> +0
-    for (int l = 0; l < L; l++) O[(int64_t)l * so] = 0u;
+    for (int l = 0; l < L; l++) {
+      if (INPLACE) sts32(S.at(l + 1), 0u);
+      else O[(int64_t)l * so] = 0u;
+    }
     *oexp = 0;
     *ocls = DS_CLS_PZERO;
     return;
@@ -395,6 +409,10 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
   int64_t e = E - 32 * (int64_t)L - 31 + h;
   int off = h - 32 * L + 1;
   if (off < 0) {  // massive cancellation: move the window up by whole limbs
+    if (mneg) {  // materialise |S| first (rare)
+      for (int wi = 0; wi <= L + 1; wi++) sts32(S.at(wi), get(wi));
+      mneg = 0u;
+    }
     int qs = (-off + 31) / 32;
     for (int wi = L + 1; wi >= 0; wi--) S.set(wi, S.get(wi - qs));
     h += 32 * qs;
@@ -405,21 +423,23 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
   bool stk = S.sticky;
   if (lsbw - 1 >= 0) {
     int rb = lsbw - 1;
-    rbit = (S.get(rb >> 5) >> (rb & 31)) & 1u;
+    rbit = (get(rb >> 5) >> (rb & 31)) & 1u;
     for (int wi = 0; wi < (rb >> 5) && !stk; wi++)
-      if (S.get(wi)) stk = true;
-    if (!stk && (rb & 31) && (S.get(rb >> 5) & ((1u << (rb & 31)) - 1u))) stk = true;
+      if (get(wi)) stk = true;
+    if (!stk && (rb & 31) && (get(rb >> 5) & ((1u << (rb & 31)) - 1u))) stk = true;
   }
-  uint32_t lsb = (lsbw >= 0) ? ((S.get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
+  uint32_t lsb = (lsbw >= 0) ? ((get(lsbw >> 5) >> (lsbw & 31)) & 1u) : 0u;
   uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
   // 0 <= off <= 33 here, so base = off >> 5 is 0 or 1 and the window limbs
-  // base + l + 1 (l < L) stay inside [0, L + 1]
+  // base + l + 1 (l < L) stay inside [0, L + 1]; in place, slot l + 1 is
+  // written only after slots base + l, base + l + 1 were read
   const int base = off >> 5, rs = off & 31;
   uint32_t ad = S.at(base);
-  uint32_t lo = lds32(ad);
+  uint32_t lo = lds32(ad) ^ mneg;
   ad += sb;
+  uint32_t first;
   {
-    uint32_t hi = lds32(ad);
+    uint32_t hi = lds32(ad) ^ mneg;
     ad += sb;
     uint32_t v = __funnelshift_r(lo, hi, rs);
     lo = hi;
@@ -427,15 +447,18 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
     uint32_t add = carry << zb;
     uint32_t rr = v + add;
     carry = rr < v ? 1u : 0u;
-    O[0] = rr;
+    first = rr;
   }
+  if (INPLACE) sts32(S.at(1), first);
+  else O[0] = first;
   uint32_t* Op = O + so;
+  uint32_t wa = S.at(2);
   int l = 1;
   for (; l + 4 <= L; l += 4) {
     uint32_t h4[4], v4[4];
     const uint32_t z4[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int k = 0; k < 4; k++) h4[k] = lds32(ad + (uint32_t)k * sb);
+    for (int k = 0; k < 4; k++) h4[k] = lds32(ad + (uint32_t)k * sb) ^ mneg;
     ad += 4 * sb;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -445,27 +468,43 @@ __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, 
     addc4(v4, v4, z4, carry);
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      *Op = v4[k];
-      Op += so;
+      if (INPLACE) {
+        sts32(wa, v4[k]);
+        wa += sb;
+      } else {
+        *Op = v4[k];
+        Op += so;
+      }
     }
   }
   for (; l < L; l++) {
-    uint32_t hi = lds32(ad);
+    uint32_t hi = lds32(ad) ^ mneg;
     ad += sb;
     uint32_t v = __funnelshift_r(lo, hi, rs);
     lo = hi;
     uint32_t rr = v + carry;
     carry = rr < v ? 1u : 0u;
-    *Op = rr;
-    Op += so;
+    if (INPLACE) {
+      sts32(wa, rr);
+      wa += sb;
+    } else {
+      *Op = rr;
+      Op += so;
+    }
   }
   if (carry) {
-    O[(int64_t)(L - 1) * so] = 0x80000000u;
+    if (INPLACE) sts32(S.at(L), 0x80000000u);
+    else O[(int64_t)(L - 1) * so] = 0x80000000u;
     e += 1;
   }
   if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&status[2], 1);
   *oexp = (int32_t)e;
   *ocls = neg ? DS_CLS_NEG : DS_CLS_POS;
+}
+
+__device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,
+                                            int64_t so, int32_t* oexp, uint8_t* ocls, int32_t* status) {
+  round_out<false>(S, neg, E, L, p, zb, O, so, oexp, ocls, status);
 }
 
 }  // namespace dss

@@ -30,6 +30,7 @@
 // (canonical no-swizzle K-major layout) for all its rows.  TMEM holds two
 // 176-column accumulator buffers (the epilogue of one tile overlaps the MMAs
 // of the next).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -55,7 +56,9 @@ struct TcArgs {
   int p, L, zb, D8p, nks, ntiles, c_lo, eps;
   int tn;                  // output digit columns per MMA tile (N)
   int br;                  // Toeplitz bank rows: ntiles * tn + 32 (nks - 1)
+  int tma_ok;              // a planes reachable by the tile tensor map
   int nrows, ncols, kstart, skip_col, n;
+  int kmin;                // first column to update (kstart = kmin rounded down to 4: aligned tiles)
   int jl0;
   const uint8_t* zbytes;   // [nrows][D8p]
   const uint8_t* bbytes;   // [n][D8p]
@@ -115,6 +118,28 @@ __device__ __forceinline__ void cp_wait_all() {
   asm volatile("cp.async.commit_group;");
   asm volatile("cp.async.wait_group 0;");
 }
+// ---- TMA (bulk tensor) tile copies of the a planes: box = 128 columns x L planes
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(sdst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* ssrc) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"((uint64_t)map),
+               "r"(x), "r"(y), "r"(smem_u32(ssrc))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count));
 }
@@ -154,11 +179,12 @@ __device__ __forceinline__ void bar_pipe(int id, int count) {
 // TMEM: accumulators [0, 4 tn) = (group, double buffer) x tn columns; the
 // pivot-row digits (MMA A operand, lane = column k, 4 digits per 32-bit
 // column) at [4 tn, 4 tn + 8 nks).
-__global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_bank_empty[2];
   __shared__ __align__(8) uint64_t bar_tfull[2][2];
   __shared__ __align__(8) uint64_t bar_tempty[2][2];
+  __shared__ __align__(8) uint64_t bar_tile[2];  // a-tile loads (TMA), one per epilogue group
   __shared__ uint32_t tmem_base_sh;
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -167,7 +193,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
   const int zbase = (m_min - 32) & ~3;  // zw[v] = Z[zbase + v]
   const int ZWL = ((BR + 64) + 15) & ~15;
   uint8_t* bank0 = smem;                              // 2 banks of BR * 32 bytes
-  uint32_t* Swin = (uint32_t*)(smem + 2 * BR * KS);   // NEPI windows of L + 2 limbs
+  uint32_t* Swin = (uint32_t*)(smem + 2 * BR * KS);   // per group: [L + 2 slots][TM columns]
   uint8_t* zw0 = (uint8_t*)(Swin + (L + 2) * NEPI);    // 2 x ZWL bytes
   const int kbase = a.kstart + blockIdx.x * TM;
   const int row0 = blockIdx.y * RBR;
@@ -177,6 +203,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
   if (tid == 0) {
     for (int g = 0; g < 2; g++) {
       mbar_init(&bar_bank_empty[g], 1);
+      mbar_init(&bar_tile[g], 1);
       for (int b = 0; b < 2; b++) {
         mbar_init(&bar_tfull[g][b], 1);
         mbar_init(&bar_tempty[g][b], 4);
@@ -279,13 +306,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
     const int grp = warp >> 2, qw = warp & 3;
     const int r = qw * 32 + lane;  // TMEM lane = column within the CTA
     const int k = kbase + r;
-    const bool col_ok = k < a.n && k != a.skip_col;
-    uint32_t* Sw = Swin + tid;  // window limb w at Sw[w * NEPI]
+    const bool col_ok = k < a.n && k >= a.kmin && k != a.skip_col;
+    uint32_t* region = Swin + grp * (L + 2) * TM;  // the group's windows: slot w of column r at [w * TM + r]
+    uint32_t* Sw = region + r;
+    // full 128-column tiles move a's limbs with one TMA load / store per row
+    // (box = 128 columns x L planes into slots 1..L); edge tiles per thread
+    const bool tile_io = a.tma_ok && kbase + TM <= a.n && (a.n & 3) == 0;  // box start 16-byte aligned
     int q = 0;
     for (int ri = grp; ri < nrow_cta; ri += 2, q++) {
       const int zr = row0 + ri;  // row index relative to jl0
       const int jl = a.jl0 + zr;
       const int64_t idx = (int64_t)jl * a.n + k;
+      const int tx = (int)((int64_t)jl * a.n + kbase);
+      if (tile_io) {
+        if (r == 0) {
+          bulk_wait_read0();  // this group's previous tile store has read the window
+          mbar_expect_tx(&bar_tile[grp], (uint32_t)(TM * L * 4));
+          tma_load_2d(region + TM, &amap, tx, 0, &bar_tile[grp]);
+        }
+      }
       // ---- element setup (mirrors ds_update.cu fused_element)
       bool process = false, fallback = false;
       int neg = 0, norm = 0;
@@ -320,15 +359,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
           }
         }
       }
-      // prefetch a's limbs into the window (slots 1..L): coalesced across the warp
-      if (process && !za) {
-        const uint32_t* A = a.a_limbs + idx;
+      // a's limbs in the window (slots 1..L): coalesced across the warp
+      if (tile_io) {
+        mbar_wait(&bar_tile[grp], q & 1);
+      } else {
+        if (process && !za) {
+          const uint32_t* A = a.a_limbs + idx;
 #pragma unroll 4
-        for (int l = 0; l < L; l++) cp4(Sw + (l + 1) * NEPI, A + (int64_t)l * a.a_count);
+          for (int l = 0; l < L; l++) cp4(Sw + (l + 1) * TM, A + (int64_t)l * a.a_count);
+        }
+        cp_wait_all();
       }
-      cp_wait_all();
       SWin S;
-      S.base(Sw, NEPI);
+      S.base(Sw, TM);
       Emit em;
       if (process) {
         S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
@@ -393,13 +436,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a) {
       }
       if (process && !ok) fallback = true;
       if (process && ok) {
-        round_write(S, neg, E, L, a.p, a.zb, a.a_limbs + idx, a.a_count, a.a_exp + idx, a.a_cls + idx, a.status);
+        if (tile_io)
+          round_out<true>(S, neg, E, L, a.p, a.zb, nullptr, 0, a.a_exp + idx, a.a_cls + idx, a.status);
+        else
+          round_write(S, neg, E, L, a.p, a.zb, a.a_limbs + idx, a.a_count, a.a_exp + idx, a.a_cls + idx, a.status);
       } else if (fallback) {
+        if (tile_io && process) {  // the window was written: the tile store must put a back unchanged
+          const uint32_t* A = a.a_limbs + idx;
+          for (int l = 0; l < L; l++) Sw[(l + 1) * TM] = A[(int64_t)l * a.a_count];
+        }
         int slot = atomicAdd(a.fb_count, 1);
         if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
         else atomicAdd(&a.status[5], 1);
       }
+      if (tile_io) {  // all 128 results of the row in the window -> one tile store
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_pipe(3 + grp, TM);
+        if (r == 0) tma_store_2d(&amap, tx, 0, region + TM);
+      }
     }
+    if (tile_io && r == 0) bulk_wait0();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -446,6 +502,24 @@ size_t tc_smem(int L, int br) {
 }  // namespace
 
 // ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
 struct TcWork {
   uint8_t* zbytes;
   uint8_t* bbytes;
@@ -456,6 +530,10 @@ struct TcWork {
   uint32_t* scratch;
   int64_t sthreads;
   int fb_cap;
+  CUtensorMap amap;        // a planes: dims {a_count, L}, box {128, L}
+  const void* amap_base;
+  int64_t amap_count;
+  int amap_ok;
 };
 
 int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
@@ -523,7 +601,8 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   TcWork* w = (TcWork*)plan->work;
   const int L = plan->L;
   const int nrows = nloc - jl0;
-  const int kstart = collect_minors ? 0 : i + 1;
+  const int kmin = collect_minors ? 0 : i + 1;
+  const int kstart = kmin & ~3;  // column tiles start 16-byte aligned (tile tensor map)
   const int ncols = n - kstart;
   if (nrows <= 0 || ncols <= 0) return DS_OK;
   const uint32_t* b_limbs = (const uint32_t*)pbuf;
@@ -537,7 +616,7 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   TcArgs a;
   a.p = plan->p; a.L = L; a.zb = 32 * L - plan->p; a.D8p = plan->D8p; a.nks = plan->nks; a.ntiles = plan->ntiles;
   a.c_lo = plan->c_lo; a.eps = plan->eps;
-  a.nrows = nrows; a.ncols = ncols; a.kstart = kstart; a.skip_col = i; a.n = n; a.jl0 = jl0;
+  a.nrows = nrows; a.ncols = ncols; a.kstart = kstart; a.kmin = kmin; a.skip_col = i; a.n = n; a.jl0 = jl0;
   a.zbytes = w->zbytes; a.bbytes = w->bbytes; a.zf = w->zf; a.bf = w->bf;
   a.zexp = z_exp + jl0; a.zcls = z_cls + jl0; a.bexp = b_exp; a.bcls = b_cls;
   a.a_limbs = a_limbs; a.a_exp = a_exp; a.a_cls = a_cls; a.a_count = a_count;
@@ -545,8 +624,25 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   a.fb_count = w->fb_count; a.fb_list = w->fb_list; a.fb_cap = w->fb_cap;
   a.tn = plan->tn;
   a.br = plan->br;
+  if (w->amap_base != (const void*)a_limbs || w->amap_count != a_count) {
+    w->amap_base = a_limbs;
+    w->amap_count = a_count;
+    w->amap_ok = 0;
+    EncodeTiledFn enc = encode_tiled();
+    if (enc && !getenv("DS_TC_NO_TMA") && (a_count * 4) % 16 == 0 && L <= 256 && a_count < (1ll << 31)) {
+      cuuint64_t dims[2] = {(cuuint64_t)a_count, (cuuint64_t)L};
+      cuuint64_t strides[1] = {(cuuint64_t)a_count * 4};
+      cuuint32_t box[2] = {(cuuint32_t)TM, (cuuint32_t)L};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult cr = enc(&w->amap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)a_limbs, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      w->amap_ok = cr == CUDA_SUCCESS ? 1 : 0;
+    }
+  }
+  a.tma_ok = w->amap_ok;
   dim3 grid((ncols + TM - 1) / TM, (nrows + RBR - 1) / RBR);
-  k_update_tc<<<grid, NTHREADS, plan->smem, s>>>(a);
+  k_update_tc<<<grid, NTHREADS, plan->smem, s>>>(a, w->amap);
   k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
   *launches += 4;
   cudaError_t e = cudaGetLastError();

@@ -36,7 +36,8 @@ def _device_run(A, n, p, steps, minors, env=None):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("n,p,steps", [(150, 4096, 3), (261, 1024, 5), (140, 2000, 4), (130, 333, 6)])
+@pytest.mark.parametrize("n,p,steps", [(150, 4096, 3), (152, 4096, 3), (261, 1024, 5), (300, 2048, 4),
+                                          (140, 2000, 4), (130, 333, 6)])
 def test_tc_matches_oracle(n, p, steps):
     A = random_uniform_soa(n, p, seed=n + p)
     ref = oracle.OracleRank(n, p, "real")

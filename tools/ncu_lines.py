@@ -22,9 +22,9 @@ for r in rows:
         except ValueError:
             pass
 REG = {"ds_tc.cu": [(0, "tc helpers"), (150, "tc setup"), (217, "pipelines"), (278, "epi setup+prefetch"),
-                    (350, "epi tiles"), (391, "epi tail")],
+                    (350, "epi tiles"), (394, "epi tail")],
        "ds_stream.cuh": [(0, "stream helpers"), (70, "swin access"), (118, "swin init/push/finish"),
-                         (173, "swin fast_block"), (241, "emit"), (358, "round_write")]}
+                         (173, "swin fast_block"), (241, "emit"), (364, "round_write")]}
 
 
 def region(f, line):
