@@ -14,9 +14,9 @@ value    = schoolbook limb-MACs of the whole elimination (n(n-1)^2/2 * L^2)
 e2e      = same metric through the C ABI with HOST buffers: per step the
            pinned host matrix is copied in (ds_load), the pass runs, and the
            pivots/dets/signed/normalized minors are copied out.
-roofline = the fused update kernel (ds_update.cu) timed live with CUDA
-           events around every launch: achieved schoolbook limb-MAC/s vs the
-           INT32-IMAD limb-product roofline (measured IMAD rate / 2).
+roofline = the update kernel (ds_tc.cu, tcgen05 kind::i8) timed live with
+           CUDA events around every launch: algorithmic HBM bytes (read + write
+           of every updated element) per second vs the measured HBM peak.
 cpu_baseline / --impl reference = the reference hot loop (elim.py:37-53)
            restated over MPFR (oracle/), all host threads, bounded sample.
 Multi-GPU (torchrun): row-cyclic shards, per-step NCCL broadcast of the pivot
@@ -36,10 +36,26 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# measured on this pool's B200 (tools/microbench/imad_tput.cu, gpurun_out/imad_tput.txt):
-# IMAD 1.79e13 lane-ops/s, DFMA 1.78e13 lane-ops/s at 1965 MHz
-IMAD_OPS_PER_S = 1.79e13
-DFMA_OPS_PER_S = 1.78e13
+
+def measured_hbm_peak():
+    """HBM GB/s from MEASURED_PEAKS.json (driver-written), else the profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def committed_traffic(n, prec):
+    """DRAM bytes per update launch (dram__bytes_read.sum + write) from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "update_traffic.json")) as f:
+            d = json.load(f)
+        if d.get("n") == n and d.get("prec_bits") == prec:
+            return d["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
 
 
 def parse():
@@ -329,16 +345,28 @@ def main():
         d2h = res.pivots.nbytes + res.dets.nbytes + res.signed.nbytes + res.normalized.nbytes + res.row_flags.nbytes
         e2e = {"value": total_work / e2e_s, "unit": "limb-MAC/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "seconds_to_all_minors": e2e_s}
-    # ---- roofline of the fused update kernel
-    imad_peak = IMAD_OPS_PER_S / 2  # one 32x32->64 limb product = 2 IMAD (lo + hi)
-    achieved = upd_work / (upd_ms / 1e3 / args.steps * args.steps) if upd_ms > 0 else 0.0
-    roof = {"kernel": "k_update_dfma (ds_update.cu) + digit prep", "bound": "int32-imad (limb products)",
-            "achieved": achieved, "peak": imad_peak, "unit": "limb-MAC/s", "frac": achieved / imad_peak,
-            "traffic": None, "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
+    # ---- roofline of the dominant kernel: the update (tensor-core engine)
+    # algorithmic bytes per updated element: read + write a_jk (L limbs + exp + cls)
+    elems = upd_work / (L * L) if L else 0.0
+    upd_s = upd_ms / 1e3
+    bytes_alg = elems * 2 * (4 * L + 5)
+    hbm_peak, peak_src = measured_hbm_peak()
+    achieved_gbs = bytes_alg / upd_s / 1e9 if upd_s > 0 else 0.0
+    counters = eng.counters()
+    engine_name = ("k_update_tc (ds_tc.cu): tcgen05.mma kind::i8 digit products in TMEM + rounding epilogue"
+                   if counters.get("tc_engine") else "k_fused (ds_update.cu): FP64 digit products + rounding epilogue")
+    roof = {"kernel": engine_name, "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved_gbs / hbm_peak if hbm_peak else None, "traffic": committed_traffic(n, p),
+            "algorithmic_bytes_per_element": 2 * (4 * L + 5),
+            "elements_per_step": elems / args.steps if args.steps else None,
+            "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
             "launches_per_step": upd_launches / args.steps,
-            "note": "peak = measured IMAD rate / 2; the kernel runs the products on the FP64 pipe "
-                    "(exact 24-bit digit DFMAs) with a short product, so frac > 1 is possible; "
-                    "pipe utilisation from ncu in profiles/"}
+            "limb_mac_rate": upd_work / upd_s if upd_s > 0 else None,
+            "peak_source": peak_src,
+            "tc_fallback_elements": counters.get("tc_fallback_elements"),
+            "note": "achieved = algorithmic bytes (read+write of every updated a_jk) / summed update-kernel time "
+                    "(CUDA events on the launch stream); the kernel is bound by integer issue in the rounding "
+                    "epilogue, not by HBM or the tensor cores -- see profiles/ for issue/pipe utilisation"}
     out = None
     if rank == 0:
         cpu = None
@@ -350,7 +378,7 @@ def main():
         out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
                "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "f64 (exact 24-bit digit products) + u32 limbs", "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
+               "dtype": "u8 digit products (tcgen05 kind::i8, s32 accumulate) + u32 limbs", "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
                "config": workload(args, desc), "seconds_to_all_minors": ms / 1e3,
                "input_generation_s": gen_s,
                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": gpu_launches,

@@ -42,9 +42,21 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
   const int lane = threadIdx.x & 31;
   const uint64_t vtop = V[n - 1];
   const uint64_t vnext = V[n - 2];
+  const double vinv = 1.0 / (double)vtop;  // vtop >= 2^31: the estimate below is within 1 of num / vtop
   for (int j = nu - n - 1; j >= 0; j--) {
     uint64_t num = ((uint64_t)U[j + n] << 32) | U[j + n - 1];
-    uint64_t qhat = num / vtop;
+    // qhat = min(floor(num / vtop), 2^32 - 1): double estimate + exact correction
+    uint64_t qhat = (uint64_t)((double)num * vinv);
+    if (qhat > 0x1ffffffffull) qhat = 0x1ffffffffull;
+    int64_t rr = (int64_t)(num - qhat * vtop);
+    while (rr < 0) {
+      qhat -= 1;
+      rr += (int64_t)vtop;
+    }
+    while (rr >= (int64_t)vtop) {
+      qhat += 1;
+      rr -= (int64_t)vtop;
+    }
     if (qhat > 0xffffffffull) qhat = 0xffffffffull;
     uint64_t rhat = num - qhat * vtop;
     while (rhat < (1ull << 32) && qhat * vnext > ((rhat << 32) | (uint64_t)U[j + n - 2])) {

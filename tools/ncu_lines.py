@@ -21,10 +21,10 @@ for r in rows:
             out.append((int(r[7]), int(r[4]), fname, int(r[0]), r[1][:80]))
         except ValueError:
             pass
-REG = {"ds_tc.cu": [(0, "tc helpers"), (150, "tc setup"), (217, "pipelines"), (278, "epi setup+prefetch"),
-                    (350, "epi tiles"), (394, "epi tail")],
+REG = {"ds_tc.cu": [(0, "tc helpers"), (150, "tc setup"), (244, "pipelines"), (305, "epi setup+prefetch"),
+                    (393, "epi tiles"), (436, "epi tail")],
        "ds_stream.cuh": [(0, "stream helpers"), (70, "swin access"), (118, "swin init/push/finish"),
-                         (173, "swin fast_block"), (241, "emit"), (364, "round_write")]}
+                         (173, "swin fast_block"), (241, "emit"), (361, "round_out")]}
 
 
 def region(f, line):
