@@ -46,13 +46,14 @@ def measured_hbm_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def committed_traffic(n, prec):
-    """DRAM bytes per update launch (dram__bytes_read.sum + write) from the committed ncu summary, if any."""
+def committed_traffic(n, prec, elems_per_launch):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of an average update launch, scaled from the
+    committed ncu --set full capture of one launch of this workload (profiles/update_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "update_traffic.json")) as f:
             d = json.load(f)
         if d.get("n") == n and d.get("prec_bits") == prec:
-            return d["dram_bytes_per_launch"]
+            return d["dram_bytes_per_element"] * elems_per_launch
     except Exception:
         pass
     return None
@@ -356,7 +357,7 @@ def main():
     engine_name = ("k_update_tc (ds_tc.cu): tcgen05.mma kind::i8 digit products in TMEM + rounding epilogue"
                    if counters.get("tc_engine") else "k_fused (ds_update.cu): FP64 digit products + rounding epilogue")
     roof = {"kernel": engine_name, "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved_gbs / hbm_peak if hbm_peak else None, "traffic": committed_traffic(n, p),
+            "frac": achieved_gbs / hbm_peak if hbm_peak else None, "traffic": committed_traffic(n, p, elems / upd_launches if upd_launches else 0.0),
             "algorithmic_bytes_per_element": 2 * (4 * L + 5),
             "elements_per_step": elems / args.steps if args.steps else None,
             "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
@@ -375,7 +376,7 @@ def main():
                 cpu = cpu_reference(n, p, args.cpu_seconds, A)
             except Exception as exc:  # never fail the GPU line on the baseline
                 cpu = {"error": repr(exc)}
-        out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
+        out = {"metric": f"limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N={n} @{p}b",
                "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "u8 digit products (tcgen05 kind::i8, s32 accumulate) + u32 limbs", "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
