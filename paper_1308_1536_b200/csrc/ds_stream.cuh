@@ -6,6 +6,7 @@
 #pragma once
 #include <stdint.h>
 #include "../../include/detseries_b200.h"
+#include "ds_carry.cuh"
 
 namespace dss {
 
@@ -26,45 +27,6 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 }
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
-}
-
-// s = x + y + cy over N limbs (low -> high) with the PTX carry chain;
-// cy (0/1) in, carry out.  Chains of 4 and 2 limbs, the carry handed over in
-// a register between them.
-__device__ __forceinline__ void addc4(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
-  asm("{\n\t.reg .u32 t;\n\t"
-      "add.cc.u32 t, %4, 0xffffffff;\n\t"
-      "addc.cc.u32 %0, %5, %9;\n\t"
-      "addc.cc.u32 %1, %6, %10;\n\t"
-      "addc.cc.u32 %2, %7, %11;\n\t"
-      "addc.cc.u32 %3, %8, %12;\n\t"
-      "addc.u32 %4, 0, 0;\n\t}"
-      : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "+r"(cy)
-      : "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]));
-}
-__device__ __forceinline__ void addc2(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
-  asm("{\n\t.reg .u32 t;\n\t"
-      "add.cc.u32 t, %2, 0xffffffff;\n\t"
-      "addc.cc.u32 %0, %3, %5;\n\t"
-      "addc.cc.u32 %1, %4, %6;\n\t"
-      "addc.u32 %2, 0, 0;\n\t}"
-      : "=r"(s[0]), "=r"(s[1]), "+r"(cy)
-      : "r"(x[0]), "r"(x[1]), "r"(y[0]), "r"(y[1]));
-}
-__device__ __forceinline__ void addc1(uint32_t* s, const uint32_t* x, const uint32_t* y, uint32_t& cy) {
-  asm("{\n\t.reg .u32 t;\n\t"
-      "add.cc.u32 t, %1, 0xffffffff;\n\t"
-      "addc.cc.u32 %0, %2, %3;\n\t"
-      "addc.u32 %1, 0, 0;\n\t}"
-      : "=r"(s[0]), "+r"(cy)
-      : "r"(x[0]), "r"(y[0]));
-}
-template <int N>
-__device__ __forceinline__ void addc_n(uint32_t (&s)[N], const uint32_t (&x)[N], const uint32_t (&y)[N], uint32_t& cy) {
-#pragma unroll
-  for (int k = 0; k + 4 <= N; k += 4) addc4(s + k, x + k, y + k, cy);
-  if (N & 2) addc2(s + (N & ~3), x + (N & ~3), y + (N & ~3), cy);
-  if (N & 1) addc1(s + (N - 1), x + (N - 1), y + (N - 1), cy);
 }
 
 struct SWin {
@@ -262,12 +224,15 @@ struct Emit {
     // interior: T indices q0 = g0 - oq - 1 with [q0, q0+NL) inside [1, L), and
     // the S window slots inside [1, L]:  xa: q0 - dq >= 1, q0 - dq + NL <= L;
     // otherwise a limbs read up to q0 + dq + NL stay below L
+    // q0 = 0 is interior too when there is no low mask (zb = 0) and nothing of t
+    // falls below the window (non-xa, or xa with dq = 0: T_0 lands in the guard slot)
     int qlo = 1, qhi = L - NL;
     if (S->xa) {
-      qlo = 1 + S->dq;
+      qlo = (zb == 0 && S->dq == 0) ? 0 : 1 + S->dq;
     } else if (S->yzero) {
-      qhi = 0;
+      qhi = 0;  // no a limbs in the window (pure products, a = 0): generic path
     } else {
+      qlo = zb == 0 ? 0 : 1;
       qhi = L - NL - 1 - S->dq;
     }
     glo = qlo + oq + 1;

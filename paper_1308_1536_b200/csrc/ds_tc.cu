@@ -179,7 +179,9 @@ __device__ __forceinline__ void bar_pipe(int id, int count) {
 // TMEM: accumulators [0, 4 tn) = (group, double buffer) x tn columns; the
 // pivot-row digits (MMA A operand, lane = column k, 4 digits per 32-bit
 // column) at [4 tn, 4 tn + 8 nks).
-__global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
+// register cap 144 (launch bound 448 threads): 384 x 144 leaves ~10K registers per SM for a
+// side-stream block (minors emission, det chain) to co-run in the epilogue's idle issue slots
+__global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_bank_empty[2];
   __shared__ __align__(8) uint64_t bar_tfull[2][2];
@@ -396,8 +398,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a, const __gri
         mbar_wait(&bar_tfull[grp][buf], (gt >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t taddr = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((2 * grp + buf) * TN);
+        // digit columns >= 8L are zero (P < 2^(64L)): stop at the chunk holding column 8L - 1
+        const int cend = min(TN, 8 * L - (a.c_lo + t * TN));
 #pragma unroll 1
-        for (int cb = 0; cb < TN; cb += 32) {
+        for (int cb = 0; cb < cend; cb += 32) {
           uint32_t v[32];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -410,18 +414,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_update_tc(TcArgs a, const __gri
               : "r"(taddr + cb));
           asm volatile("tcgen05.wait::ld.sync.aligned;");
           if (process && ok) {
-            // limb g = sum_j v[4g+j] 2^(8j) + carry (< 2^51): 4 wide multiply-adds,
-            // low word = the limb, high word = the carry into the next limb
-            uint32_t P[8];
+            // limb g = w_g + (high word of w_(g-1)) + carry, w_g = sum_j v[4g+j] 2^(8j) < 2^50:
+            // three independent wide multiply-adds per limb, then one add.cc/addc chain
+            uint32_t lo[8], hi[8], P[8];
 #pragma unroll
             for (int g = 0; g < 8; g++) {
-              uint64_t acc = (uint64_t)v[4 * g] + carry;
-              acc += (uint64_t)v[4 * g + 1] * 256u;
-              acc += (uint64_t)v[4 * g + 2] * 65536u;
-              acc += (uint64_t)v[4 * g + 3] * 16777216u;
-              P[g] = (uint32_t)acc;
-              carry = (uint32_t)(acc >> 32);
+              uint64_t w = (uint64_t)v[4 * g + 1] * 256u + v[4 * g];
+              w += (uint64_t)v[4 * g + 2] * 65536u;
+              w += (uint64_t)v[4 * g + 3] * 16777216u;
+              lo[g] = (uint32_t)w;
+              hi[g] = (uint32_t)(w >> 32);
             }
+            asm("add.cc.u32 %0, %9, %8;\n\t"
+              "addc.cc.u32 %1, %10, %17;\n\t"
+              "addc.cc.u32 %2, %11, %18;\n\t"
+              "addc.cc.u32 %3, %12, %19;\n\t"
+              "addc.cc.u32 %4, %13, %20;\n\t"
+              "addc.cc.u32 %5, %14, %21;\n\t"
+              "addc.cc.u32 %6, %15, %22;\n\t"
+              "addc.cc.u32 %7, %16, %23;\n\t"
+              "addc.u32 %8, %24, 0;"
+                : "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]), "+r"(carry)
+                : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
             ok = em.block<8>(g0, P);
           }
@@ -552,6 +566,15 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   int clo = (rmin - 2 - 32 - plan->eps) / 8;
   clo &= ~3;
   if (clo < 0) clo = 0;
+  // align the 8-limb epilogue blocks so one starts at limb L + 1, the first T
+  // limb of normalised products (T_q = P' bits from r' - zb = 32 L + 32 q): then
+  // every T block of those lanes is an interior (branch-free) block
+  {
+    int g = clo / 4;
+    int d = ((g - (plan->L + 1)) % 8 + 8) % 8;
+    g -= d;
+    clo = g > 0 ? 4 * g : 0;
+  }
   plan->c_lo = clo;
   // TMEM: 4 accumulator buffers of tn columns + 8 nks columns of A <= 512
   int tn = ((512 - 8 * plan->nks) / 4) & ~31;  // multiple of the 32-column epilogue chunk

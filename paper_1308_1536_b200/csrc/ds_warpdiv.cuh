@@ -14,6 +14,7 @@
 #pragma once
 #include <stdint.h>
 #include "../../include/detseries_b200.h"
+#include "ds_carry.cuh"
 
 namespace dsw {
 
@@ -72,59 +73,49 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
       pb[u] = (uint32_t)t;
       h = t >> 32;
     }
-    // add the previous lane's carry word at the bottom of this block
+    // add the previous lane's carry word at the bottom of this block (carry chain)
     uint32_t hin = __shfl_up_sync(FULL, (uint32_t)h, 1);
     if (lane == 0) hin = 0;
-    uint64_t acc = (uint64_t)pb[0] + hin;
-    pb[0] = (uint32_t)acc;
-    uint32_t ov = (uint32_t)(acc >> 32);
-    bool allones = true;
+    uint32_t zk[K], mk[K];
 #pragma unroll
-    for (int u = 1; u < K; u++) {
-      uint64_t t2 = (uint64_t)pb[u] + ov;
-      pb[u] = (uint32_t)t2;
-      ov = (uint32_t)(t2 >> 32);
-    }
+    for (int u = 0; u < K; u++) zk[u] = 0u;
+    zk[0] = hin;
+    uint32_t ov = 0;
+    dss::addc_n<K>(pb, pb, zk, ov);
+    uint32_t andv = pb[0];
 #pragma unroll
-    for (int u = 0; u < K; u++) allones &= (pb[u] == 0xffffffffu);
+    for (int u = 1; u < K; u++) andv &= pb[u];
+    const bool allones = andv == 0xffffffffu;
     // carries of the block additions between lanes (product is < 2^(32(n+1)))
     uint32_t cio = 0;
     uint32_t c = cla(ov != 0, allones && ov == 0, cio, 32);
-    if (c) {
 #pragma unroll
-      for (int u = 0; u < K; u++) {
-        uint32_t o = pb[u];
-        pb[u] = o + 1u;
-        if (pb[u] != 0) break;
-      }
-    }
+    for (int u = 0; u < K; u++) zk[u] = 0u;
+    dss::addc_n<K>(pb, pb, zk, c);  // + carry-in from the lane below
     // product top limb: last lane's carry word + carry out of the lane chain
     uint32_t htop = __shfl_sync(FULL, (uint32_t)h, 31) + cio;
-    // subtract the block from U[j + lane*K ..]
+    // subtract the block from U[j + lane*K ..]: U + ~pb + 1 (carry chain; borrow = 1 - carry)
     uint32_t* Ub = U + j + lane * K;
     uint32_t ub[K];
-    uint32_t bo = 0;  // lane-local borrow
-    bool allzero = true;
 #pragma unroll
     for (int u = 0; u < K; u++) {
       ub[u] = Ub[u];
-      uint64_t y = (uint64_t)pb[u] + bo;
-      uint32_t d = (uint32_t)((uint64_t)ub[u] - y);
-      bo = ((uint64_t)ub[u] < y) ? 1u : 0u;
-      ub[u] = d;
+      mk[u] = ~pb[u];
     }
+    uint32_t cy = 1u;
+    dss::addc_n<K>(ub, ub, mk, cy);
+    const uint32_t bo = cy ^ 1u;  // lane-local borrow
+    uint32_t orv = ub[0];
 #pragma unroll
-    for (int u = 0; u < K; u++) allzero &= (ub[u] == 0u);
+    for (int u = 1; u < K; u++) orv |= ub[u];
+    const bool allzero = orv == 0u;
     uint32_t bio = 0;
     uint32_t b = cla(bo != 0, allzero && bo == 0, bio, 32);
-    if (b) {
+    // borrow-in from the lane below: ub - b = ub + (b ? ~0 : 0) over the K limbs
 #pragma unroll
-      for (int u = 0; u < K; u++) {
-        uint32_t o = ub[u];
-        ub[u] = o - 1u;
-        if (o != 0) break;
-      }
-    }
+    for (int u = 0; u < K; u++) mk[u] = b ? 0xffffffffu : 0u;
+    uint32_t c0 = 0u;
+    dss::addc_n<K>(ub, ub, mk, c0);
 #pragma unroll
     for (int u = 0; u < K; u++) Ub[u] = ub[u];
     __syncwarp();

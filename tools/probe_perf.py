@@ -12,7 +12,14 @@ import torch  # noqa: E402,F401
 from paper_1308_1536_b200.engine import DeviceElimination, HostResults  # noqa: E402
 from paper_1308_1536_b200.synth import random_uniform_soa  # noqa: E402
 
-for spec in sys.argv[1:]:
+series = True
+specs = []
+for arg in sys.argv[1:]:
+    if arg == "--no-series":
+        series = False  # minors emitted only at the last step (same update work)
+    else:
+        specs.append(arg)
+for spec in specs:
     n, p = map(int, spec.split("@"))
     A = random_uniform_soa(n, p, 1)
     L = (p + 31) // 32
@@ -22,13 +29,13 @@ for spec in sys.argv[1:]:
         eng.profile(True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rc, done = eng.run(True, True, 0, n, None)
+        rc, done = eng.run(True, series, 0, n, None)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         eng.results(n, res)
         t2 = time.perf_counter()
         ms, nl, w = eng.profile_read()
         work = n * (n - 1) ** 2 / 2 * L * L
-        print(f"n={n} p={p} done={done} device={t1 - t0:.3f}s results-D2H={t2 - t1:.3f}s "
+        print(f"n={n} p={p} series={series} done={done} device={t1 - t0:.3f}s results-D2H={t2 - t1:.3f}s "
               f"limb-MAC/s={work / (t1 - t0):.3e} update={ms / 1e3:.3f}s ({w / (ms * 1e-3):.3e}/s over {nl} launches) "
               f"launches={eng.launches()} {eng.counters()}", flush=True)
