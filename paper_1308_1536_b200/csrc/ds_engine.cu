@@ -691,10 +691,15 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   ctx->launches = 0;
   memset(&ctx->plan, 0, sizeof(ctx->plan));
   CK(cudaSetDevice(device));
-  CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  // the elimination's critical path (pivot -> multipliers -> update) runs at the
+  // highest stream priority, the outputs-only side stream (det chain, minors
+  // emission) at the lowest: pending update CTAs get SMs before emission blocks
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&ctx->own_stream, cudaStreamNonBlocking, prio_hi));
   ctx->stream = ctx->own_stream;
   CK(cudaEventCreateWithFlags(&ctx->ev, cudaEventDisableTiming));
-  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_lo));
   CK(cudaEventCreateWithFlags(&ctx->ev_piv, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
   int L = ctx->L, nc = ctx->ncomp;

@@ -92,6 +92,7 @@ struct SWin {
       emit(0u, 0u);
       return;
     }
+    set(L + 1, 0u);  // a limb L (above a's top) reads as zero in the branch-free blocks
     int64_t below = 32 * (int64_t)(dq - 1) + dr;  // a bits [0, below) are under the window
     for (int l = 0; l < L && (int64_t)l * 32 < below; l++) {
       uint32_t v = aload(l);
@@ -131,8 +132,11 @@ struct SWin {
   // One branch-free path for both operand orders (lanes of a warp differ in
   // xa / sub): X -/+ Y as X + (Y ^ m) + carry with PTX carry chains
   // (subtraction = add of the complement; the borrow is 1 - carry).
+  // fz >= 0: this block starts at T_0 (q0 = 0): low fz = zb bits masked, the
+  // round increment added at bit zb (as Emit::limb does for q = 0).
   template <int NL>
-  __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry) {
+  __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry,
+                                             int fz = -1) {
     uint32_t T[NL], Z[NL];
     uint32_t pp = prevP;
 #pragma unroll
@@ -141,7 +145,14 @@ struct SWin {
       Z[k] = 0u;
       pp = P[k];
     }
-    addc_n<NL>(T, T, Z, tcarry);
+    uint32_t tc = tcarry;
+    if (fz >= 0) {
+      T[0] &= ~((1u << fz) - 1u);
+      Z[0] = tcarry << fz;
+      tc = 0u;
+    }
+    addc_n<NL>(T, T, Z, tc);
+    tcarry = tc;
     // X = a (slot w+k) or T;  Y stream = T (xa) or a limbs (slot w+k+dq+1)
     const uint32_t ad0 = at(w + (xa ? 0 : dq + 1));
     uint32_t Ld[NL];
@@ -224,16 +235,16 @@ struct Emit {
     // interior: T indices q0 = g0 - oq - 1 with [q0, q0+NL) inside [1, L), and
     // the S window slots inside [1, L]:  xa: q0 - dq >= 1, q0 - dq + NL <= L;
     // otherwise a limbs read up to q0 + dq + NL stay below L
-    // q0 = 0 is interior too when there is no low mask (zb = 0) and nothing of t
-    // falls below the window (non-xa, or xa with dq = 0: T_0 lands in the guard slot)
-    int qlo = 1, qhi = L - NL;
+    // q0 = 0 (T_0, masked + round increment) is interior when nothing of t falls
+    // below the window: non-xa, or xa with dq = 0 (T_0 lands in the guard slot).
+    // Non-xa reads a limbs up to slot q0 + dq + NL + 1 <= L + 1 (slot L + 1 = 0).
+    int qlo = 0, qhi = L - NL;
     if (S->xa) {
-      qlo = (zb == 0 && S->dq == 0) ? 0 : 1 + S->dq;
+      qlo = S->dq == 0 ? 0 : 1 + S->dq;
     } else if (S->yzero) {
-      qhi = 0;  // no a limbs in the window (pure products, a = 0): generic path
+      qhi = -1;  // no a limbs in the window (pure products, a = 0): generic path
     } else {
-      qlo = zb == 0 ? 0 : 1;
-      qhi = L - NL - 1 - S->dq;
+      qhi = L - NL - S->dq;
     }
     glo = qlo + oq + 1;
     ghi = qhi + oq + 1;
@@ -306,7 +317,7 @@ struct Emit {
       return true;
     }
     gn = g0 + NL;
-    S->fast_block<NL>(prevP, P, orr, tcarry);
+    S->fast_block<NL>(prevP, P, orr, tcarry, q0 == 0 ? zb : -1);
     prevP = P[NL - 1];
     tl = q0 + NL;
     return true;

@@ -378,13 +378,16 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
       if (process) {
         S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
         em.S = &S;
-        em.r = (norm ? a.p : a.p - 1) + 2 * a.zb;  // t's LSB in P' = M_z * M_b
+        // every lane's P' is shifted to the normalised position (non-normalised
+        // products x 2, nsh = 1): t's LSB at r' = p + 2 zb for all lanes, so T limbs
+        // are whole P' limbs and all lanes of a warp share block boundaries
+        em.r = a.p + 2 * a.zb;
         em.zb = a.zb;
         em.p = a.p;
         em.L = L;
         em.exact = false;
         em.onesided = true;
-        em.lo_chk = 8 * a.c_lo + a.eps;
+        em.lo_chk = 8 * a.c_lo + a.eps + 1;  // the omitted part doubles with the shift
         em.hi_chk = em.r - 2;
         em.allz = true; em.allo = true; em.sticky = false; em.decided = false;
         em.rbit = 0; em.tcarry = 0; em.tl = 0; em.excess = false;
@@ -392,6 +395,8 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
       }
       bool ok = true;
       uint32_t carry = 0;
+      const int nsh = norm ? 0 : 1;
+      uint32_t praw = 0u;  // previous unshifted P limb
       for (int t = 0; t < ntiles; t++) {
         const int gt = q * ntiles + t;
         const int buf = gt & 1;
@@ -436,6 +441,12 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
               "addc.u32 %8, %24, 0;"
                 : "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]), "+r"(carry)
                 : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+              const uint32_t raw = P[g];
+              P[g] = __funnelshift_l(praw, raw, nsh);
+              praw = raw;
+            }
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
             ok = em.block<8>(g0, P);
           }
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
         if (lane == 0) mbar_arrive(&bar_tempty[grp][buf]);
       }
       if (process && ok) {
-        em.finish(carry ? 1.0 : 0.0);
+        em.finish((carry || (nsh && (praw >> 31))) ? 1.0 : 0.0);  // the bit shifted out of the top limb
         if (em.excess) ok = false;
       }
       if (process && !ok) fallback = true;
