@@ -137,6 +137,10 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int 
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map), "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
@@ -325,6 +329,8 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
           bulk_wait_read0();  // this group's previous tile store has read the window
           mbar_expect_tx(&bar_tile[grp], (uint32_t)(TM * L * 4));
           tma_load_2d(region + TM, &amap, tx, 0, &bar_tile[grp]);
+          if (ri + 2 < nrow_cta)  // the group's next tile into L2 while this row runs
+            tma_prefetch_2d(&amap, (int)((int64_t)(jl + 2) * a.n + kbase), 0);
         }
       }
       // ---- element setup (mirrors ds_update.cu fused_element)

@@ -21,10 +21,30 @@ for r in rows:
             out.append((int(r[7]), int(r[4]), fname, int(r[0]), r[1][:80]))
         except ValueError:
             pass
-REG = {"ds_tc.cu": [(0, "tc helpers"), (150, "tc setup"), (244, "pipelines"), (305, "epi setup+prefetch"),
-                    (393, "epi tiles"), (436, "epi tail")],
-       "ds_stream.cuh": [(0, "stream helpers"), (70, "swin access"), (118, "swin init/push/finish"),
-                         (173, "swin fast_block"), (241, "emit"), (361, "round_out")]}
+MARKERS = {"ds_tc.cu": [("tc helpers", None), ("tc setup", "k_update_tc(TcArgs"),
+                         ("pipelines", "pipelines: banks + MMAs"), ("epi setup+prefetch", "epilogue\n"),
+                         ("epi tiles", "for (int t = 0; t < ntiles; t++) {\n        const int gt"),
+                         ("epi tail", "if (process && ok) {\n        em.finish")],
+           "ds_stream.cuh": [("stream helpers", None), ("swin access", "struct SWin {"),
+                             ("swin init/push/finish", "void init("), ("swin fast_block", "void fast_block("),
+                             ("emit", "struct Emit {"), ("round_out", "void round_out(")]}
+
+
+def _regions():
+    import os
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1308_1536_b200", "csrc")
+    reg = {}
+    for f, marks in MARKERS.items():
+        src = open(os.path.join(root, f)).read()
+        lst = []
+        for name, m in marks:
+            line = 0 if m is None else src[:src.index(m)].count("\n") + 1
+            lst.append((line, name))
+        reg[f] = sorted(lst)
+    return reg
+
+
+REG = _regions()
 
 
 def region(f, line):
