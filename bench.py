@@ -238,10 +238,13 @@ def run_reference(args):
     wall = time.perf_counter() - t0
     rate = sum(v["value"] for v in vals) / len(vals)
     base = vals[-1]
-    out = {"metric": "limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N=2000 @4096b",
+    out = {"metric": f"limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, "
+                     f"N={args.n} @{args.prec}b",
            "value": rate, "unit": "limb-MAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "mpfr (u64 limbs)", "data": "synthetic", "impl": "reference",
+           "vs_baseline": None, "dtype": "mpfr (u64 limbs)",
+           "data": "Artless beta matrix from data/ zeta zeros" if desc.startswith("Artless") else "synthetic",
+           "impl": "reference",
            "config": workload(args, desc),
            "seconds_to_all_minors": work_limb_macs(args.n, L) / rate,
            "cpu_baseline": {"value": rate, "unit": "limb-MAC/s", "cores": base["cores"], "kind": "port",
