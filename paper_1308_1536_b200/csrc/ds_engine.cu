@@ -45,9 +45,19 @@ struct ds_ctx {
   uint8_t* own_pbuf;
   size_t pbuf_bytes;
   // multipliers z_j for local rows: [ncomp][L][nloc]
-  uint32_t* z_limbs;
+  uint32_t* z_limbs;   // multipliers of the current step (= zb_*[step & 1])
   int32_t* z_exp;
   uint8_t* z_cls;
+  uint32_t* zb_limbs[2];  // double buffer: the lookahead writes step i+1's multipliers
+  int32_t* zb_exp[2];     // while step i's update still reads step i's
+  uint8_t* zb_cls[2];
+  // lookahead (world 1, tensor-core update): the column tile holding column
+  // i+1 is updated first on `la`, then step i+1's multipliers are computed
+  // there while the rest of step i's update runs on the main stream
+  cudaStream_t la;
+  cudaEvent_t ev_prep, ev_a, ev_mult, ev_la_done;
+  int la_step;   // the step whose multipliers are already computed (-1: none)
+  int la_limit;  // lookahead only for steps i + 1 < la_limit (set by ds_run)
   // trace: pivots/dets [ncomp][L][n]; det running value [ncomp][L][1]
   uint32_t *piv_limbs, *det_limbs, *cur_limbs;
   int32_t *piv_exp, *det_exp, *cur_exp;
@@ -489,15 +499,20 @@ __device__ void wdiv_rn(Out o, const Val& a, const Val& b, int L, int p, uint32_
   }
 }
 
+// divisor_from_matrix (lookahead, world 1): the pivot a_ii is read from the
+// matrix (row i is not staged yet); a zero pivot leaves everything untouched
+// (the step's k_pivot_lite reports it)
 template <int K>
-__global__ void k_mult_w(KArgs k, int i, int jl0, int wwords) {
+__global__ void k_mult_w(KArgs k, int i, int jl0, int wwords, int divisor_from_matrix) {
   extern __shared__ uint32_t wsm[];
   if (k.status[0] >= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (r >= k.nloc - jl0) return;
   PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
-  Val b = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  Val b = divisor_from_matrix ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, (int64_t)i * k.n + i)
+                              : val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  if (divisor_from_matrix && is_zero_cls(b.c)) return;
   int64_t jl = jl0 + r;
   int64_t idx = jl * k.n + i;
   Val a = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
@@ -652,12 +667,20 @@ void ds_destroy(ds_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  void* ptrs[] = {ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->own_pbuf, ctx->z_limbs, ctx->z_exp, ctx->z_cls,
+  // ctx->z_* alias one of the two multiplier buffers: free those by their own pointers
+  void* ptrs[] = {ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->own_pbuf, ctx->zb_limbs[0], ctx->zb_exp[0], ctx->zb_cls[0],
                   ctx->piv_limbs, ctx->det_limbs, ctx->cur_limbs, ctx->piv_exp, ctx->det_exp, ctx->cur_exp,
                   ctx->piv_cls, ctx->det_cls, ctx->cur_cls, ctx->sig_limbs, ctx->nrm_limbs, ctx->sig_exp,
                   ctx->nrm_exp, ctx->sig_cls, ctx->nrm_cls, ctx->row_flags, ctx->status, ctx->scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  void* zb1[] = {ctx->zb_limbs[1], ctx->zb_exp[1], ctx->zb_cls[1]};
+  for (void* p : zb1)
+    if (p) cudaFree(p);
+  if (ctx->la) {
+    cudaStreamSynchronize(ctx->la);
+    cudaStreamDestroy(ctx->la);
+  }
   update_plan_free(&ctx->plan);
   tc_plan_free(&ctx->tc);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
@@ -694,12 +717,19 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   // the elimination's critical path (pivot -> multipliers -> update) runs at the
   // highest stream priority, the outputs-only side stream (det chain, minors
   // emission) at the lowest: pending update CTAs get SMs before emission blocks
+  // (numerically lower = higher priority): lookahead > main > side
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  CK(cudaStreamCreateWithPriority(&ctx->own_stream, cudaStreamNonBlocking, prio_hi));
+  const int prio_main = prio_hi < prio_lo ? prio_hi + 1 : prio_hi;
+  CK(cudaStreamCreateWithPriority(&ctx->own_stream, cudaStreamNonBlocking, prio_main));
   ctx->stream = ctx->own_stream;
   CK(cudaEventCreateWithFlags(&ctx->ev, cudaEventDisableTiming));
   CK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithPriority(&ctx->la, cudaStreamNonBlocking, prio_hi));
+  CK(cudaEventCreateWithFlags(&ctx->ev_prep, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_mult, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_la_done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_piv, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
   int L = ctx->L, nc = ctx->ncomp;
@@ -713,9 +743,17 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   ctx->pbuf_bytes = pbuf_size(n, L, nc);
   AL(ctx->own_pbuf, ctx->pbuf_bytes);
   ctx->pbuf = ctx->own_pbuf;
-  AL(ctx->z_limbs, (int64_t)nc * L * ctx->nloc);
-  AL(ctx->z_exp, (int64_t)nc * ctx->nloc);
-  AL(ctx->z_cls, (int64_t)nc * ctx->nloc);
+  AL(ctx->zb_limbs[0], (int64_t)nc * L * ctx->nloc);
+  AL(ctx->zb_exp[0], (int64_t)nc * ctx->nloc);
+  AL(ctx->zb_cls[0], (int64_t)nc * ctx->nloc);
+  AL(ctx->zb_limbs[1], (int64_t)nc * L * ctx->nloc);
+  AL(ctx->zb_exp[1], (int64_t)nc * ctx->nloc);
+  AL(ctx->zb_cls[1], (int64_t)nc * ctx->nloc);
+  ctx->z_limbs = ctx->zb_limbs[0];
+  ctx->z_exp = ctx->zb_exp[0];
+  ctx->z_cls = ctx->zb_cls[0];
+  ctx->la_step = -1;
+  ctx->la_limit = -1;
   AL(ctx->piv_limbs, (int64_t)nc * L * n); AL(ctx->piv_exp, (int64_t)nc * n); AL(ctx->piv_cls, (int64_t)nc * n);
   AL(ctx->det_limbs, (int64_t)nc * L * n); AL(ctx->det_exp, (int64_t)nc * n); AL(ctx->det_cls, (int64_t)nc * n);
   AL(ctx->cur_limbs, (int64_t)nc * L); AL(ctx->cur_exp, nc); AL(ctx->cur_cls, nc);
@@ -791,6 +829,7 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
   }
   // reset run state
   ctx->host_have_det = 0;
+  ctx->la_step = -1;
   ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
   int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
@@ -896,6 +935,12 @@ static void set_wdiv_attrs(int maxsm) {
 int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   if (i < 0 || i >= ctx->n) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
+  // multipliers of step i live in z buffer i & 1 (the lookahead fills the other)
+  ctx->z_limbs = ctx->zb_limbs[i & 1];
+  ctx->z_exp = ctx->zb_exp[i & 1];
+  ctx->z_cls = ctx->zb_cls[i & 1];
+  const bool la_have = ctx->la_step == i;
+  ctx->la_step = -1;
   KArgs k = kargs(ctx);
   cudaStream_t s = ctx->stream;
   const bool fast = fast_real(ctx);
@@ -950,10 +995,12 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   }
   if (nrows > 0) {
     // ---- multipliers z_j = RN(a_ji / piv), a_ji <- -z_j (elim.py:47, 53)
-    if (fast) {
+    if (fast && la_have) {
+      CK(cudaStreamWaitEvent(s, ctx->ev_mult, 0));  // computed by the previous step's lookahead
+    } else if (fast) {
       int blocks = (nrows + wpb - 1) / wpb;
       size_t smem = (size_t)wpb * wwords * 4;
-      WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords);
+      WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0);
     } else {
       k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
     }
@@ -966,14 +1013,36 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
       ctx->prof_work += (double)nrows * ncols_u * (double)L * L * (ctx->kind == DS_KIND_COMPLEX ? 4.0 : 1.0);
     }
     if (fast) {
+      // lookahead for step i + 1 (one rank, inside the current ds_run range, rows left)
+      const int la_col = (ctx->tc.enabled && ctx->world == 1 && i + 1 < ctx->la_limit && i + 2 < n &&
+                          !getenv("DS_NO_LOOKAHEAD"))
+                             ? i + 1
+                             : -1;
+      int la_used = 0;
       int rc = ctx->tc.enabled
                    ? tc_update_launch(&ctx->tc, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
                                       ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
-                                      ctx->status, &ctx->launches)
+                                      ctx->status, &ctx->launches, ctx->la, ctx->ev_prep, ctx->ev_a, la_col, &la_used)
                    : update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
                                    ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
                                    ctx->status, &ctx->launches);
       if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
+      if (la_used) {
+        // column i+1 is final: step i+1's multipliers on the lookahead stream (after
+        // the tile holding that column) while the other tiles of step i still run
+        KArgs kn = k;
+        kn.z_limbs = ctx->zb_limbs[(i + 1) & 1];
+        kn.z_exp = ctx->zb_exp[(i + 1) & 1];
+        kn.z_cls = ctx->zb_cls[(i + 1) & 1];
+        const int jl1 = i + 2;  // world 1: local row = global row
+        const int rows1 = ctx->nloc - jl1;
+        int blocks = (rows1 + wpb - 1) / wpb;
+        size_t smem = (size_t)wpb * wwords * 4;
+        WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, ctx->la, kn, i + 1, jl1, wwords, 1);
+        ctx->launches++;
+        CK(cudaEventRecord(ctx->ev_mult, ctx->la));
+        ctx->la_step = i + 1;
+      }
     } else {
       int kfirst = collect_minors ? 0 : i + 1;
       int64_t ncols = n - kfirst - (collect_minors ? 1 : 0);
@@ -1038,6 +1107,7 @@ int ds_snapshot(ds_ctx* ctx, int save) {
   CK(cudaMemcpyAsync(ctx->a_exp, ctx->snap_exp, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->a_cls, ctx->snap_cls, cb, cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->host_have_det = 0;
+  ctx->la_step = -1;
   ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, ctx->n, ctx->stream));
   CK(cudaMemsetAsync(ctx->status + 1, 0, 7 * sizeof(int32_t), ctx->stream));
@@ -1176,10 +1246,15 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
   if (ctx->world != 1) return DS_INVALID;
   if (start_step < 0 || stop_step > ctx->n || start_step > stop_step) return DS_INVALID;
   int rc;
+  ctx->la_limit = stop_step;
   for (int i = start_step; i < stop_step; i++) {
-    if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) return rc;
-    if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) return rc;
+    if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) { ctx->la_limit = -1; return rc; }
+    if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) { ctx->la_limit = -1; return rc; }
   }
+  ctx->la_limit = -1;
+  ctx->la_step = -1;
+  CK(cudaEventRecord(ctx->ev_la_done, ctx->la));  // nothing of the lookahead stream is left behind
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_la_done, 0));
   int failed;
   rc = ds_status(ctx, &failed);
   int upto = failed >= 0 ? failed : stop_step;

@@ -6,30 +6,19 @@
 // consecutive columns k of the pivot row and one row j this is one int8 GEMM
 //     D[k][c] = sum_s B[k][s] * T_j[s][c],   T_j[s][c] = Z_j[c - s]  (Toeplitz)
 // computed by tcgen05.mma.cta_group::1.kind::i8 (u8 x u8 -> s32) into TMEM:
-// M = 128 columns k (TMEM lanes), N = 176 output digit columns per tile, K =
-// 32 digits per instruction.  Only digit columns c >= c_lo are formed (short
-// product: the omitted part E is >= 0 and < D8*2^8 units of 2^(8 c_lo)); the
-// rounding of z*b is decided from the computed columns unless the bits under
-// the round bit are all ones (or a possible tie), in which case the element is
-// handed to the exact general engine through a fallback list (probability
-// ~2^-40 on non-exact data).
+// M = 128 columns k (TMEM lanes), N = tn output digit columns per tile (96 at
+// 4096 bits), K = 32 digits per instruction.  Only digit columns c >= c_lo are
+// formed (short product: the omitted part E is >= 0 and < D8*2^8 units of
+// 2^(8 c_lo)); the rounding of z*b is decided from the computed columns unless
+// the bits under the round bit are all ones (or a possible tie), in which case
+// the element is handed to the exact general engine through a fallback list
+// (probability ~2^-40 on non-exact data).
 //
-// CTA roles (256 threads; one CTA = 128 columns x RBR rows):
-//   warps 0-3  epilogue: thread = column k = TMEM lane, so a warp touches 32
-//              consecutive a_jk of one row (coalesced in the plane-major SoA);
-//              tcgen05.ld of 16 digit columns at a time, carry propagation
-//              into 8-bit digits, 4 digits = one 32-bit limb of P, then the
-//              shared rounding stream (ds_stream.cuh: round to t, exact
-//              a -/+ t window in shared memory with a's limbs prefetched by
-//              cp.async, RN, store).
-//   warps 4-7  producers: per row, 16 pre-shifted copies of the row's reversed
-//              digits; per MMA, a K-major Toeplitz tile in a shared-memory ring
-//              (one LDS.128 + STS.128 per 16-byte chunk); one elected thread
-//              issues the MMAs and commits to mbarriers.
-// The pivot-row digits of the CTA's 128 columns stay in shared memory
-// (canonical no-swizzle K-major layout) for all its rows.  TMEM holds two
-// 176-column accumulator buffers (the epilogue of one tile overlaps the MMAs
-// of the next).
+// A operand (pivot-row digits) in TMEM, B operand = per-row Toeplitz bank in
+// shared memory addressed by descriptor offsets, a's limbs moved by TMA tiles
+// (128 columns x L planes) into per-group windows, rounded in place and stored
+// back with one bulk tensor store.  Roles, pipelining and barriers: see the
+// comment above k_update_tc and DESIGN.md section 5.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -50,7 +39,8 @@ constexpr int KS = 32;       // digits per MMA K step
 constexpr int NEPI = 256;    // epilogue threads: two groups of 4 warps (alternate rows)
 constexpr int NPIPE = 64;    // producer threads per pipeline (2 warps; one per row parity)
 constexpr int NTHREADS = NEPI + 2 * NPIPE;
-constexpr int RBR = 16;      // rows per CTA
+constexpr int RBR = 16;      // rows per CTA (the lookahead tile uses RBR_LA)
+constexpr int RBR_LA = 4;
 
 struct TcArgs {
   int p, L, zb, D8p, nks, ntiles, c_lo, eps;
@@ -59,6 +49,8 @@ struct TcArgs {
   int tma_ok;              // a planes reachable by the tile tensor map
   int nrows, ncols, kstart, skip_col, n;
   int kmin;                // first column to update (kstart = kmin rounded down to 4: aligned tiles)
+  int tile0, tskip;        // column tile of blockIdx.x 0; tile index skipped (-1: none)
+  int rbr;                 // rows per CTA
   int jl0;
   const uint8_t* zbytes;   // [nrows][D8p]
   const uint8_t* bbytes;   // [n][D8p]
@@ -201,9 +193,10 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
   uint8_t* bank0 = smem;                              // 2 banks of BR * 32 bytes
   uint32_t* Swin = (uint32_t*)(smem + 2 * BR * KS);   // per group: [L + 2 slots][TM columns]
   uint8_t* zw0 = (uint8_t*)(Swin + (L + 2) * NEPI);    // 2 x ZWL bytes
-  const int kbase = a.kstart + blockIdx.x * TM;
-  const int row0 = blockIdx.y * RBR;
-  const int nrow_cta = min(RBR, a.nrows - row0);
+  const int tile = (int)blockIdx.x + a.tile0 + ((a.tskip >= 0 && (int)blockIdx.x >= a.tskip) ? 1 : 0);
+  const int kbase = a.kstart + tile * TM;
+  const int row0 = blockIdx.y * a.rbr;
+  const int nrow_cta = min(a.rbr, a.nrows - row0);
   const uint32_t ACOL = 4 * TN;
 
   if (tid == 0) {
@@ -551,6 +544,11 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+#define CK_TC(x)                                   \
+  do {                                             \
+    if ((x) != cudaSuccess) return DS_CUDA;        \
+  } while (0)
+
 struct TcWork {
   uint8_t* zbytes;
   uint8_t* bbytes;
@@ -637,7 +635,9 @@ void tc_plan_free(TcPlan* plan) {
 int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
                      int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
                      const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
-                     int64_t* launches) {
+                     int64_t* launches, cudaStream_t la, cudaEvent_t ev_prep, cudaEvent_t ev_a, int la_col,
+                     int* la_used) {
+  if (la_used) *la_used = 0;
   TcWork* w = (TcWork*)plan->work;
   const int L = plan->L;
   const int nrows = nloc - jl0;
@@ -681,8 +681,33 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     }
   }
   a.tma_ok = w->amap_ok;
-  dim3 grid((ncols + TM - 1) / TM, (nrows + RBR - 1) / RBR);
-  k_update_tc<<<grid, NTHREADS, plan->smem, s>>>(a, w->amap);
+  a.rbr = RBR;
+  const int ntile = (ncols + TM - 1) / TM;
+  const int nrg = (nrows + RBR - 1) / RBR;
+  const int ts = la_col >= 0 ? (la_col - kstart) / TM : -1;  // tile holding the lookahead column
+  if (ts >= 0 && ts < ntile && ntile >= 2 && la) {
+    // A: that tile on the lookahead stream (the caller chains the next multipliers
+    // after it); B: the other tiles on the main stream; fallback after both
+    CK_TC(cudaEventRecord(ev_prep, s));
+    CK_TC(cudaStreamWaitEvent(la, ev_prep, 0));
+    TcArgs aa = a;
+    aa.tile0 = ts;
+    aa.tskip = -1;
+    aa.rbr = RBR_LA;  // short CTAs: the next step's multipliers wait on this tile only
+    k_update_tc<<<dim3(1, (nrows + RBR_LA - 1) / RBR_LA), NTHREADS, plan->smem, la>>>(aa, w->amap);
+    CK_TC(cudaEventRecord(ev_a, la));
+    TcArgs ab = a;
+    ab.tile0 = 0;
+    ab.tskip = ts;
+    k_update_tc<<<dim3(ntile - 1, nrg), NTHREADS, plan->smem, s>>>(ab, w->amap);
+    CK_TC(cudaStreamWaitEvent(s, ev_a, 0));
+    *launches += 1;
+    *la_used = 1;
+  } else {
+    a.tile0 = 0;
+    a.tskip = -1;
+    k_update_tc<<<dim3(ntile, nrg), NTHREADS, plan->smem, s>>>(a, w->amap);
+  }
   k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
   *launches += 4;
   cudaError_t e = cudaGetLastError();

@@ -17,4 +17,5 @@ void tc_plan_free(TcPlan* plan);
 int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
                      int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
                      const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
-                     int64_t* launches);
+                     int64_t* launches, cudaStream_t la = nullptr, cudaEvent_t ev_prep = nullptr,
+                     cudaEvent_t ev_a = nullptr, int la_col = -1, int* la_used = nullptr);
