@@ -134,14 +134,15 @@ struct SWin {
   // (subtraction = add of the complement; the borrow is 1 - carry).
   // fz >= 0: this block starts at T_0 (q0 = 0): low fz = zb bits masked, the
   // round increment added at bit zb (as Emit::limb does for q = 0).
-  template <int NL>
+  // ALIGNED: t's limbs are whole P limbs (orr = 0, the tensor-core engine)
+  template <int NL, bool ALIGNED = false>
   __device__ __forceinline__ void fast_block(uint32_t prevP, const uint32_t (&P)[NL], int orr, uint32_t& tcarry,
                                              int fz = -1) {
     uint32_t T[NL], Z[NL];
     uint32_t pp = prevP;
 #pragma unroll
     for (int k = 0; k < NL; k++) {
-      T[k] = __funnelshift_r(pp, P[k], orr);
+      T[k] = ALIGNED ? pp : __funnelshift_r(pp, P[k], orr);  // orr = 0: funnel(lo, hi, 0) = lo
       Z[k] = 0u;
       pp = P[k];
     }
@@ -195,7 +196,7 @@ struct DryTop {
     if ((bitpos >> 5) == g) top = (v >> (bitpos & 31)) & 1u;
     return true;
   }
-  template <int NL>
+  template <int NL, bool ALIGNED = false>
   __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
 #pragma unroll
     for (int k = 0; k < NL; k++) limb(g0 + k, P[k]);
@@ -306,7 +307,7 @@ struct Emit {
     return true;
   }
 
-  template <int NL>
+  template <int NL, bool ALIGNED = false>
   __device__ __forceinline__ bool block(int g0, const uint32_t (&P)[NL]) {
     const int q0 = g0 - oq - 1;
     // interior fast path (bounds from setup<NL>)
@@ -317,7 +318,7 @@ struct Emit {
       return true;
     }
     gn = g0 + NL;
-    S->fast_block<NL>(prevP, P, orr, tcarry, q0 == 0 ? zb : -1);
+    S->fast_block<NL, ALIGNED>(prevP, P, orr, tcarry, q0 == 0 ? zb : -1);
     prevP = P[NL - 1];
     tl = q0 + NL;
     return true;

@@ -423,9 +423,10 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
             uint32_t lo[8], hi[8], P[8];
 #pragma unroll
             for (int g = 0; g < 8; g++) {
-              uint64_t w = (uint64_t)v[4 * g + 1] * 256u + v[4 * g];
+              uint64_t w = (uint64_t)v[4 * g + 3] * 16777216u;  // IMAD.WIDE chain, no zero-extension moves
               w += (uint64_t)v[4 * g + 2] * 65536u;
-              w += (uint64_t)v[4 * g + 3] * 16777216u;
+              w += (uint64_t)v[4 * g + 1] * 256u;
+              w += (uint64_t)v[4 * g] * 1u;
               lo[g] = (uint32_t)w;
               hi[g] = (uint32_t)(w >> 32);
             }
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
               praw = raw;
             }
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
-            ok = em.block<8>(g0, P);
+            ok = em.block<8, true>(g0, P);  // r' - zb = 32 L: aligned limbs
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");

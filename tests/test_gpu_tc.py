@@ -62,3 +62,48 @@ def test_tc_matches_dfma_engine(n, p, steps, minors):
     assert np.array_equal(fin_t.exp, fin_f.exp)
     assert np.array_equal(fin_t.limbs, fin_f.limbs)
     assert results_digest(res_f, fin_f, n, p, steps) == results_digest(res_t, fin_t, n, p, steps)
+
+
+@pytest.mark.parametrize("n,p,steps", [(140, 256, 5), (133, 257, 4), (136, 4064, 3), (131, 4095, 3)])
+def test_tc_precision_edges(n, p, steps):
+    """Smallest TC precision, non-multiple-of-32 precisions (low mask zb > 0), largest sizes."""
+    A = random_uniform_soa(n, p, seed=3 * n + p)
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res_o = HostResults.alloc(n, 1, ref.L, True)
+    ref.run(True, True, 0, steps, res_o)
+    fin_o = A.copy()
+    ref.fetch(fin_o)
+    res_d, fin_d = _device_run(A, n, p, steps, True)
+    assert not first_mismatch(fin_o, fin_d, p)
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+@pytest.mark.parametrize("minors,series", [(False, True), (True, False)])
+def test_tc_lookahead_modes_vs_dfma(minors, series):
+    """Whole eliminations (lookahead active) in the no-minors / no-series modes against the DFMA engine."""
+    n, p = 300, 1024
+    A = random_uniform_soa(n, p, seed=11)
+    outs = []
+    for env in (None, {"DS_DISABLE_TC": "1"}):
+        old = {}
+        for k, v in (env or {}).items():
+            old[k] = os.environ.get(k)
+            os.environ[k] = v
+        try:
+            with DeviceElimination(n, p, "real") as eng:
+                eng.load(A)
+                res = HostResults.alloc(n, 1, eng.L, minors)
+                eng.run(minors, series, 0, n, res)
+                fin = A.copy()
+                eng.fetch(fin)
+                outs.append((res, fin))
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+    (rt, ft), (rf, ff) = outs
+    assert np.array_equal(ft.limbs, ff.limbs) and np.array_equal(ft.exp, ff.exp) and np.array_equal(ft.cls, ff.cls)
+    assert results_digest(rt, ft, n, p, n) == results_digest(rf, ff, n, p, n)
