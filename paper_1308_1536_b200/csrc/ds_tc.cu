@@ -36,9 +36,15 @@ using namespace dss;
 
 constexpr int TM = 128;      // columns per CTA (TMEM lanes)
 constexpr int KS = 32;       // digits per MMA K step
-constexpr int NEPI = 256;    // epilogue threads: two groups of 4 warps (alternate rows)
-constexpr int NPIPE = 64;    // producer threads per pipeline (2 warps; one per row parity)
-constexpr int NTHREADS = NEPI + 2 * NPIPE;
+// NG epilogue groups of 4 warps (rows ri = grp mod NG) and NG producer
+// pipelines of 2 warps; NG = 2 up to 4096 bits, 1 where two groups' windows do
+// not fit in shared memory (8192 bits)
+constexpr int NPIPE = 64;    // producer threads per pipeline
+template <int NG>
+struct Cfg {
+  static constexpr int NEPI = 128 * NG;
+  static constexpr int NTHREADS = NEPI + NG * NPIPE;
+};
 constexpr int RBR = 16;      // rows per CTA (the lookahead tile uses RBR_LA)
 constexpr int RBR_LA = 4;
 
@@ -177,7 +183,10 @@ __device__ __forceinline__ void bar_pipe(int id, int count) {
 // column) at [4 tn, 4 tn + 8 nks).
 // register cap 144 (launch bound 448 threads): 384 x 144 leaves ~10K registers per SM for a
 // side-stream block (minors emission, det chain) to co-run in the epilogue's idle issue slots
-__global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
+// NG = 2 is bounded as if 448 threads: the 128-register cap measured faster than ~158
+template <int NG>
+__global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
+  constexpr int NEPI = Cfg<NG>::NEPI;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_bank_empty[2];
   __shared__ __align__(8) uint64_t bar_tfull[2][2];
@@ -190,17 +199,17 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
   const int m_min = a.c_lo - KS * (nks - 1);
   const int zbase = (m_min - 32) & ~3;  // zw[v] = Z[zbase + v]
   const int ZWL = ((BR + 64) + 15) & ~15;
-  uint8_t* bank0 = smem;                              // 2 banks of BR * 32 bytes
-  uint32_t* Swin = (uint32_t*)(smem + 2 * BR * KS);   // per group: [L + 2 slots][TM columns]
-  uint8_t* zw0 = (uint8_t*)(Swin + (L + 2) * NEPI);    // 2 x ZWL bytes
+  uint8_t* bank0 = smem;                               // NG banks of BR * 32 bytes
+  uint32_t* Swin = (uint32_t*)(smem + NG * BR * KS);   // per group: [L + 2 slots][TM columns]
+  uint8_t* zw0 = (uint8_t*)(Swin + (L + 2) * NEPI);     // NG x ZWL bytes
   const int tile = (int)blockIdx.x + a.tile0 + ((a.tskip >= 0 && (int)blockIdx.x >= a.tskip) ? 1 : 0);
   const int kbase = a.kstart + tile * TM;
   const int row0 = blockIdx.y * a.rbr;
   const int nrow_cta = min(a.rbr, a.nrows - row0);
-  const uint32_t ACOL = 4 * TN;
+  const uint32_t ACOL = 2 * NG * TN;
 
   if (tid == 0) {
-    for (int g = 0; g < 2; g++) {
+    for (int g = 0; g < NG; g++) {
       mbar_init(&bar_bank_empty[g], 1);
       mbar_init(&bar_tile[g], 1);
       for (int b = 0; b < 2; b++) {
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
     const uint32_t bank_sa = smem_u32(bank);
     const bool issuer = ptid == 0;
     int q = 0;  // row counter of this pipeline
-    for (int ri = pp; ri < nrow_cta; ri += 2, q++) {
+    for (int ri = pp; ri < nrow_cta; ri += NG, q++) {
       if (q >= 1) mbar_wait(&bar_bank_empty[pp], (q - 1) & 1);  // MMAs of row ri-2 completed
       const uint8_t* zrow = a.zbytes + (int64_t)(row0 + ri) * a.D8p;
       for (int v = ptid; v < ZWL / 4; v += NPIPE) {
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
     // (box = 128 columns x L planes into slots 1..L); edge tiles per thread
     const bool tile_io = a.tma_ok && kbase + TM <= a.n && (a.n & 3) == 0;  // box start 16-byte aligned
     int q = 0;
-    for (int ri = grp; ri < nrow_cta; ri += 2, q++) {
+    for (int ri = grp; ri < nrow_cta; ri += NG, q++) {
       const int zr = row0 + ri;  // row index relative to jl0
       const int jl = a.jl0 + zr;
       const int64_t idx = (int64_t)jl * a.n + k;
@@ -322,8 +331,8 @@ __global__ void __launch_bounds__(448, 1) k_update_tc(TcArgs a, const __grid_con
           bulk_wait_read0();  // this group's previous tile store has read the window
           mbar_expect_tx(&bar_tile[grp], (uint32_t)(TM * L * 4));
           tma_load_2d(region + TM, &amap, tx, 0, &bar_tile[grp]);
-          if (ri + 2 < nrow_cta)  // the group's next tile into L2 while this row runs
-            tma_prefetch_2d(&amap, (int)((int64_t)(jl + 2) * a.n + kbase), 0);
+          if (ri + NG < nrow_cta)  // the group's next tile into L2 while this row runs
+            tma_prefetch_2d(&amap, (int)((int64_t)(jl + NG) * a.n + kbase), 0);
         }
       }
       // ---- element setup (mirrors ds_update.cu fused_element)
@@ -519,9 +528,9 @@ __global__ void k_tc_fallback(TcArgs a, const uint32_t* z_limbs, int64_t z_count
   }
 }
 
-size_t tc_smem(int L, int br) {
+size_t tc_smem(int L, int br, int ng) {
   const size_t zwl = ((br + 64) + 15) & ~15;
-  return 2 * (size_t)br * KS + 4 * (size_t)(L + 2) * NEPI + 2 * zwl;
+  return ng * ((size_t)br * KS + 4 * (size_t)(L + 2) * TM + zwl);
 }
 
 }  // namespace
@@ -543,6 +552,13 @@ static EncodeTiledFn encode_tiled() {
       fn = (EncodeTiledFn)p;
   }
   return fn;
+}
+
+static void launch_update(int ng, dim3 grid, size_t smem, cudaStream_t s, const TcArgs& a, const CUtensorMap& m) {
+  if (ng == 2)
+    k_update_tc<2><<<grid, Cfg<2>::NTHREADS, smem, s>>>(a, m);
+  else
+    k_update_tc<1><<<grid, Cfg<1>::NTHREADS, smem, s>>>(a, m);
 }
 
 #define CK_TC(x)                                   \
@@ -592,19 +608,33 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
     clo = g > 0 ? 4 * g : 0;
   }
   plan->c_lo = clo;
-  // TMEM: 4 accumulator buffers of tn columns + 8 nks columns of A <= 512
-  int tn = ((512 - 8 * plan->nks) / 4) & ~31;  // multiple of the 32-column epilogue chunk
-  if (tn > 256) tn = 256;
-  if (tn < 32 || p < 256) return DS_OK;  // not applicable: other engines
-  plan->tn = tn;
-  plan->ntiles = (2 * plan->D8p - clo + tn - 1) / tn;
-  plan->br = plan->ntiles * tn + KS * (plan->nks - 1);
+  // TMEM: 2 NG accumulator buffers of tn columns + 8 nks columns of A <= 512;
+  // two epilogue groups if their windows fit in shared memory, else one
+  if (p < 256) return DS_OK;  // not applicable: other engines
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  size_t smem = tc_smem(plan->L, plan->br) + 1024;
-  if ((int)smem > maxsm - 2048) return DS_OK;  // not applicable: other engines
-  if (cudaFuncSetAttribute(k_update_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return DS_CUDA;
+  size_t smem = 0;
+  int ng = 0;
+  for (int g = 2; g >= 1 && !ng; g--) {
+    if (g == 2 && getenv("DS_TC_ONE_GROUP")) continue;
+    int tn = ((512 - 8 * plan->nks) / (2 * g)) & ~31;  // multiple of the 32-column epilogue chunk
+    if (tn > 256) tn = 256;
+    if (tn < 32) continue;
+    int ntiles = (2 * plan->D8p - clo + tn - 1) / tn;
+    int br = ntiles * tn + KS * (plan->nks - 1);
+    size_t sm = tc_smem(plan->L, br, g) + 1024;
+    if ((int)sm > maxsm - 2048) continue;
+    ng = g;
+    plan->tn = tn;
+    plan->ntiles = ntiles;
+    plan->br = br;
+    smem = sm;
+  }
+  if (!ng) return DS_OK;  // not applicable: other engines
+  plan->ng = ng;
+  cudaError_t ea = ng == 2 ? cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                           : cudaFuncSetAttribute(k_update_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ea != cudaSuccess) return DS_CUDA;
   plan->smem = smem;
   TcWork* w = new TcWork();
   memset(w, 0, sizeof(*w));
@@ -695,19 +725,19 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     aa.tile0 = ts;
     aa.tskip = -1;
     aa.rbr = RBR_LA;  // short CTAs: the next step's multipliers wait on this tile only
-    k_update_tc<<<dim3(1, (nrows + RBR_LA - 1) / RBR_LA), NTHREADS, plan->smem, la>>>(aa, w->amap);
+    launch_update(plan->ng, dim3(1, (nrows + RBR_LA - 1) / RBR_LA), plan->smem, la, aa, w->amap);
     CK_TC(cudaEventRecord(ev_a, la));
     TcArgs ab = a;
     ab.tile0 = 0;
     ab.tskip = ts;
-    k_update_tc<<<dim3(ntile - 1, nrg), NTHREADS, plan->smem, s>>>(ab, w->amap);
+    launch_update(plan->ng, dim3(ntile - 1, nrg), plan->smem, s, ab, w->amap);
     CK_TC(cudaStreamWaitEvent(s, ev_a, 0));
     *launches += 1;
     *la_used = 1;
   } else {
     a.tile0 = 0;
     a.tskip = -1;
-    k_update_tc<<<dim3(ntile, nrg), NTHREADS, plan->smem, s>>>(a, w->amap);
+    launch_update(plan->ng, dim3(ntile, nrg), plan->smem, s, a, w->amap);
   }
   k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
   *launches += 4;

@@ -8,6 +8,7 @@ struct TcPlan {
   int p, L, D8p, nks;  // precision, 32-bit limbs, 8-bit digits (padded to the MMA K), K steps
   int c_lo, ntiles, eps;
   int tn, br;          // MMA N per tile, Toeplitz bank rows
+  int ng;              // epilogue groups / producer pipelines per CTA (1 or 2)
   size_t smem;
   void* work;
 };

@@ -461,8 +461,13 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int TR = pick_tr(W, plan->D, plan->L, maxsm);
-  if (TR == 0) return DS_OK;  // too wide for one CTA: general engine
   int tc = TC;
+  if (TR == 0) {  // wide precisions (~16K bits): 16-column CTAs with fewer rows
+    tc = 16;
+    TR = 8;
+    while (TR > 1 && fused_smem(W, TR, plan->D, plan->L, 16) > maxsm) TR /= 2;
+    if (fused_smem(W, TR, plan->D, plan->L, 16) > maxsm) return DS_OK;  // too wide for one CTA: general engine
+  }
   int smsm = 0;  // shared memory per SM
   cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   // two independent 16-column CTAs per SM desynchronise the warps' epilogues

@@ -1,6 +1,9 @@
 import os
 import sys
 
+if hasattr(sys, "set_int_max_str_digits"):
+    sys.set_int_max_str_digits(0)  # canonical digests of >4300-digit mantissas (p >= 16384)
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

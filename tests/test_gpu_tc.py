@@ -107,3 +107,33 @@ def test_tc_lookahead_modes_vs_dfma(minors, series):
     (rt, ft), (rf, ff) = outs
     assert np.array_equal(ft.limbs, ff.limbs) and np.array_equal(ft.exp, ff.exp) and np.array_equal(ft.cls, ff.cls)
     assert results_digest(rt, ft, n, p, n) == results_digest(rf, ff, n, p, n)
+
+
+@pytest.mark.parametrize("n,p,steps", [(136, 8192, 2), (130, 6000, 2)])
+def test_tc_one_group_wide_precision(n, p, steps):
+    """Precisions where one epilogue group per CTA is used (two groups' windows do not fit)."""
+    A = random_uniform_soa(n, p, seed=5 * n + p)
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res_o = HostResults.alloc(n, 1, ref.L, True)
+    ref.run(True, True, 0, steps, res_o)
+    fin_o = A.copy()
+    ref.fetch(fin_o)
+    res_d, fin_d = _device_run(A, n, p, steps, True)
+    assert not first_mismatch(fin_o, fin_d, p)
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+def test_dfma_wide_precision_16k():
+    """p = 16384 on the DFMA engine (16-column CTAs) against the oracle."""
+    n, p, steps = 40, 16384, 2
+    A = random_uniform_soa(n, p, seed=99)
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res_o = HostResults.alloc(n, 1, ref.L, True)
+    ref.run(True, True, 0, steps, res_o)
+    fin_o = A.copy()
+    ref.fetch(fin_o)
+    res_d, fin_d = _device_run(A, n, p, steps, True)
+    assert not first_mismatch(fin_o, fin_d, p)
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
