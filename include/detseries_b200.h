@@ -161,8 +161,9 @@ int ds_profile_read(ds_ctx *ctx, double *update_ms, int64_t *launches, double *l
 /* Internal engine counters (observability; no reference counterpart):
  * out[0] = elements the tensor-core update handed to the exact fallback
  * (short product undecided / normalisation uncertain), out[1] = 1 if the
- * tensor-core update engine is active, out[2] = 1 if the DFMA engine is.
- * Writes min(n, 3) values. */
+ * tensor-core update engine is active, out[2] = 1 if the DFMA engine is,
+ * out[3] = elements whose predicted normalisation (single-pass rounding) was
+ * wrong and which went to the exact fallback.  Writes min(n, 4) values. */
 int ds_counters(ds_ctx *ctx, int64_t *out, int n);
 
 /* Last error message of this context (or of the last failed ds_create when

@@ -1144,8 +1144,9 @@ int ds_counters(ds_ctx* ctx, int64_t* out, int n) {
   int32_t st[8];
   CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  int64_t v[3] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.enabled && !ctx->tc.enabled) ? 1 : 0};
-  for (int q = 0; q < n && q < 3; q++) out[q] = v[q];
+  int64_t v[4] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.enabled && !ctx->tc.enabled) ? 1 : 0,
+                  (int64_t)(uint32_t)st[7]};
+  for (int q = 0; q < n && q < 4; q++) out[q] = v[q];
   return DS_OK;
 }
 

@@ -42,6 +42,14 @@ struct SWin {
   uint32_t cb;
   bool sticky;
   uint32_t curA;
+  // direct mode (single pass): the normalisation offset off = 32 obase + ors of
+  // the result was predicted, so each window limb S_w is turned into the
+  // truncated result limb l = w - obase - 1 (bits [off + 32 l, +32)) as soon as
+  // it is produced and written in place to slot l + 1; S_0, S_1 (round/sticky
+  // bits) and the last two S limbs (verification) are kept in registers
+  bool single;
+  int obase, ors;
+  uint32_t sprev, sprev2, s0, s1;
 
   __device__ __forceinline__ void base(uint32_t* S, int nth) {
     sa = (uint32_t)__cvta_generic_to_shared(S);
@@ -66,7 +74,20 @@ struct SWin {
       s = (uint32_t)t;
       cb = (uint32_t)(t >> 32);
     }
-    set(w, s);
+    put(s);
+  }
+
+  __device__ __forceinline__ void put(uint32_t s) {
+    if (single) {
+      if (w == 0) s0 = s;
+      if (w == 1) s1 = s;
+      const int sl = w - obase;  // slot of result limb l = w - obase - 1 (0, L + 1: scratch)
+      if (sl >= 0) set(sl, __funnelshift_r(sprev, s, ors));
+      sprev2 = sprev;
+      sprev = s;
+    } else {
+      set(w, s);
+    }
     w++;
   }
 
@@ -77,12 +98,17 @@ struct SWin {
     return v;
   }
 
-  __device__ void init(int L_, bool xa_, bool sub_, bool yzero_, int64_t shift) {
+  // off >= 0: direct mode with the predicted normalisation offset (in-place windows only)
+  __device__ void init(int L_, bool xa_, bool sub_, bool yzero_, int64_t shift, int off = -1) {
     L = L_; xa = xa_; sub = sub_; yzero = yzero_;
     if (shift > 32 * (int64_t)(L + 3)) shift = 32 * (int64_t)(L + 3);
     dq = (int)(shift >> 5);
     dr = (int)(shift & 31);
     prev = 0; q = 0; w = 0; cb = 0; sticky = false; curA = 0;
+    single = off >= 0;
+    obase = off >> 5;
+    ors = off & 31;
+    sprev = sprev2 = s0 = s1 = 0u;
     if (xa) {
       set(0, 0u);
       set(L + 1, 0u);
@@ -172,9 +198,29 @@ struct SWin {
     uint32_t cy = sub ? (cb ^ 1u) : cb;
     addc_n<NL>(X, X, Y, cy);
     cb = sub ? (cy ^ 1u) : cy;
-    const uint32_t adw = at(w);
+    if (single && w <= 1) {  // keep S_0, S_1 for the rounding bits
 #pragma unroll
-    for (int k = 0; k < NL; k++) sts32(adw + (uint32_t)k * sb, X[k]);
+      for (int k = 0; k < NL; k++) {
+        if (w + k == 0) s0 = X[k];
+        if (w + k == 1) s1 = X[k];
+      }
+    }
+    // store S_w (two-pass) or the shifted result limb w - obase - 1 to slot
+    // w - obase (direct mode).  Slots 0 and L + 1 are scratch by then (their
+    // X / a reads happened earlier or in this block's loads), so the only write
+    // to skip is slot -1 (first block, obase 1).
+    const uint32_t adw = at(single ? w - obase : w);
+    const bool skip0 = single && w < obase;
+    const int rse = single ? ors : 0;
+    uint32_t sp = sprev;
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+      const uint32_t v = __funnelshift_r(single ? sp : X[k], X[k], rse);  // two-pass: funnel(x, x, 0) = x
+      if (k > 0 || !skip0) sts32(adw + (uint32_t)k * sb, v);
+      sp = X[k];
+    }
+    sprev2 = NL >= 2 ? X[NL - 2] : sprev;
+    sprev = X[NL - 1];
     w += NL;
     if (xa) {
       prev = yp;
@@ -477,6 +523,71 @@ __device__ __forceinline__ void round_out(SWin& S, int neg, int64_t E, int L, in
   if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&status[2], 1);
   *oexp = (int32_t)e;
   *ocls = neg ? DS_CLS_NEG : DS_CLS_POS;
+}
+
+// Direct mode finish: the truncated result limbs are already in slots 1..L.
+// Verify the predicted normalisation (nonnegative window, MSB of the top limb
+// set, nothing above it), round to nearest-even at p bits (round bit / sticky
+// from S_0, S_1 and the low result limb, carry propagated while it lasts) and
+// write exponent and class.  Returns false on a misprediction (the caller puts
+// a back and hands the element to the exact fallback).
+__device__ __forceinline__ bool round_direct(SWin& S, int neg, int64_t E, int L, int p, int zb, int32_t* oexp,
+                                             uint8_t* ocls, int32_t* status) {
+  const int off = 32 * S.obase + S.ors;
+  if (S.sub && S.cb) return false;                       // negative window
+  const uint32_t top = lds32(S.at(L));
+  if (!(top >> 31)) return false;                         // normalised lower than predicted
+  // bits at or above window bit off + 32 L: S_{obase+L} >> ors and, for obase 0, S_{L+1}
+  const uint32_t s_hi = S.obase ? S.sprev : S.sprev2;     // S_{obase + L}
+  if (S.ors ? (s_hi >> S.ors) : s_hi) return false;
+  if (S.obase == 0 && S.sprev) return false;
+  uint32_t out0 = lds32(S.at(1));
+  // round bit = window bit off + zb - 1, sticky = the bits below it (+ S.sticky)
+  uint32_t rbit;
+  bool stk = S.sticky;
+  if (zb >= 1) {
+    rbit = (out0 >> (zb - 1)) & 1u;
+    if (zb >= 2 && (out0 & ((1u << (zb - 1)) - 1u))) stk = true;
+    // window bits [0, off): S_0 and the low off - 32 bits of S_1
+    if (off >= 32) {
+      if (S.s0 || (off > 32 && (S.s1 & ((off - 32 >= 32) ? 0xffffffffu : ((1u << (off - 32)) - 1u))))) stk = true;
+    } else if (off > 0 && (S.s0 & ((1u << off) - 1u))) {
+      stk = true;
+    }
+  } else {
+    // zb = 0: round bit = window bit off - 1, sticky = window bits [0, off - 1)
+    const int rb = off - 1;
+    if (rb < 0) {
+      rbit = 0u;
+    } else if (rb < 32) {
+      rbit = (S.s0 >> rb) & 1u;
+      if (rb > 0 && (S.s0 & ((1u << rb) - 1u))) stk = true;
+    } else {
+      rbit = (S.s1 >> (rb - 32)) & 1u;
+      if (S.s0 || (rb > 32 && (S.s1 & ((1u << (rb - 32)) - 1u)))) stk = true;
+    }
+  }
+  const uint32_t lsb = (out0 >> zb) & 1u;
+  uint32_t carry = rbit & ((stk ? 1u : 0u) | lsb);
+  if (zb) out0 &= ~((1u << zb) - 1u);
+  uint32_t r0 = out0 + (carry << zb);
+  carry = r0 < out0 ? 1u : 0u;
+  sts32(S.at(1), r0);
+  for (int l = 1; l < L && carry; l++) {  // usually stops at once
+    const uint32_t a2 = S.at(l + 1);
+    const uint32_t v = lds32(a2) + 1u;
+    sts32(a2, v);
+    carry = v == 0u ? 1u : 0u;
+  }
+  int64_t e = E + off - 32;
+  if (carry) {  // rounded up to 2^p
+    sts32(S.at(L), 0x80000000u);
+    e += 1;
+  }
+  if (e < DS_EMIN || e > DS_EMAX) atomicAdd(&status[2], 1);
+  *oexp = (int32_t)e;
+  *ocls = neg ? DS_CLS_NEG : DS_CLS_POS;
+  return true;
 }
 
 __device__ __forceinline__ void round_write(SWin& S, int neg, int64_t E, int L, int p, int zb, uint32_t* O,

@@ -53,6 +53,7 @@ struct TcArgs {
   int tn;                  // output digit columns per MMA tile (N)
   int br;                  // Toeplitz bank rows: ntiles * tn + 32 (nks - 1)
   int tma_ok;              // a planes reachable by the tile tensor map
+  int no_direct;           // DS_TC_NO_DIRECT: always the two-pass rounding
   int nrows, ncols, kstart, skip_col, n;
   int kmin;                // first column to update (kstart = kmin rounded down to 4: aligned tiles)
   int tile0, tskip;        // column tile of blockIdx.x 0; tile index skipped (-1: none)
@@ -383,8 +384,35 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       SWin S;
       S.base(Sw, TM);
       Emit em;
+      // direct (single-pass) rounding: predict the result's normalisation from the
+      // leading bits -- a's top 64 bits (exact, from the window) and t's fp64
+      // estimate (relative error < 2^-50) -- when it is certain with a 2^-40 margin
+      // (cancellation of at most ~20 bits); an exactly predicted negative window
+      // (equal exponents, |t| > |a|) swaps the operand roles.  Others: two-pass.
+      int off_pred = -1;
+      if (process && !za && tile_io && !a.no_direct) {
+        const uint64_t atop = ((uint64_t)Sw[L * TM] << 32) | Sw[(L - 1) * TM];
+        const double am = (double)atop * 0x1p-63;  // [1, 2)
+        const double prv = a.zf[zr] * a.bf[k];
+        const double tm = norm ? prv * 0.5 : prv;  // [1, 2)
+        const int64_t sh = xa ? d : -d;
+        const double yv = sh < 200 ? ldexp(xa ? tm : am, -(int)sh) : 0.0;
+        double sd = sub ? (xa ? am : tm) - yv : (xa ? am : tm) + yv;
+        if (sd < 0.0) {  // only xa, d == 0, sub: t - a with the roles swapped
+          sd = -sd;
+          xa = false;
+          neg = (int)(((a.zcls[zr] & 1) ^ (a.bcls[k] & 1)) ^ 1);
+          E = (int64_t)a.zexp[zr] + a.bexp[k] - (norm ? 0 : 1);
+        }
+        if (sd > 0x1p-20) {
+          int e2;
+          const double fr = frexp(sd, &e2);  // sd = fr 2^e2, fr in [0.5, 1)
+          const int off = 32 + (e2 - 1);
+          if (fr - 0.5 > 0x1p-41 && 1.0 - fr > 0x1p-41 && off >= 0 && off <= 33) off_pred = off;
+        }
+      }
       if (process) {
-        S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d));
+        S.init(L, xa, sub, za, xa ? d : (za ? 0 : -d), off_pred);
         em.S = &S;
         // every lane's P' is shifted to the normalised position (non-normalised
         // products x 2, nsh = 1): t's LSB at r' = p + 2 zb for all lanes, so T limbs
@@ -469,12 +497,18 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
         if (em.excess) ok = false;
       }
       if (process && !ok) fallback = true;
-      if (process && ok) {
+      if (process && ok && S.single) {
+        if (!round_direct(S, neg, E, L, a.p, a.zb, a.a_exp + idx, a.a_cls + idx, a.status)) {
+          fallback = true;
+          atomicAdd(&a.status[7], 1);  // direct-mode misprediction (counted; exact fallback)
+        }
+      } else if (process && ok) {
         if (tile_io)
           round_out<true>(S, neg, E, L, a.p, a.zb, nullptr, 0, a.a_exp + idx, a.a_cls + idx, a.status);
         else
           round_write(S, neg, E, L, a.p, a.zb, a.a_limbs + idx, a.a_count, a.a_exp + idx, a.a_cls + idx, a.status);
-      } else if (fallback) {
+      }
+      if (fallback) {
         if (tile_io && process) {  // the window was written: the tile store must put a back unchanged
           const uint32_t* A = a.a_limbs + idx;
           for (int l = 0; l < L; l++) Sw[(l + 1) * TM] = A[(int64_t)l * a.a_count];
@@ -713,6 +747,7 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   }
   a.tma_ok = w->amap_ok;
   a.rbr = RBR;
+  a.no_direct = getenv("DS_TC_NO_DIRECT") ? 1 : 0;
   const int ntile = (ncols + TM - 1) / TM;
   const int nrg = (nrows + RBR - 1) / RBR;
   const int ts = la_col >= 0 ? (la_col - kstart) / TM : -1;  // tile holding the lookahead column

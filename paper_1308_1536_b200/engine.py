@@ -166,9 +166,10 @@ class DeviceElimination:
 
     def counters(self) -> dict:
         """Internal engine counters (ds_counters): tensor-core fallback elements, active update engine."""
-        out = (ctypes.c_int64 * 3)()
-        _check(self.lib.ds_counters(self.ctx, out, 3), self.ctx, "ds_counters", self.rank)
-        return {"tc_fallback_elements": int(out[0]), "tc_engine": bool(out[1]), "dfma_engine": bool(out[2])}
+        out = (ctypes.c_int64 * 4)()
+        _check(self.lib.ds_counters(self.ctx, out, 4), self.ctx, "ds_counters", self.rank)
+        return {"tc_fallback_elements": int(out[0]), "tc_engine": bool(out[1]), "dfma_engine": bool(out[2]),
+                "direct_mispredictions": int(out[3])}
 
     def stream(self) -> int:
         return self.lib.ds_stream(self.ctx) or 0
