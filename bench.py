@@ -86,7 +86,7 @@ def gamma_cache_path(n: int, p: int) -> str:
     return os.path.join(ROOT, "data", f"beta_gammas_p{p}_N{n}.npz")
 
 
-def build_input(args, pinned: bool, rank: int = 0, world: int = 1):
+def build_input(args, pinned: bool, rank: int = 0, world: int = 1, agree=None):
     """(SoA matrix, description, seconds).  beta: bit-identical to
     genmat.beta_matrix(load_zeros(zeros, Precision(p), n), n, SpougeGamma(),
     Precision(p)) (tests/test_hostgen.py), built by the multi-threaded C
@@ -111,6 +111,8 @@ def build_input(args, pinned: bool, rank: int = 0, world: int = 1):
         bb.fill(probe)
         # later columns (larger ordinates) cost more per entry: 1.3x margin
         est = 1.3 * (time.perf_counter() - t0) * args.n / probe
+        if agree is not None:  # every rank must build the same family: decide on the slowest rank's estimate
+            est = agree(est)
         if est <= args.gen_budget:
             bb.fill(args.n)
             A = bb.out
@@ -272,7 +274,13 @@ def main():
 
     n, p = args.n, args.prec
     L = (p + 31) // 32
-    A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world)  # this rank's rows
+    agree = None
+    if use_dist:
+        def agree(x: float) -> float:
+            t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+    A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world, agree=agree)  # this rank's rows
     eng = DeviceElimination(n, p, "real", local, rank, world)
     stream = torch.cuda.current_stream()
     pivot = None
