@@ -1203,6 +1203,36 @@ static int copy_vec(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32
   return DS_OK;
 }
 
+// minors rows [r0, r1) of a world-1 context, the first `width` entries of each
+// (row m-1 holds m entries), on stream s: one 2D copy per limb plane
+static int copy_row_range(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
+                          int r0, int r1, int width, cudaStream_t s) {
+  if (!dst || !dst->limbs || r1 <= r0 || width <= 0) return DS_OK;
+  const int n = ctx->n, L = ctx->L;
+  const size_t rows = (size_t)(r1 - r0);
+  const int64_t o = (int64_t)r0 * n;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++)
+      CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + o, sizeof(uint32_t) * n,
+                           limbs + ((int64_t)c * L + l) * ctx->a_count + o, sizeof(uint32_t) * n,
+                           sizeof(uint32_t) * width, rows, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + o, sizeof(int32_t) * n, ex + (int64_t)c * ctx->a_count + o,
+                         sizeof(int32_t) * n, sizeof(int32_t) * width, rows, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + o, n, cl + (int64_t)c * ctx->a_count + o, n, width, rows,
+                         cudaMemcpyDeviceToHost, s));
+  }
+  return DS_OK;
+}
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl) {
   // owned minors rows (local index jl <-> global row rank + jl*world) into a
   // full n*n host matrix
@@ -1222,14 +1252,24 @@ static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int3
   return DS_OK;
 }
 
-int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) {
+// minors_from: minors rows below it were already copied (progressive D2H in ds_run)
+static int results_fetch_from(ds_ctx* ctx, int upto, ds_results* r, int minors_from) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
   int rc;
   if ((rc = copy_vec(ctx, &r->pivots, ctx->piv_limbs, ctx->piv_exp, ctx->piv_cls, ctx->n, upto)) != DS_OK) return rc;
   if ((rc = copy_vec(ctx, &r->dets, ctx->det_limbs, ctx->det_exp, ctx->det_cls, ctx->n, upto)) != DS_OK) return rc;
-  if ((rc = copy_rows(ctx, &r->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls)) != DS_OK) return rc;
-  if ((rc = copy_rows(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls)) != DS_OK) return rc;
+  if (minors_from > 0) {
+    if ((rc = copy_row_range(ctx, &r->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, minors_from, ctx->n,
+                             ctx->n, ctx->stream)) != DS_OK)
+      return rc;
+    if ((rc = copy_row_range(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls, minors_from, ctx->n,
+                             ctx->n, ctx->stream)) != DS_OK)
+      return rc;
+  } else {
+    if ((rc = copy_rows(ctx, &r->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls)) != DS_OK) return rc;
+    if ((rc = copy_rows(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls)) != DS_OK) return rc;
+  }
   if (r->row_flags) {
     // flags of rows this rank owns (m-1 % world == rank)
     uint8_t* tmp = (uint8_t*)malloc(ctx->n);
@@ -1242,15 +1282,38 @@ int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) {
   return DS_OK;
 }
 
+int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) { return results_fetch_from(ctx, upto, r, 0); }
+
 int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop_step, ds_results* res,
            int* steps_done) {
   if (ctx->world != 1) return DS_INVALID;
   if (start_step < 0 || stop_step > ctx->n || start_step > stop_step) return DS_INVALID;
   int rc;
+  // progressive D2H of the minors (pinned host buffers): rows finalised by
+  // the emission are copied in batches on the side stream while the
+  // elimination runs -- row m-1 holds m entries (triangle)
+  const bool prog = res && collect_minors && series && res->signed_minors.limbs && res->normalized.limbs &&
+                    host_pinned(res->signed_minors.limbs) && host_pinned(res->normalized.limbs) &&
+                    host_pinned(res->signed_minors.exp) && host_pinned(res->signed_minors.cls) &&
+                    host_pinned(res->normalized.exp) && host_pinned(res->normalized.cls) &&
+                    res->signed_minors.count == (int64_t)ctx->n * ctx->n && !getenv("DS_NO_PROGRESSIVE_D2H");
+  const int BATCH = 64;
+  int copied = 0;
   ctx->la_limit = stop_step;
   for (int i = start_step; i < stop_step; i++) {
     if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) { ctx->la_limit = -1; return rc; }
     if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) { ctx->la_limit = -1; return rc; }
+    if (prog && (i + 1 - start_step) % BATCH == 0) {
+      const int r1 = i + 2 < ctx->n ? i + 2 : ctx->n;  // rows 0 .. i+1 are final after step i
+      if ((rc = copy_row_range(ctx, &res->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, copied, r1, r1,
+                               ctx->side)) != DS_OK ||
+          (rc = copy_row_range(ctx, &res->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls, copied, r1, r1,
+                               ctx->side)) != DS_OK) {
+        ctx->la_limit = -1;
+        return rc;
+      }
+      copied = r1;
+    }
   }
   ctx->la_limit = -1;
   ctx->la_step = -1;
@@ -1261,7 +1324,7 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
   int upto = failed >= 0 ? failed : stop_step;
   *steps_done = upto;
   if (res) {
-    int rc2 = ds_results_fetch(ctx, upto, res);
+    int rc2 = results_fetch_from(ctx, upto, res, prog ? copied : 0);
     if (rc2 != DS_OK) return rc2;
   }
   if (rc != DS_OK) return rc;

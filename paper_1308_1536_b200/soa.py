@@ -40,9 +40,17 @@ class SoA:
             else:
                 limbs = np.zeros((self.ncomp, self.L, self.count), dtype=np.uint32)
         if exp is None:
-            exp = np.zeros((self.ncomp, self.count), dtype=np.int32)
+            if pinned:
+                exp = _pinned_empty((self.ncomp, self.count), np.int32)
+                exp.fill(0)
+            else:
+                exp = np.zeros((self.ncomp, self.count), dtype=np.int32)
         if cls is None:
-            cls = np.full((self.ncomp, self.count), CLS_PZERO, dtype=np.uint8)
+            if pinned:
+                cls = _pinned_empty((self.ncomp, self.count), np.uint8)
+                cls.fill(CLS_PZERO)
+            else:
+                cls = np.full((self.ncomp, self.count), CLS_PZERO, dtype=np.uint8)
         self.limbs, self.exp, self.cls = limbs, exp, cls
         assert self.limbs.shape == (self.ncomp, self.L, self.count) and self.limbs.dtype == np.uint32
         assert self.limbs.flags.c_contiguous and self.exp.flags.c_contiguous and self.cls.flags.c_contiguous

@@ -137,3 +137,21 @@ def test_dfma_wide_precision_16k():
     res_d, fin_d = _device_run(A, n, p, steps, True)
     assert not first_mismatch(fin_o, fin_d, p)
     assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+def test_progressive_minors_d2h_matches_full_fetch():
+    """ds_run with pinned result buffers streams finalised minors rows to the host during the run
+    (triangle, batches of 64 steps); the outputs must equal a pageable-buffer run's full fetch."""
+    n, p = 300, 1024
+    A = random_uniform_soa(n, p, seed=21)
+    outs = []
+    for pinned in (True, False):
+        with DeviceElimination(n, p, "real") as eng:
+            eng.load(A)
+            res = HostResults.alloc(n, 1, eng.L, True, pinned=pinned)
+            eng.run(True, True, 0, n, res)
+            fin = A.copy()
+            eng.fetch(fin)
+            outs.append((res, fin))
+    (rp, fp), (rq, fq) = outs
+    assert results_digest(rp, fp, n, p, n) == results_digest(rq, fq, n, p, n)
