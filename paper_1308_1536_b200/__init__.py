@@ -28,3 +28,4 @@ from .elim import (EliminationTrace, MinorRow, MinorSeries, apply_pivot_to_row, 
                    laplace_residual, minors_row_from_l, normalize_minors)
 from .parexec import CommStats, WorkerTopology, pack_row, par_eliminate, unpack_row  # noqa: F401
 from .genmat import SpougeGamma, beta_matrix, load_zeros, power_matrix, synth_matrix  # noqa: F401
+from .output import write_dets, write_minors, write_results  # noqa: F401

@@ -127,7 +127,7 @@ static int spouge_gamma(mpc_ptr out, mpc_srcptr z, long bits, int guard) {
 /* a[n][j] = beta_n(gamma_j) for n, j = 1..N (genmat.py:156-190); zeros are
  * decimal strings parsed at precision p (load_zeros, genmat.py:40-73).
  * Returns 0, or -1 if a Gamma evaluation failed to stabilise. */
-static void get_soa(mpfr_ptr x, const ds_soa *s, int c, int64_t idx, int L) {
+void dsh_get_soa(mpfr_ptr x, const ds_soa *s, int c, int64_t idx, int L) {
   uint8_t k = s->cls[c * s->count + idx];
   if (k >= DS_CLS_PZERO) {
     mpfr_set_ui(x, 0, RN);
@@ -221,8 +221,8 @@ int dsh_beta_matrix_cols(int N, long p, const char **zeros, int guard_bits, int 
     mpc_set_fr_fr(z, val, ztmp, RNN);
     if (gammas) {
       int Lw = (int)((work + 31) / 32);
-      get_soa(mpc_realref(g), gammas, 0, j, Lw);
-      get_soa(mpc_imagref(g), gammas, 1, j, Lw);
+      dsh_get_soa(mpc_realref(g), gammas, 0, j, Lw);
+      dsh_get_soa(mpc_imagref(g), gammas, 1, j, Lw);
     } else if (spouge_gamma(g, z, work, 64) != 0) {
       failed = 1;
     }

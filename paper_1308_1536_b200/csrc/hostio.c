@@ -1,0 +1,164 @@
+/* hostio.c -- native output path: the reference CLI's result files written
+ * straight from the ds SoA results, many files in parallel.
+ *
+ *   dets.txt        "<i> <det_i>\n" for i = 1..count          (cli.py:218-221)
+ *   minors_<m>.txt  "<k+1> <signed_k> <normalized_k | undefined>\n"
+ *                   for every emitted size m, k = 0..m-1       (cli.py:224-232)
+ *
+ * Scalars are formatted exactly like format_scalar (scalars.py:89-104):
+ * mpfr_get_str(base 10, `digits` digits, RNDN) -- the call behind gmpy2's
+ * mpfr.digits -- then "<sign>0.<digits>e<exp10>", or "<sign>0" when every
+ * digit is 0; complex scalars are "<re> <im>".  The Python writer
+ * (paper_1308_1536_b200/output.py) restates the same loops over scalar
+ * objects; tests/test_output.py checks both byte-for-byte against files the
+ * reference wrote.
+ */
+#include <errno.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <omp.h>
+
+#include "mp_abi.h"
+#include "../../include/detseries_b200.h"
+
+void dsh_get_soa(mpfr_ptr x, const ds_soa *s, int c, int64_t idx, int L);
+
+typedef struct {
+  char *p;
+  size_t n, cap;
+} obuf;
+
+static int ob_reserve(obuf *b, size_t more) {
+  if (b->n + more <= b->cap) return 0;
+  size_t cap = b->cap ? b->cap : 1 << 16;
+  while (cap < b->n + more) cap *= 2;
+  char *q = (char *)realloc(b->p, cap);
+  if (!q) return -ENOMEM;
+  b->p = q;
+  b->cap = cap;
+  return 0;
+}
+
+/* one real component, format_scalar semantics; dbuf holds digits + 2 bytes */
+static void fmt_real(obuf *b, mpfr_ptr x, int digits, char *dbuf) {
+  mpfr_exp_t e10 = 0;
+  mpfr_get_str(dbuf, &e10, 10, (size_t)digits, x, MPFR_RNDN);
+  const char *d = dbuf;
+  int neg = 0;
+  if (*d == '-') {
+    neg = 1;
+    d++;
+  }
+  int allz = 1;
+  for (const char *q = d; *q; q++)
+    if (*q != '0') {
+      allz = 0;
+      break;
+    }
+  size_t dl = strlen(d);
+  char *o = b->p + b->n;
+  if (neg) *o++ = '-';
+  if (allz) {
+    *o++ = '0';
+  } else {
+    *o++ = '0';
+    *o++ = '.';
+    memcpy(o, d, dl);
+    o += dl;
+    o += sprintf(o, "e%ld", (long)e10);
+  }
+  b->n = (size_t)(o - b->p);
+}
+
+static void fmt_scalar(obuf *b, mpfr_ptr x, const ds_soa *s, int ncomp, int64_t idx, int L, int digits,
+                       char *dbuf) {
+  for (int c = 0; c < ncomp; c++) {
+    if (c) b->p[b->n++] = ' ';
+    dsh_get_soa(x, s, c, idx, L);
+    fmt_real(b, x, digits, dbuf);
+  }
+}
+
+static int write_file(const char *path, const obuf *b) {
+  FILE *f = fopen(path, "wb");
+  if (!f) return -errno;
+  size_t w = fwrite(b->p, 1, b->n, f);
+  int rc = (w == b->n) ? 0 : -EIO;
+  if (fclose(f) != 0 && rc == 0) rc = -EIO;
+  return rc;
+}
+
+/* worst-case text bytes of one formatted component */
+static size_t comp_bytes(int digits) { return (size_t)digits + 32; }
+
+int dsh_write_dets(const char *path, int count, int kind, int L, long p, const ds_soa *dets, int digits) {
+  const int ncomp = kind == DS_KIND_COMPLEX ? 2 : 1;
+  obuf b = {0, 0, 0};
+  mpfr_t x;
+  mpfr_init2(x, p);
+  char *dbuf = (char *)malloc((size_t)digits + 2);
+  int rc = dbuf ? 0 : -ENOMEM;
+  for (int i = 0; i < count && rc == 0; i++) {
+    if ((rc = ob_reserve(&b, 24 + ncomp * comp_bytes(digits))) != 0) break;
+    b.n += (size_t)sprintf(b.p + b.n, "%d ", i + 1);
+    fmt_scalar(&b, x, dets, ncomp, i, L, digits, dbuf);
+    b.p[b.n++] = '\n';
+  }
+  if (rc == 0) rc = write_file(path, &b);
+  mpfr_clear(x);
+  free(dbuf);
+  free(b.p);
+  return rc;
+}
+
+/* flags[m-1]: 0 = size m not emitted, 1 = emitted with normalized None
+ * (leading signed minor zero), 3 = emitted with normalized values.  Row m-1
+ * of sig / nrm (count n*n) holds the m entries of size m. */
+int dsh_write_minors(const char *outdir, int n, int kind, int L, long p, const ds_soa *sig, const ds_soa *nrm,
+                     const uint8_t *flags, int digits, int nthreads) {
+  const int ncomp = kind == DS_KIND_COMPLEX ? 2 : 1;
+  int err = 0;
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+  {
+    obuf b = {0, 0, 0};
+    mpfr_t x;
+    mpfr_init2(x, p);
+    char *dbuf = (char *)malloc((size_t)digits + 2);
+    char path[4096];
+#pragma omp for schedule(dynamic, 1)
+    for (int m = n; m >= 2; m--) {  /* large files first */
+      if (!flags[m - 1] || err) continue;
+      int rc = dbuf ? 0 : -ENOMEM;
+      b.n = 0;
+      const int64_t row = (int64_t)(m - 1) * n;
+      for (int k = 0; k < m && rc == 0; k++) {
+        if ((rc = ob_reserve(&b, 48 + 2 * ncomp * comp_bytes(digits))) != 0) break;
+        b.n += (size_t)sprintf(b.p + b.n, "%d ", k + 1);
+        fmt_scalar(&b, x, sig, ncomp, row + k, L, digits, dbuf);
+        b.p[b.n++] = ' ';
+        if (flags[m - 1] == 1) {
+          memcpy(b.p + b.n, "undefined", 9);
+          b.n += 9;
+        } else {
+          fmt_scalar(&b, x, nrm, ncomp, row + k, L, digits, dbuf);
+        }
+        b.p[b.n++] = '\n';
+      }
+      if (rc == 0) {
+        snprintf(path, sizeof(path), "%s/minors_%d.txt", outdir, m);
+        rc = write_file(path, &b);
+      }
+      if (rc != 0) {
+#pragma omp critical
+        err = rc;
+      }
+    }
+    mpfr_clear(x);
+    free(dbuf);
+    free(b.p);
+  }
+  return err;
+}

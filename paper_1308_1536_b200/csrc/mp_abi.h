@@ -50,6 +50,7 @@ int mpfr_zero_p(mpfr_srcptr);
 int mpfr_signbit(mpfr_srcptr);
 long mpfr_get_si(mpfr_srcptr, mpfr_rnd_t);
 double mpfr_get_d(mpfr_srcptr, mpfr_rnd_t);
+char *mpfr_get_str(char *, mpfr_exp_t *, int, size_t, mpfr_srcptr, mpfr_rnd_t);
 
 void mpc_init2(mpc_ptr, mpfr_prec_t);
 void mpc_clear(mpc_ptr);
