@@ -42,6 +42,16 @@ static void put_soa(ds_soa *s, int64_t idx, mpfr_srcptr x, int L) {
   s->cls[idx] = mpfr_signbit(x) ? DS_CLS_NEG : DS_CLS_POS;
 }
 
+
+/* component c of element idx (complex SoA: c = 0 real, 1 imaginary) */
+void dsh_put_soa(ds_soa *s, int c, int64_t idx, mpfr_srcptr x, int L) {
+  ds_soa v = *s;
+  v.limbs = s->limbs + (int64_t)c * L * s->count;
+  v.exp = s->exp + (int64_t)c * s->count;
+  v.cls = s->cls + (int64_t)c * s->count;
+  put_soa(&v, idx, x, L);
+}
+
 /* Spouge coefficients at (a, work2): genmat.py:100-112 */
 static void spouge_coeffs(mpfr_t *c, long a, long w) {
   mpfr_t pi, t, km, lg, s, f;

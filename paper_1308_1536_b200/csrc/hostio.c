@@ -162,3 +162,187 @@ int dsh_write_minors(const char *outdir, int n, int kind, int L, long p, const d
   }
   return err;
 }
+
+/* ---------------------------------------------------------------- MPMAT
+ * MatrixBuffer.save / load (matrix.py:109-140): header
+ * "MPMAT 1 <kind> <n> <bits>\n", then the n*n scalars row-major, one per line,
+ * format_scalar with its default digits int(bits*log10(2)) + 3 -- the text
+ * round-trips bit-exactly through parse_scalar (mpfr from the decimal token,
+ * RNDN at bits).  The reference's checkpoints (cli.py:110-120) are this
+ * file plus state.txt. */
+int mpfr_set_str(mpfr_ptr, const char *, int, mpfr_rnd_t);
+void dsh_put_soa(ds_soa *s, int c, int64_t idx, mpfr_srcptr x, int L);
+
+static int default_digits(long p) { return (int)((double)p * 0.30102999566398120) + 3; }
+
+int dsh_write_mpmat(const char *path, int n, int kind, int L, long p, const ds_soa *m, int nthreads) {
+  const int ncomp = kind == DS_KIND_COMPLEX ? 2 : 1;
+  const int digits = default_digits(p);
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+  FILE *f = fopen(path, "wb");
+  if (!f) return -errno;
+  int rc = fprintf(f, "MPMAT 1 %s %d %ld\n", kind == DS_KIND_COMPLEX ? "complex" : "real", n, p) > 0 ? 0 : -EIO;
+  const int64_t total = (int64_t)n * n, chunk = 512;
+  const int R = 4 * nthreads;  /* chunks per round */
+  obuf *bufs = (obuf *)calloc((size_t)R, sizeof(obuf));
+  if (!bufs) rc = -ENOMEM;
+  /* rounds of R chunks: formatted in parallel (any thread count), written in order */
+  for (int64_t base = 0; base < total && rc == 0; base += (int64_t)R * chunk) {
+    int err = 0;
+#pragma omp parallel num_threads(nthreads)
+    {
+      mpfr_t x;
+      mpfr_init2(x, p);
+      char *dbuf = (char *)malloc((size_t)digits + 2);
+#pragma omp for schedule(dynamic, 1)
+      for (int c = 0; c < R; c++) {
+        obuf *b = &bufs[c];
+        b->n = 0;
+        const int64_t i0 = base + (int64_t)c * chunk;
+        for (int64_t i = i0; i < i0 + chunk && i < total; i++) {
+          if (!dbuf || ob_reserve(b, 8 + ncomp * comp_bytes(digits)) != 0) {
+#pragma omp critical
+            err = -ENOMEM;
+            break;
+          }
+          fmt_scalar(b, x, m, ncomp, i, L, digits, dbuf);
+          b->p[b->n++] = '\n';
+        }
+      }
+      mpfr_clear(x);
+      free(dbuf);
+    }
+    for (int c = 0; c < R && !err; c++)
+      if (bufs[c].n && fwrite(bufs[c].p, 1, bufs[c].n, f) != bufs[c].n) err = -EIO;
+    rc = err;
+  }
+  for (int q = 0; bufs && q < R; q++) free(bufs[q].p);
+  free(bufs);
+  if (fclose(f) != 0 && rc == 0) rc = -EIO;
+  return rc;
+}
+
+/* [-+]?[0-9]+(\.[0-9]+)?([eE][-+]?[0-9]+)?  (scalars.py:32) over [s, e) */
+static int real_token_ok(const char *s, const char *e) {
+  if (s < e && (*s == '-' || *s == '+')) s++;
+  const char *d = s;
+  while (s < e && *s >= '0' && *s <= '9') s++;
+  if (s == d) return 0;
+  if (s < e && *s == '.') {
+    s++;
+    d = s;
+    while (s < e && *s >= '0' && *s <= '9') s++;
+    if (s == d) return 0;
+  }
+  if (s < e && (*s == 'e' || *s == 'E')) {
+    s++;
+    if (s < e && (*s == '-' || *s == '+')) s++;
+    d = s;
+    while (s < e && *s >= '0' && *s <= '9') s++;
+    if (s == d) return 0;
+  }
+  return s == e;
+}
+
+/* MatrixBuffer.load: parse into `out` (ncomp x L x n*n, caller-allocated for
+ * the header values read by dsh_mpmat_header).  Returns 0, -1 malformed
+ * header/token, -2 truncated, or -errno. */
+int dsh_mpmat_header(const char *path, int *n, int *kind, long *bits) {
+  FILE *f = fopen(path, "rb");
+  if (!f) return -errno;
+  char kbuf[16] = {0};
+  int ver = 0;
+  int got = fscanf(f, "MPMAT %d %15s %d %ld", &ver, kbuf, n, bits);
+  fclose(f);
+  if (got != 4 || ver != 1) return -1;
+  if (!strcmp(kbuf, "real")) *kind = DS_KIND_REAL;
+  else if (!strcmp(kbuf, "complex")) *kind = DS_KIND_COMPLEX;
+  else return -1;
+  return 0;
+}
+
+int dsh_read_mpmat(const char *path, int n, int kind, int L, long p, ds_soa *out, int nthreads) {
+  const int ncomp = kind == DS_KIND_COMPLEX ? 2 : 1;
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+  FILE *f = fopen(path, "rb");
+  if (!f) return -errno;
+  if (fseek(f, 0, SEEK_END) != 0) {
+    fclose(f);
+    return -EIO;
+  }
+  long sz = ftell(f);
+  rewind(f);
+  char *buf = (char *)malloc((size_t)sz + 1);
+  if (!buf) {
+    fclose(f);
+    return -ENOMEM;
+  }
+  size_t rd = fread(buf, 1, (size_t)sz, f);
+  fclose(f);
+  buf[rd] = 0;
+  const int64_t total = (int64_t)n * n;
+  char **lines = (char **)malloc(sizeof(char *) * (size_t)(total + 1));
+  int rc = lines ? 0 : -ENOMEM;
+  /* line starts (first line = header) */
+  char *q = strchr(buf, '\n');
+  int64_t cnt = 0;
+  while (rc == 0 && q && cnt < total) {
+    q++;
+    if (!*q) break;
+    lines[cnt++] = q;
+    q = strchr(q, '\n');
+  }
+  if (rc == 0 && cnt < total) rc = -2;
+  if (rc == 0) {
+    int err = 0;
+#pragma omp parallel num_threads(nthreads)
+    {
+      mpfr_t x;
+      mpfr_init2(x, p);
+      char *tok = (char *)malloc(65536);
+      size_t tcap = 65536;
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < total; i++) {
+        if (err) continue;
+        char *s = lines[i];
+        char *e = strchr(s, '\n');
+        if (!e) e = s + strlen(s);
+        for (int c = 0; c < ncomp; c++) {
+          while (s < e && (*s == ' ' || *s == '\t' || *s == '\r')) s++;
+          char *t = s;
+          while (t < e && *t != ' ' && *t != '\t' && *t != '\r') t++;
+          size_t len = (size_t)(t - s);
+          if (!real_token_ok(s, t)) {
+#pragma omp critical
+            err = -1;
+            break;
+          }
+          if (len + 1 > tcap) {
+            char *nt = (char *)realloc(tok, len + 1);
+            if (!nt) {
+              err = -ENOMEM;
+              break;
+            }
+            tok = nt;
+            tcap = len + 1;
+          }
+          memcpy(tok, s, len);
+          tok[len] = 0;
+          mpfr_set_str(x, tok, 10, MPFR_RNDN);
+          dsh_put_soa(out, c, i, x, L);
+          s = t;
+        }
+        if (!err) {  /* nothing but blanks may follow */
+          while (s < e && (*s == ' ' || *s == '\t' || *s == '\r')) s++;
+          if (s != e) err = -1;
+        }
+      }
+      mpfr_clear(x);
+      free(tok);
+    }
+    rc = err;
+  }
+  free(lines);
+  free(buf);
+  return rc;
+}

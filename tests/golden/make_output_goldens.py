@@ -8,8 +8,10 @@ Run in this container only (the reference is absent on the GPU box):
 For a few cases of make_goldens.py (same inputs), the UNMODIFIED reference
 runs eliminate() and writes dets.txt / minors_<m>.txt with its own
 cli._write_dets / cli._write_minors (cli.py:218-232) at the CLI's default
-digits (Precision.decimal_digits, cli.py:326) and, for one case, digits=25.
-tests/test_output.py compares the native and Python writers byte for byte.
+digits (Precision.decimal_digits, cli.py:326) and, for one case, digits=25;
+and, for two cases, a mid-run checkpoint directory with its own
+cli._Checkpointer.write (matrix.mpmat + state.txt, cli.py:110-120).
+tests/test_output.py compares the product's writers byte for byte.
 """
 
 import os
@@ -62,5 +64,34 @@ def main():
     record("complex8_r9_p192", MatrixBuffer(8, "complex", prec, rows))
 
 
+def record_checkpoint(name, A, stop_after):
+    """The reference's _Checkpointer.write (cli.py:110-120) after `stop_after` steps."""
+    from detseries.cli import _Checkpointer
+    d = os.path.join(OUT, "ckpt_" + name)
+    shutil.rmtree(d, ignore_errors=True)
+    ck = _Checkpointer(d, every=0)
+
+    def hook(completed, buf, trace):
+        if completed == stop_after:
+            ck.write(buf, trace)
+            return True
+        return False
+
+    eliminate(A, collect_minors=True, series=True, step_hook=lambda c, B, t: hook(c, B, t))
+    print("ckpt", name, sorted(os.listdir(d)))
+
+
+def main_ckpt():
+    record_checkpoint("uniform13_s5_p192_step4", synth_matrix("random_uniform", 13, 5, Precision(192)), 4)
+    prec = Precision(192)
+    import random
+    rnd = random.Random(9)
+    with prec.context():
+        rows = [[mpc(gmpy2.mpfr(rnd.uniform(-1, 1)), gmpy2.mpfr(rnd.uniform(-1, 1))) for _ in range(8)]
+                for _ in range(8)]
+    record_checkpoint("complex8_r9_p192_step3", MatrixBuffer(8, "complex", prec, rows), 3)
+
+
 if __name__ == "__main__":
     main()
+    main_ckpt()

@@ -155,3 +155,36 @@ def test_progressive_minors_d2h_matches_full_fetch():
             outs.append((res, fin))
     (rp, fp), (rq, fq) = outs
     assert results_digest(rp, fp, n, p, n) == results_digest(rq, fq, n, p, n)
+
+
+def test_device_resume_from_checkpoint(tmp_path):
+    """Checkpoint mid-run (native MPMAT writer), load it, resume on the device: the
+    final state and the minors equal an uninterrupted device run."""
+    from paper_1308_1536_b200.checkpoint import Checkpoint
+    from paper_1308_1536_b200.soa import SoA
+    n, p, stop = 260, 1024, 97
+    A = random_uniform_soa(n, p, seed=31)
+    with DeviceElimination(n, p, "real") as eng:
+        eng.load(A)
+        res = HostResults.alloc(n, 1, eng.L, True)
+        eng.run(True, True, 0, stop, res)
+        cur = A.copy()
+        eng.fetch(cur)
+        Checkpoint(tmp_path).write_soa(cur, n, p, "real", stop, [res.pivots.get(i, p) for i in range(stop)])
+    soa, _, _, _, trace = Checkpoint(tmp_path).load_soa()
+    with DeviceElimination(n, p, "real") as eng:
+        eng.load(soa)
+        eng.set_det(SoA.from_scalars([trace.det_series[-1]], p, "real"))
+        res_r = HostResults.alloc(n, 1, eng.L, True)
+        eng.run(True, True, stop, n, res_r)
+        fin_r = soa.copy()
+        eng.fetch(fin_r)
+    res_f, fin_f = _device_run(A, n, p, n, True)
+    assert np.array_equal(fin_r.limbs, fin_f.limbs) and np.array_equal(fin_r.cls, fin_f.cls)
+    assert np.array_equal(fin_r.exp, fin_f.exp)
+    for m in range(stop + 2, n + 1):  # minors emitted after the resume point: m valid entries in row m-1
+        sl = slice((m - 1) * n, (m - 1) * n + m)
+        for a, b in ((res_r.signed, res_f.signed), (res_r.normalized, res_f.normalized)):
+            assert np.array_equal(a.limbs[:, :, sl], b.limbs[:, :, sl]) and np.array_equal(a.exp[:, sl], b.exp[:, sl])
+            assert np.array_equal(a.cls[:, sl], b.cls[:, sl])
+    assert np.array_equal(res_r.dets.limbs[:, :, stop:], res_f.dets.limbs[:, :, stop:])

@@ -16,7 +16,7 @@ from paper_1308_1536_b200.elim import EliminationTrace, MinorSeries, minor_rows_
 from paper_1308_1536_b200.engine import HostResults
 from paper_1308_1536_b200.matrix import MatrixBuffer
 from paper_1308_1536_b200.output import write_dets, write_minors, write_results
-from paper_1308_1536_b200.scalars import Precision
+from paper_1308_1536_b200.scalars import Precision, canonical_bits
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "output")
 P256 = Precision(256)
@@ -81,3 +81,81 @@ def test_python_writer_matches_reference_files(name, tmp_path):
     write_dets(trace, os.path.join(tmp_path, "dets.txt"), dig)
     write_minors(minors, tmp_path, dig)
     _same_tree(os.path.join(GOLD, name), tmp_path)
+
+
+# ---------------------------------------------------------------- checkpoints
+from paper_1308_1536_b200.checkpoint import Checkpoint, load_mpmat  # noqa: E402
+from paper_1308_1536_b200.soa import SoA  # noqa: E402
+
+CKPT = {"uniform13_s5_p192_step4": (lambda: genmat.synth_matrix("random_uniform", 13, 5, Precision(192)), 4),
+        "complex8_r9_p192_step3": (_complex8, 3)}
+
+
+def _oracle_state(A, steps):
+    n, p = A.n, A.prec.bits
+    ref = oracle.OracleRank(n, p, A.kind)
+    ref.load(A.to_soa())
+    res = HostResults.alloc(n, 2 if A.kind == "complex" else 1, ref.L, True)
+    ref.run(True, True, 0, steps, res)
+    cur = A.to_soa()
+    ref.fetch(cur)
+    pivots = [res.pivots.get(i, p) for i in range(steps)]
+    return cur, pivots
+
+
+@pytest.mark.parametrize("name", sorted(CKPT))
+def test_checkpoint_write_matches_reference(name, tmp_path):
+    build, steps = CKPT[name]
+    A = build()
+    cur, pivots = _oracle_state(A, steps)
+    Checkpoint(tmp_path).write_soa(cur, A.n, A.prec.bits, A.kind, steps, pivots)
+    _same_tree(os.path.join(GOLD, "ckpt_" + name), tmp_path)
+
+
+@pytest.mark.parametrize("name", sorted(CKPT))
+def test_checkpoint_load_and_resume(name):
+    """Loading the reference's checkpoint gives its exact state; resuming from it
+    ends bit-identical to the uninterrupted run."""
+    build, steps = CKPT[name]
+    A = build()
+    n, p = A.n, A.prec.bits
+    cur, pivots = _oracle_state(A, steps)
+    soa, n2, bits, kind, trace = Checkpoint(os.path.join(GOLD, "ckpt_" + name)).load_soa()
+    assert (n2, bits, kind, trace.step) == (n, p, A.kind, steps)
+    assert [soa.canonical(i, p) for i in range(n * n)] == [cur.canonical(i, p) for i in range(n * n)]
+    assert [canonical_bits(a) for a in trace.pivots] == [canonical_bits(b) for b in pivots]
+    # resume: load the state, seed the det chain, run the remaining steps
+    nc = 2 if A.kind == "complex" else 1
+    ref = oracle.OracleRank(n, p, A.kind)
+    ref.load(soa)
+    ref.set_det(SoA.from_scalars([trace.det_series[-1]], p, A.kind))
+    res_r = HostResults.alloc(n, nc, ref.L, True)
+    ref.run(True, True, steps, n, res_r)
+    fin_r = soa.copy()
+    ref.fetch(fin_r)
+    full = oracle.OracleRank(n, p, A.kind)
+    full.load(A.to_soa())
+    res_f = HostResults.alloc(n, nc, full.L, True)
+    full.run(True, True, 0, n, res_f)
+    fin_f = A.to_soa()
+    full.fetch(fin_f)
+    assert [fin_r.canonical(i, p) for i in range(n * n)] == [fin_f.canonical(i, p) for i in range(n * n)]
+    for m in range(steps + 2, n + 1):  # minors emitted after the resume point
+        base = (m - 1) * n
+        assert [res_r.signed.canonical(base + k, p) for k in range(m)] == \
+            [res_f.signed.canonical(base + k, p) for k in range(m)]
+    for i in range(steps, n):
+        assert res_r.dets.canonical(i, p) == res_f.dets.canonical(i, p)
+
+
+def test_mpmat_roundtrip_random(tmp_path):
+    """save_mpmat -> load_mpmat is the identity on the bits (format_scalar's default digits)."""
+    from paper_1308_1536_b200.checkpoint import save_mpmat
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    for n, p in ((17, 333), (9, 4096)):
+        S = random_uniform_soa(n, p, seed=n + p)
+        path = os.path.join(tmp_path, f"m{n}.mpmat")
+        save_mpmat(S, n, p, "real", path)
+        T, n2, p2, kind = load_mpmat(path)
+        assert (n2, p2, kind) == (n, p, "real")
+        assert [T.canonical(i, p) for i in range(n * n)] == [S.canonical(i, p) for i in range(n * n)]
