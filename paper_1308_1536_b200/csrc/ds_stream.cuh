@@ -211,11 +211,11 @@ struct SWin {
     // to skip is slot -1 (first block, obase 1).
     const uint32_t adw = at(single ? w - obase : w);
     const bool skip0 = single && w < obase;
-    const int rse = single ? ors : 0;
+    const int rse = single ? ors : 32;  // clamped funnel: shift 32 gives S_w itself (two-pass lanes)
     uint32_t sp = sprev;
 #pragma unroll
     for (int k = 0; k < NL; k++) {
-      const uint32_t v = __funnelshift_r(single ? sp : X[k], X[k], rse);  // two-pass: funnel(x, x, 0) = x
+      const uint32_t v = __funnelshift_rc(sp, X[k], rse);
       if (k > 0 || !skip0) sts32(adw + (uint32_t)k * sb, v);
       sp = X[k];
     }
