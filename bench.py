@@ -252,7 +252,7 @@ def run_reference(args):
            "cpu_baseline": {"value": rate, "unit": "limb-MAC/s", "cores": base["cores"], "kind": "port",
                             "sample": base["sample"]},
            "e2e": {"value": rate, "unit": "limb-MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit_json(out)
 
 
 def main():
@@ -395,12 +395,30 @@ def main():
                "input_generation_s": gen_s,
                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
                "clocks": clk.summary(), "parallelism": f"row-cyclic x{world}"}
-        print(json.dumps(out), flush=True)
+        emit_json(out)
     eng.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit_json(obj):
+    """The one JSON line, on the process's original stdout."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+
+
 if __name__ == "__main__":
+    # libraries (NCCL's version banner, CUDA/torch notices) print to fd 1: route
+    # everything but the result line to stderr so stdout carries exactly one JSON line
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     main()
