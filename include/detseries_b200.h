@@ -158,6 +158,21 @@ int ds_snapshot(ds_ctx *ctx, int save);
  * (rows * cols * L^2, x4 for complex), then clears the counters. */
 int ds_profile(ds_ctx *ctx, int enable);
 int ds_profile_read(ds_ctx *ctx, double *update_ms, int64_t *launches, double *limb_macs);
+/* Multi-rank lookahead (one process per GPU): with ds_lookahead_enable(ctx,
+ * limit) the TC update of step i (i + 1 < limit) runs the column tile that
+ * holds column i+1 first, on the context's lookahead stream
+ * (ds_lookahead_stream).  The caller then, on that stream: lets the owner of
+ * row i+1 stage a_{i+1,i+1} into a (4L + 8)-byte exchange buffer
+ * (ds_lookahead_pivot), broadcasts the buffer from that owner, and launches
+ * step i+1's multipliers from it (ds_lookahead_mult); ds_step(i+1) then uses
+ * them.  Same results as without lookahead; parexec.py:290-333 exchange
+ * order is kept (every rank issues the same broadcasts in the same order).
+ * limit <= 0 disables. */
+int ds_lookahead_enable(ds_ctx *ctx, int limit);
+int ds_lookahead_stream(ds_ctx *ctx, void **stream);
+int ds_lookahead_pivot(ds_ctx *ctx, int i1, void *buf);
+int ds_lookahead_mult(ds_ctx *ctx, int i1, const void *buf);
+
 /* Internal engine counters (observability; no reference counterpart):
  * out[0] = elements the tensor-core update handed to the exact fallback
  * (short product undecided / normalisation uncertain), out[1] = 1 if the

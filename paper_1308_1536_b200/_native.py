@@ -25,7 +25,8 @@ DS_KIND_REAL, DS_KIND_COMPLEX = 0, 1
 EXPORTS = ("ds_version", "ds_create", "ds_destroy", "ds_load", "ds_fetch", "ds_run", "ds_pivot_buffer",
            "ds_pivot_stage", "ds_step", "ds_status", "ds_results_fetch", "ds_set_det", "ds_stream",
            "ds_launch_count", "ds_last_error", "ds_scalar_op", "ds_set_stream", "ds_use_pivot_buffer",
-           "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters")
+           "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters", "ds_lookahead_enable", "ds_lookahead_stream",
+           "ds_lookahead_pivot", "ds_lookahead_mult")
 
 
 class ds_results(ctypes.Structure):
@@ -69,6 +70,10 @@ def load_library(path: str = LIB_PATH):
         "ds_profile": (I, [VP, I]),
         "ds_profile_read": (I, [VP, P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_double)]),
         "ds_counters": (I, [VP, P(ctypes.c_int64), ctypes.c_int]),
+        "ds_lookahead_enable": (I, [VP, I]),
+        "ds_lookahead_stream": (I, [VP, P(VP)]),
+        "ds_lookahead_pivot": (I, [VP, I, VP]),
+        "ds_lookahead_mult": (I, [VP, I, VP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

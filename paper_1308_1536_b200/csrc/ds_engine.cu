@@ -57,7 +57,8 @@ struct ds_ctx {
   cudaStream_t la;
   cudaEvent_t ev_prep, ev_a, ev_mult, ev_la_done;
   int la_step;   // the step whose multipliers are already computed (-1: none)
-  int la_limit;  // lookahead only for steps i + 1 < la_limit (set by ds_run)
+  int la_limit;  // lookahead only for steps i + 1 < la_limit (set by ds_run / ds_lookahead_enable)
+  int la_ext;    // multi-rank: the caller exchanges the next pivot (ds_lookahead_pivot / _mult)
   // trace: pivots/dets [ncomp][L][n]; det running value [ncomp][L][1]
   uint32_t *piv_limbs, *det_limbs, *cur_limbs;
   int32_t *piv_exp, *det_exp, *cur_exp;
@@ -503,16 +504,17 @@ __device__ void wdiv_rn(Out o, const Val& a, const Val& b, int L, int p, uint32_
 // matrix (row i is not staged yet); a zero pivot leaves everything untouched
 // (the step's k_pivot_lite reports it)
 template <int K>
-__global__ void k_mult_w(KArgs k, int i, int jl0, int wwords, int divisor_from_matrix) {
+__global__ void k_mult_w(KArgs k, int i, int jl0, int wwords, int divisor_from_matrix, const uint8_t* pscal) {
   extern __shared__ uint32_t wsm[];
   if (k.status[0] >= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (r >= k.nloc - jl0) return;
   PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
-  Val b = divisor_from_matrix ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, (int64_t)i * k.n + i)
-                              : val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
-  if (divisor_from_matrix && is_zero_cls(b.c)) return;
+  Val b = pscal ? Val{CPtr{(const uint32_t*)pscal, 1}, *(const int32_t*)(pscal + 4 * k.L), pscal[4 * k.L + 4]}
+          : divisor_from_matrix ? val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, (int64_t)i * k.n + i)
+                                : val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  if ((pscal || divisor_from_matrix) && is_zero_cls(b.c)) return;
   int64_t jl = jl0 + r;
   int64_t idx = jl * k.n + i;
   Val a = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
@@ -528,6 +530,18 @@ __global__ void k_mult_w(KArgs k, int i, int jl0, int wwords, int divisor_from_m
     *ao.e = (int32_t)zv.e;
     uint8_t c = zv.c;
     *ao.c = (c == DS_CLS_POS) ? DS_CLS_NEG : (c == DS_CLS_NEG) ? DS_CLS_POS : (c == DS_CLS_PZERO) ? DS_CLS_NZERO : DS_CLS_PZERO;
+  }
+}
+
+// multi-rank lookahead: the owner copies a_{i1,i1} (its local row jl) into the
+// exchange buffer [L limbs | exp | cls] that is broadcast to every rank
+__global__ void k_pscal_stage(KArgs k, int i1, int64_t jl, uint8_t* dst) {
+  if (k.status[0] >= 0) return;
+  const int64_t idx = jl * k.n + i1;
+  for (int l = threadIdx.x; l < k.L; l += blockDim.x) ((uint32_t*)dst)[l] = k.a_limbs[(int64_t)l * k.a_count + idx];
+  if (threadIdx.x == 0) {
+    *(int32_t*)(dst + 4 * k.L) = k.a_exp[idx];
+    dst[4 * k.L + 4] = k.a_cls[idx];
   }
 }
 
@@ -1000,7 +1014,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     } else if (fast) {
       int blocks = (nrows + wpb - 1) / wpb;
       size_t smem = (size_t)wpb * wwords * 4;
-      WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0);
+      WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0, nullptr);
     } else {
       k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
     }
@@ -1014,8 +1028,8 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     }
     if (fast) {
       // lookahead for step i + 1 (one rank, inside the current ds_run range, rows left)
-      const int la_col = (ctx->tc.enabled && ctx->world == 1 && i + 1 < ctx->la_limit && i + 2 < n &&
-                          !getenv("DS_NO_LOOKAHEAD"))
+      const int la_col = (ctx->tc.enabled && (ctx->world == 1 || ctx->la_ext) && i + 1 < ctx->la_limit &&
+                          i + 2 < n && !getenv("DS_NO_LOOKAHEAD"))
                              ? i + 1
                              : -1;
       int la_used = 0;
@@ -1027,7 +1041,15 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
                                    ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
                                    ctx->status, &ctx->launches);
       if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
-      if (la_used) {
+      if (ctx->la_ext) {
+        // caller-driven lookahead: it stages / broadcasts a_{i+1,i+1} and launches
+        // the multipliers (ds_lookahead_pivot, ds_lookahead_mult) on the lookahead
+        // stream; without the tile split that stream must see the whole update
+        if (!la_used) {
+          CK(cudaEventRecord(ctx->ev_a, s));
+          CK(cudaStreamWaitEvent(ctx->la, ctx->ev_a, 0));
+        }
+      } else if (la_used) {
         // column i+1 is final: step i+1's multipliers on the lookahead stream (after
         // the tile holding that column) while the other tiles of step i still run
         KArgs kn = k;
@@ -1038,7 +1060,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         const int rows1 = ctx->nloc - jl1;
         int blocks = (rows1 + wpb - 1) / wpb;
         size_t smem = (size_t)wpb * wwords * 4;
-        WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, ctx->la, kn, i + 1, jl1, wwords, 1);
+        WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, ctx->la, kn, i + 1, jl1, wwords, 1, nullptr);
         ctx->launches++;
         CK(cudaEventRecord(ctx->ev_mult, ctx->la));
         ctx->la_step = i + 1;
@@ -1135,6 +1157,56 @@ int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
   ctx->prof_used = 0;
   ctx->prof_launches = 0;
   ctx->prof_work = 0;
+  return DS_OK;
+}
+
+int ds_lookahead_enable(ds_ctx* ctx, int limit) {
+  ctx->la_limit = limit;
+  ctx->la_ext = limit > 0 ? 1 : 0;
+  if (limit <= 0) ctx->la_step = -1;
+  return DS_OK;
+}
+
+int ds_lookahead_stream(ds_ctx* ctx, void** stream) {
+  *stream = (void*)ctx->la;
+  return DS_OK;
+}
+
+int ds_lookahead_pivot(ds_ctx* ctx, int i1, void* buf) {
+  if (i1 < 0 || i1 >= ctx->n || i1 % ctx->world != ctx->rank || !fast_real(ctx)) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  KArgs k = kargs(ctx);
+  k_pscal_stage<<<1, 128, 0, ctx->la>>>(k, i1, (int64_t)(i1 / ctx->world), (uint8_t*)buf);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return DS_OK;
+}
+
+int ds_lookahead_mult(ds_ctx* ctx, int i1, const void* buf) {
+  if (i1 < 0 || i1 >= ctx->n || !fast_real(ctx)) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  KArgs k = kargs(ctx);
+  k.z_limbs = ctx->zb_limbs[i1 & 1];
+  k.z_exp = ctx->zb_exp[i1 & 1];
+  k.z_cls = ctx->zb_cls[i1 & 1];
+  const int L = ctx->L;
+  const int K = warp_k(L);
+  const int wwords = wdiv_words(L, ctx->p, K);
+  const int wpb = 4;
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  set_wdiv_attrs(maxsm);
+  const int jl1 = first_local_after(i1, ctx->rank, ctx->world);
+  const int rows1 = ctx->nloc - jl1;
+  if (rows1 > 0) {
+    int blocks = (rows1 + wpb - 1) / wpb;
+    size_t smem = (size_t)wpb * wwords * 4;
+    WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, ctx->la, k, i1, jl1, wwords, 0, (const uint8_t*)buf);
+    ctx->launches++;
+  }
+  CK(cudaEventRecord(ctx->ev_mult, ctx->la));
+  ctx->la_step = i1;
+  CK(cudaGetLastError());
   return DS_OK;
 }
 
@@ -1299,6 +1371,7 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
                     res->signed_minors.count == (int64_t)ctx->n * ctx->n && !getenv("DS_NO_PROGRESSIVE_D2H");
   const int BATCH = 64;
   int copied = 0;
+  ctx->la_ext = 0;  // single-rank run: the engine chains the lookahead itself
   ctx->la_limit = stop_step;
   for (int i = start_step; i < stop_step; i++) {
     if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) { ctx->la_limit = -1; return rc; }

@@ -171,6 +171,23 @@ class DeviceElimination:
         return {"tc_fallback_elements": int(out[0]), "tc_engine": bool(out[1]), "dfma_engine": bool(out[2]),
                 "direct_mispredictions": int(out[3])}
 
+    # -- multi-rank lookahead (ds_lookahead_*) ------------------------------
+    def lookahead_enable(self, limit: int):
+        _check(self.lib.ds_lookahead_enable(self.ctx, int(limit)), self.ctx, "ds_lookahead_enable", self.rank)
+
+    def lookahead_stream(self) -> int:
+        p = ctypes.c_void_p()
+        _check(self.lib.ds_lookahead_stream(self.ctx, ctypes.byref(p)), self.ctx, "ds_lookahead_stream", self.rank)
+        return p.value or 0
+
+    def lookahead_pivot(self, i1: int, buf_ptr: int):
+        _check(self.lib.ds_lookahead_pivot(self.ctx, int(i1), ctypes.c_void_p(buf_ptr)), self.ctx,
+               "ds_lookahead_pivot", self.rank)
+
+    def lookahead_mult(self, i1: int, buf_ptr: int):
+        _check(self.lib.ds_lookahead_mult(self.ctx, int(i1), ctypes.c_void_p(buf_ptr)), self.ctx,
+               "ds_lookahead_mult", self.rank)
+
     def stream(self) -> int:
         return self.lib.ds_stream(self.ctx) or 0
 

@@ -25,6 +25,8 @@ serialize -- HBM already holds the binary limb layout.
 
 from __future__ import annotations
 
+import os
+
 import struct
 import zlib
 from dataclasses import dataclass, field
@@ -242,6 +244,7 @@ def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcas
     """
     world, rank = engine.world, engine.rank
     nbytes = pivot.numel() * pivot.element_size()
+    la = _lookahead_setup(engine, n, pivot)
     for i in range(n):
         owner = i % world
         if rank == owner:
@@ -253,7 +256,39 @@ def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcas
             stats.bytes_total += nbytes
             stats.per_step_bytes.append(nbytes)
             stats.fanout_deliveries += world
+        if la is not None and i + 2 < n:
+            # lookahead: the tile holding column i+1 is already updated on the
+            # lookahead stream; the owner of row i+1 shares the next pivot there and
+            # every rank computes step i+1's multipliers while step i's update runs
+            ext, scal = la
+            o1 = (i + 1) % world
+            with _torch().cuda.stream(ext):
+                if rank == o1:
+                    engine.lookahead_pivot(i + 1, scal.data_ptr())
+                broadcast(scal, o1)
+            engine.lookahead_mult(i + 1, scal.data_ptr())
+    if la is not None:
+        engine.lookahead_enable(0)
     return engine.status()
+
+
+def _lookahead_setup(engine, n: int, pivot):
+    """(lookahead stream context, exchange buffer) for a multi-rank GPU run, or None
+    (CPU engines, one rank, DS_NO_DIST_LOOKAHEAD)."""
+    if not hasattr(engine, "lookahead_enable") or os.environ.get("DS_NO_DIST_LOOKAHEAD"):
+        return None
+    if not getattr(pivot, "is_cuda", False) or not engine.counters().get("tc_engine"):
+        return None  # only the tensor-core engine splits its update for the lookahead
+    torch = _torch()
+    engine.lookahead_enable(n)
+    ext = torch.cuda.ExternalStream(engine.lookahead_stream(), device=pivot.device)
+    scal = torch.zeros(4 * engine.L + 8, dtype=torch.uint8, device=pivot.device)
+    return ext, scal
+
+
+def _torch():
+    import torch
+    return torch
 
 
 def allreduce_gather(res: HostResults, soa: SoA | None, rank: int, world: int, allreduce):

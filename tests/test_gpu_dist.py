@@ -74,3 +74,65 @@ def test_bench_under_torchrun_small():
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     d = json.loads(line)
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+
+
+SCRIPT_LA = r'''
+import os, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, os.path.join({root!r}, "tests"))
+import numpy as np, torch, torch.distributed as dist
+dist.init_process_group("nccl")
+local = int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+from paper_1308_1536_b200.parexec import dist_run
+from paper_1308_1536_b200.synth import random_uniform_soa
+n, p = {n}, {p}
+A = random_uniform_soa(n, p, seed=41)
+eng = DeviceElimination(n, p, "real", local, dist.get_rank(), dist.get_world_size())
+eng.load(A)
+_, pbytes = eng.pivot_buffer()
+pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{{local}}")
+eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
+eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream)
+failed = dist_run(eng, n, True, True, pivot, lambda t, src: dist.broadcast(t, src=src))
+res = HostResults.alloc(n, 1, eng.L, True)
+eng.results(n, res)
+fin = A.copy()
+eng.fetch(fin)
+np.savez({out!r}, limbs=fin.limbs, exp=fin.exp, cls=fin.cls, dl=res.dets.limbs, de=res.dets.exp,
+         sl=res.signed.limbs, se=res.signed.exp, sc=res.signed.cls, flags=res.row_flags)
+eng.close()
+dist.destroy_process_group()
+'''
+
+
+def test_torchrun_lookahead_matches_single_process(tmp_path):
+    """The caller-driven lookahead (dist_run: tile split, next-pivot exchange on the
+    lookahead stream, multipliers there) gives the single-process engine's results."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    n, p = 300, 1024
+    script = tmp_path / "la.py"
+    out = tmp_path / "la.npz"
+    script.write_text(SCRIPT_LA.format(root=ROOT, n=n, p=p, out=str(out)))
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                    "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(script)],
+                   check=True, timeout=600, cwd=ROOT)
+    z = np.load(out)
+    A = random_uniform_soa(n, p, seed=41)
+    with DeviceElimination(n, p, "real") as eng:
+        eng.load(A)
+        res = HostResults.alloc(n, 1, eng.L, True)
+        eng.run(True, True, 0, n, res)
+        fin = A.copy()
+        eng.fetch(fin)
+    assert np.array_equal(z["limbs"], fin.limbs) and np.array_equal(z["exp"], fin.exp)
+    assert np.array_equal(z["cls"], fin.cls)
+    assert np.array_equal(z["dl"], res.dets.limbs) and np.array_equal(z["de"], res.dets.exp)
+    assert np.array_equal(z["flags"], res.row_flags)
+    for m in range(2, n + 1):
+        sl = slice((m - 1) * n, (m - 1) * n + m)
+        assert np.array_equal(z["sl"][:, :, sl], res.signed.limbs[:, :, sl])
+        assert np.array_equal(z["se"][:, sl], res.signed.exp[:, sl])
