@@ -562,6 +562,278 @@ __global__ void k_tc_fallback(TcArgs a, const uint32_t* z_limbs, int64_t z_count
   }
 }
 
+// ================================================================ wide precision
+// Above ~8192 bits the pivot-row digits no longer fit in TMEM and the per-column
+// windows of a no longer fit in shared memory, so the update splits in two:
+//   k_prod_tcw   the short products P_jk = z_j * b_k (digit columns c >= c_lo)
+//                on the tensor cores, A = pivot-row digits streamed by TMA per
+//                K chunk, B = the row's Toeplitz bank built per chunk; the
+//                epilogue carries the digit sums into 32-bit limbs and stores
+//                limbs q >= c_lo / 4 of every product (plane-major, coalesced)
+//   k_tcw_finish one thread per element: decides RN(P) at p bits from the
+//                stored limbs (undecidable -> the exact fallback list), then
+//                a <- RN(a - RN(P)) with the general engine's add_rn
+// Work per element: O(L^2) digit MACs on the tensor pipe vs O(L) in the finish.
+constexpr int TW_EPI = 128;                 // epilogue threads (TMEM lanes = columns)
+constexpr int TW_PROD = 128;                // bank / TMA producer threads
+constexpr int TW_THREADS = TW_EPI + TW_PROD + 32;  // + one MMA issuer warp
+constexpr int TW_ZLO = -128;                // zw[x] = Z[TW_ZLO + x]
+
+struct TwArgs {
+  int p, L, D8p, nks, c_lo, qlo, W, eps;
+  int tn, ntiles, kc, nst, brc;  // MMA N, tiles, K steps per stage, stages, bank rows per stage
+  int nrows, rbr, kstart, ncp, zwb;
+  const uint8_t* zbytes;  // the chunk's rows [nrows][D8p]
+  uint32_t* tprod;        // [W][nrows][ncp]
+  int64_t pstride;        // nrows * ncp
+  int32_t* status;
+  int step;
+};
+
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(TW_THREADS, 1) k_prod_tcw(TwArgs a, const __grid_constant__ CUtensorMap bmap) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_full[8];
+  __shared__ __align__(8) uint64_t bar_empty[8];
+  __shared__ __align__(8) uint64_t bar_tfull[2];
+  __shared__ __align__(8) uint64_t bar_tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int TN = a.tn, KC = a.kc, NST = a.nst, BRC = a.brc, D8p = a.D8p;
+  const uint32_t ABYTES = (uint32_t)KC * 4096u;               // A chunk: KC steps x (2 halves x 128 rows x 16 B)
+  const uint32_t SBYTES = ABYTES + (uint32_t)BRC * 32u;       // + bank: 2 halves x BRC rows x 16 B
+  uint8_t* zw = smem + (size_t)NST * SBYTES;
+  const int kbase = a.kstart + (int)blockIdx.x * TM;
+  const int row0 = (int)blockIdx.y * a.rbr;
+  const int nrow_cta = min(a.rbr, a.nrows - row0);
+  if (tid == 0) {
+    for (int s = 0; s < NST; s++) {
+      mbar_init(&bar_full[s], TW_PROD);
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&bar_tfull[b], 1);
+      mbar_init(&bar_tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (tid >= TW_EPI && tid < TW_EPI + TW_PROD) {
+    // =================================================== producers
+    const int ptid = tid - TW_EPI;
+    int sc = 0;  // stage counter
+    for (int ri = 0; ri < nrow_cta; ri++) {
+      bar_pipe(1, TW_PROD);  // every producer is done with the previous row's zw
+      const uint8_t* zrow = a.zbytes + (int64_t)(row0 + ri) * D8p;
+      for (int v = ptid; v < a.zwb / 4; v += TW_PROD) {
+        const int t = TW_ZLO + 4 * v;
+        ((uint32_t*)zw)[v] = (t >= 0 && t < D8p) ? *(const uint32_t*)(zrow + t) : 0u;
+      }
+      bar_pipe(1, TW_PROD);
+      for (int t = 0; t < a.ntiles; t++) {
+        const int c0 = a.c_lo + t * TN;
+        const int s_lo = max(0, c0 - (D8p - 1)), s_hi = min(D8p - 1, c0 + TN - 1);
+        const int ks0 = s_lo / KS, ks1 = s_hi / KS;
+        for (int ka = ks0; ka <= ks1; ka += KC, sc++) {
+          const int kb = min(ks1, ka + KC - 1);
+          const int st = sc % NST;
+          if (sc >= NST) mbar_wait(&bar_empty[st], ((sc / NST) - 1) & 1);
+          uint8_t* A = smem + (size_t)st * SBYTES;
+          uint8_t* bank = A + ABYTES;
+          if (ptid == 0) {
+            mbar_expect(&bar_full[st], (uint32_t)(kb - ka + 1) * 4096u);
+            for (int ks = ka; ks <= kb; ks++)
+              for (int h = 0; h < 2; h++)
+                tma_load_2d(A + (ks - ka) * 4096 + h * 2048, &bmap, KS * ks + 16 * h, kbase, &bar_full[st]);
+          }
+          // bank row r <-> m = c0 - 32 kb + r: half h holds Z[m - 16h - j], j = 0..15
+          const int bru = TN + KS * (kb - ka);
+          const int mb = c0 - KS * kb;
+          for (int c = ptid; c < 2 * bru; c += TW_PROD) {
+            const int h = c >= bru ? 1 : 0, r = c - h * bru;
+            const int off = mb + r - 16 * h - 15 - TW_ZLO;
+            const uint32_t* wp = (const uint32_t*)zw + (off >> 2);
+            const int sh = 8 * (off & 3);
+            uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+            uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
+            uint32_t x2 = __funnelshift_r(w2, w3, sh), x3 = __funnelshift_r(w3, w4, sh);
+            *(uint4*)(bank + h * BRC * 16 + (r >> 3) * 128 + (r & 7) * 16) =
+                make_uint4(__byte_perm(x3, 0, 0x0123), __byte_perm(x2, 0, 0x0123), __byte_perm(x1, 0, 0x0123),
+                           __byte_perm(x0, 0, 0x0123));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&bar_full[st]);
+        }
+      }
+    }
+  } else if (tid >= TW_EPI + TW_PROD) {
+    // =================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8(TM, TN);
+      int sc = 0, gt = 0;
+      for (int ri = 0; ri < nrow_cta; ri++) {
+        for (int t = 0; t < a.ntiles; t++, gt++) {
+          const int buf = gt & 1;
+          if (gt >= 2) mbar_wait(&bar_tempty[buf], ((gt >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t dcol = tmem + (uint32_t)(buf * TN);
+          const int c0 = a.c_lo + t * TN;
+          const int s_lo = max(0, c0 - (D8p - 1)), s_hi = min(D8p - 1, c0 + TN - 1);
+          const int ks0 = s_lo / KS, ks1 = s_hi / KS;
+          for (int ka = ks0; ka <= ks1; ka += KC, sc++) {
+            const int kb = min(ks1, ka + KC - 1);
+            const int st = sc % NST;
+            mbar_wait(&bar_full[st], (sc / NST) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t A = smem_u32(smem + (size_t)st * SBYTES);
+            const uint32_t B = A + ABYTES;
+            for (int ks = ka; ks <= kb; ks++) {
+              const uint64_t ad = umma_desc(A + (uint32_t)(ks - ka) * 4096u, 2048u, 128u);
+              const uint64_t bd = umma_desc(B + (uint32_t)(kb - ks) * 512u, (uint32_t)BRC * 16u, 128u);
+              const uint32_t acc = ks > ks0 ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dcol),
+                  "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+            }
+            umma_commit(&bar_empty[st]);
+          }
+          umma_commit(&bar_tfull[buf]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // =================================================== epilogue: digit sums -> limbs
+    const int r = tid;  // column within the tile = TMEM lane
+    const int col = (int)blockIdx.x * TM + r;
+    int gt = 0;
+    for (int ri = 0; ri < nrow_cta; ri++) {
+      uint32_t* out = a.tprod + (int64_t)(row0 + ri) * a.ncp + col;
+      uint32_t carry = 0;
+      for (int t = 0; t < a.ntiles; t++, gt++) {
+        const int buf = gt & 1;
+        mbar_wait(&bar_tfull[buf], (gt >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * TN);
+        const int c0 = a.c_lo + t * TN;
+        const int cend = min(TN, 2 * D8p - c0);
+#pragma unroll 1
+        for (int cb = 0; cb < cend; cb += 32) {
+          uint32_t v[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr + cb));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          const int q0 = (c0 + cb) >> 2;
+#pragma unroll
+          for (int g = 0; g < 8; g++) {
+            // digit sums < 2^31: limb = sum_j v[4g+j] 2^(8j) + carry < 2^56
+            uint64_t w = (uint64_t)v[4 * g + 3] * 16777216u;
+            w += (uint64_t)v[4 * g + 2] * 65536u;
+            w += (uint64_t)v[4 * g + 1] * 256u;
+            w += (uint64_t)v[4 * g] + carry;
+            const int q = q0 + g;
+            if (q < 2 * a.L) out[(int64_t)(q - a.qlo) * a.pstride] = (uint32_t)w;
+            carry = (uint32_t)(w >> 32);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_tempty[buf]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// bits [lo, hi) of S all ones / all zeros (hi > lo)
+__device__ __forceinline__ void bit_range(ds::CPtr S, int n, int64_t lo, int64_t hi, bool* ones, bool* zeros) {
+  bool o = true, z = true;
+  for (int64_t pos = lo; pos < hi; pos += 32) {
+    const int nb = (int)min((int64_t)32, hi - pos);
+    const uint32_t mask = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    const uint32_t v = ds::bits32(S, n, pos) & mask;
+    if (v != mask) o = false;
+    if (v != 0) z = false;
+  }
+  *ones = o;
+  *zeros = z;
+}
+
+// a_jk <- RN(a_jk - RN(P_jk)) for the chunk's elements; scratch [word][thread]:
+// T (L words) then add_rn's 2L + 4
+__global__ void k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch, int64_t sthreads) {
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  const int L = a.L;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)w.nrows * a.ncols;
+  ds::Ptr T{scratch + tid, sthreads};
+  ds::Ptr tmp = T.off(L);
+  for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
+    const int k = a.kstart + cidx;
+    if (k < a.kmin || k == a.skip_col || k >= a.n) continue;
+    const int zr = row_first + ri;  // relative to jl0
+    const int jl = a.jl0 + zr;
+    const int64_t idx = (int64_t)jl * a.n + k;
+    const uint8_t cz = a.zcls[zr], cb = a.bcls[k], ca = a.a_cls[idx];
+    const int st = (cz & 1) ^ (cb & 1);
+    if (cz >= DS_CLS_PZERO || cb >= DS_CLS_PZERO) {  // a - (+-0)
+      if (ca >= DS_CLS_PZERO) a.a_cls[idx] = ((ca & 1) && !st) ? DS_CLS_NZERO : DS_CLS_PZERO;
+      continue;
+    }
+    const ds::CPtr S{w.tprod + (int64_t)ri * w.ncp + cidx, w.pstride};
+    const int64_t hb = ds::top_bit(S, w.W);
+    const int64_t lsb = hb - a.p + 1;
+    bool amb = lsb - 1 <= w.eps;
+    if (!amb) {
+      bool ones, zeros, lz, lo_ones;
+      bit_range(S, w.W, w.eps, lsb - 1, &ones, &zeros);
+      const bool g = (ds::bits32(S, w.W, lsb - 1) & 1u) != 0;
+      bit_range(S, w.W, 0, w.eps, &lo_ones, &lz);
+      amb = ones || (g && zeros && lz);
+    }
+    if (amb) {
+      int slot = atomicAdd(a.fb_count, 1);
+      if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
+      else atomicAdd(&a.status[5], 1);
+      continue;
+    }
+    const int64_t base = (int64_t)a.zexp[zr] + a.bexp[k] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
+    ds::RoundOut ro = ds::round_big(T, L, a.p, S, w.W, base, false);
+    ds::Val t{ds::CPtr{T.p, T.s}, ro.e, (uint8_t)(st ? DS_CLS_NEG : DS_CLS_POS)};
+    ds::Val av{ds::CPtr{a.a_limbs + idx, a.a_count}, a.a_exp[idx], ca};
+    int32_t re;
+    uint8_t rc;
+    if (!ds::add_rn(ds::Ptr{a.a_limbs + idx, a.a_count}, &re, &rc, av, t, true, L, a.p, tmp))
+      atomicAdd(&a.status[2], 1);
+    a.a_exp[idx] = re;
+    a.a_cls[idx] = rc;
+  }
+}
+
 size_t tc_smem(int L, int br, int ng) {
   const size_t zwl = ((br + 64) + 15) & ~15;
   return ng * ((size_t)br * KS + 4 * (size_t)(L + 2) * TM + zwl);
@@ -611,10 +883,89 @@ struct TcWork {
   int64_t sthreads;
   int fb_cap;
   CUtensorMap amap;        // a planes: dims {a_count, L}, box {128, L}
+  CUtensorMap bmap;        // wide: pivot-row digits, dims {D8p, n}, box {16, 128}
+  uint32_t* tprod;         // wide: product limbs [W][rows][ncp]
+  uint32_t* tscratch;      // wide: finish-kernel scratch [3L + 8][tthreads]
+  int64_t tthreads;
   const void* amap_base;
   int64_t amap_count;
   int amap_ok;
 };
+
+static EncodeTiledFn encode_tiled();
+
+// wide-precision plan: product kernel tiles, stages and the row chunk bounded by
+// the product-limb buffer
+static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int maxsm) {
+  (void)device;
+  const int L = plan->L, D8p = plan->D8p, zb = 32 * L - p;
+  // short product: E < 2^eps units of limb q_lo; >= 32 decision bits between
+  // 2^eps and the round bit (at >= 64 L - p - 2 in P)
+  int clo = ((32 * L + zb - 34 - plan->eps) / 8) & ~3;
+  if (clo < 0) clo = 0;
+  int tn = 256;
+  if (2 * D8p - clo < tn) tn = (2 * D8p - clo + 31) & ~31;
+  if (clo + tn <= D8p || clo - D8p + 1 - 31 - TW_ZLO < 0) return DS_OK;  // zw window assumptions
+  int kc = 8, nst = 3;
+  const int zwb = (D8p + tn + 256 + 15) & ~15;
+  size_t sm = 0;
+  for (;;) {
+    sm = (size_t)nst * ((size_t)kc * 4096 + (size_t)(tn + KS * (kc - 1)) * 32) + zwb + 1024;
+    if ((int)sm <= maxsm - 2048) break;
+    if (nst > 2) nst--;
+    else if (kc > 2) kc /= 2;
+    else return DS_OK;
+  }
+  plan->wide = 1;
+  plan->c_lo = clo;
+  plan->tn = tn;
+  plan->ntiles = (2 * D8p - clo + tn - 1) / tn;
+  plan->w_kc = kc;
+  plan->w_nst = nst;
+  plan->w_brc = tn + KS * (kc - 1);
+  plan->w_qlo = clo / 4;
+  plan->w_W = 2 * L - clo / 4;
+  plan->w_zwb = zwb;
+  plan->w_rbr = 2;
+  plan->smem = sm;
+  if (cudaFuncSetAttribute(k_prod_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    return DS_CUDA;
+  const int64_t ncp = (int64_t)((n + TM - 1) / TM) * TM;
+  size_t budget = (size_t)2 << 30;
+  if (const char* e = getenv("DS_TCW_BUDGET_MB")) budget = (size_t)atol(e) << 20;
+  int64_t rows = (int64_t)(budget / ((size_t)ncp * plan->w_W * 4));
+  if (rows < 1) rows = 1;
+  if (rows > nloc) rows = nloc > 0 ? nloc : 1;
+  plan->w_rows = (int)rows;
+  TcWork* w = new TcWork();
+  memset(w, 0, sizeof(*w));
+  plan->work = w;
+  w->fb_cap = 1 << 16;
+  w->sthreads = 64 * 128;
+  w->tthreads = 148 * 4 * 128;
+  bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
+            cudaMalloc(&w->bbytes, (size_t)D8p * n) == cudaSuccess &&
+            cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
+            cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
+            cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
+            cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
+            cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W) == cudaSuccess &&
+            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * (3 * (size_t)L + 8)) == cudaSuccess;
+  if (!ok) return DS_OOM;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return DS_OK;  // no tensor maps: not applicable
+  cuuint64_t dims[2] = {(cuuint64_t)D8p, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)D8p};
+  cuuint32_t box[2] = {16, (cuuint32_t)TM};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(&w->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)w->bbytes, dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return DS_OK;
+  plan->enabled = 1;
+  return DS_OK;
+}
 
 int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   memset(plan, 0, sizeof(*plan));
@@ -664,7 +1015,7 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
     plan->br = br;
     smem = sm;
   }
-  if (!ng) return DS_OK;  // not applicable: other engines
+  if (!ng || getenv("DS_TC_WIDE")) return tcw_plan_init(plan, n, nloc, p, device, maxsm);
   plan->ng = ng;
   cudaError_t ea = ng == 2 ? cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                            : cudaFuncSetAttribute(k_update_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -690,7 +1041,7 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
 void tc_plan_free(TcPlan* plan) {
   TcWork* w = (TcWork*)plan->work;
   if (!w) return;
-  void* ptrs[] = {w->zbytes, w->bbytes, w->zf, w->bf, w->fb_count, w->fb_list, w->scratch};
+  void* ptrs[] = {w->zbytes, w->bbytes, w->zf, w->bf, w->fb_count, w->fb_list, w->scratch, w->tprod, w->tscratch};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete w;
@@ -729,6 +1080,32 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   a.fb_count = w->fb_count; a.fb_list = w->fb_list; a.fb_cap = w->fb_cap;
   a.tn = plan->tn;
   a.br = plan->br;
+  if (plan->wide) {
+    // wide precision: product limbs per row chunk, then the finish kernel
+    a.tile0 = 0;
+    a.tskip = -1;
+    const int ntile = (ncols + TM - 1) / TM;
+    const int ncp = ntile * TM;
+    for (int r0 = 0; r0 < nrows; r0 += plan->w_rows) {
+      const int rc = nrows - r0 < plan->w_rows ? nrows - r0 : plan->w_rows;
+      TwArgs tw;
+      tw.p = plan->p; tw.L = L; tw.D8p = plan->D8p; tw.nks = plan->nks; tw.c_lo = plan->c_lo;
+      tw.qlo = plan->w_qlo; tw.W = plan->w_W; tw.eps = plan->eps;
+      tw.tn = plan->tn; tw.ntiles = plan->ntiles; tw.kc = plan->w_kc; tw.nst = plan->w_nst; tw.brc = plan->w_brc;
+      tw.nrows = rc; tw.rbr = plan->w_rbr; tw.kstart = kstart; tw.ncp = ncp; tw.zwb = plan->w_zwb;
+      tw.zbytes = w->zbytes + (size_t)r0 * plan->D8p;
+      tw.tprod = w->tprod;
+      tw.pstride = (int64_t)rc * ncp;
+      tw.status = status; tw.step = i;
+      k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tw, w->bmap);
+      k_tcw_finish<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch, w->tthreads);
+      *launches += 2;
+    }
+    k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
+    *launches += 3;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DS_OK : DS_CUDA;
+  }
   if (w->amap_base != (const void*)a_limbs || w->amap_count != a_count) {
     w->amap_base = a_limbs;
     w->amap_count = a_count;

@@ -10,6 +10,9 @@ struct TcPlan {
   int tn, br;          // MMA N per tile, Toeplitz bank rows
   int ng;              // epilogue groups / producer pipelines per CTA (1 or 2)
   size_t smem;
+  // wide precision (pivot-row digits beyond TMEM): product kernel + finish kernel
+  int wide;
+  int w_kc, w_nst, w_brc, w_qlo, w_W, w_zwb, w_rows, w_rbr;
   void* work;
 };
 

@@ -1,0 +1,88 @@
+"""Wide-precision tensor-core update (ds_tc.cu k_prod_tcw + k_tcw_finish):
+the short products on the tensor cores with the pivot-row digits streamed per
+K chunk, stored as limbs, then rounded and subtracted per element.  It is the
+engine above 8192 bits; DS_TC_WIDE=1 forces it at any precision so it can be
+checked against the oracle and the other engines at sizes the oracle finishes
+quickly."""
+import numpy as np
+import pytest
+
+import oracle
+from _util import first_mismatch, results_digest
+from test_gpu_tc import _device_run
+from test_gpu_update_adversarial import crafted
+from paper_1308_1536_b200.engine import HostResults
+from paper_1308_1536_b200.synth import random_uniform_soa
+
+pytestmark = pytest.mark.gpu
+WIDE = {"DS_TC_WIDE": "1"}
+
+
+def _oracle(A, n, p, steps, minors=True):
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res = HostResults.alloc(n, 1, ref.L, minors)
+    ref.run(minors, True, 0, steps, res)
+    fin = A.copy()
+    ref.fetch(fin)
+    return res, fin
+
+
+@pytest.mark.parametrize("n,p,steps", [(150, 1024, 4), (133, 257, 3), (140, 2000, 3), (131, 4095, 2),
+                                          (261, 512, 3)])
+def test_wide_forced_matches_oracle(n, p, steps):
+    A = random_uniform_soa(n, p, seed=11 * n + p)
+    res_o, fin_o = _oracle(A, n, p, steps)
+    res_d, fin_d = _device_run(A, n, p, steps, True, env=WIDE)
+    mism = first_mismatch(fin_o, fin_d, p)
+    assert not mism, mism
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+@pytest.mark.parametrize("p", [256, 300, 1024, 2047, 4096])
+@pytest.mark.parametrize("steps", [1, 3])
+def test_wide_forced_adversarial(p, steps):
+    """Exact cancellation, +-1 ulp, exponent gaps, exact (integer / power-of-two)
+    products -- the tie / all-ones cases of the short-product decision."""
+    n = 40
+    A = crafted(n, p, p + 17 * steps)
+    res_o, fin_o = _oracle(A, n, p, steps)
+    res_d, fin_d = _device_run(A, n, p, steps, True, env=WIDE)
+    mism = first_mismatch(fin_o, fin_d, p)
+    assert not mism, mism
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+@pytest.mark.parametrize("minors", [True, False])
+def test_wide_forced_matches_tc(minors):
+    """Several row chunks (small product buffer), many column tiles, vs the regular TC engine."""
+    n, p, steps = 600, 4096, 12
+    A = random_uniform_soa(n, p, seed=5 + n)
+    res_t, fin_t = _device_run(A, n, p, steps, minors)
+    res_w, fin_w = _device_run(A, n, p, steps, minors, env=dict(WIDE, DS_TCW_BUDGET_MB="64"))
+    assert np.array_equal(fin_t.cls, fin_w.cls)
+    assert np.array_equal(fin_t.exp, fin_w.exp)
+    assert np.array_equal(fin_t.limbs, fin_w.limbs)
+    assert results_digest(res_t, fin_t, n, p, steps) == results_digest(res_w, fin_w, n, p, steps)
+
+
+@pytest.mark.parametrize("n,p,steps", [(136, 16384, 2), (40, 16000, 2)])
+def test_wide_native_16k_matches_oracle(n, p, steps):
+    """16384 bits: the wide engine is the default (A no longer fits in TMEM)."""
+    A = random_uniform_soa(n, p, seed=n + 3 * p)
+    res_o, fin_o = _oracle(A, n, p, steps)
+    res_d, fin_d = _device_run(A, n, p, steps, True)
+    mism = first_mismatch(fin_o, fin_d, p)
+    assert not mism, mism
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+
+
+def test_wide_16k_matches_dfma():
+    n, p, steps = 300, 16384, 6
+    A = random_uniform_soa(n, p, seed=1234)
+    res_w, fin_w = _device_run(A, n, p, steps, True)
+    res_f, fin_f = _device_run(A, n, p, steps, True, env={"DS_DISABLE_TC": "1"})
+    assert np.array_equal(fin_f.limbs, fin_w.limbs)
+    assert np.array_equal(fin_f.exp, fin_w.exp)
+    assert np.array_equal(fin_f.cls, fin_w.cls)
+    assert results_digest(res_f, fin_f, n, p, steps) == results_digest(res_w, fin_w, n, p, steps)
