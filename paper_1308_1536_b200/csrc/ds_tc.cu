@@ -782,15 +782,73 @@ __device__ __forceinline__ void bit_range(ds::CPtr S, int n, int64_t lo, int64_t
   *zeros = z;
 }
 
-// a_jk <- RN(a_jk - RN(P_jk)) for the chunk's elements; scratch [word][thread]:
-// T (L words) then add_rn's 2L + 4
-__global__ void k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch, int64_t sthreads) {
+// bits32(src, n, 32 k + off) for k = 0, 1, 2, ... with one load per limb
+struct BitStream {
+  ds::CPtr s;
+  int n, sh;
+  int64_t lw;
+  uint32_t lo;
+  __device__ __forceinline__ uint32_t get(int64_t i) const { return (i >= 0 && i < n) ? s[i] : 0u; }
+  __device__ __forceinline__ void init(ds::CPtr src, int nl, int64_t off) {
+    s = src;
+    n = nl;
+    lw = off >> 5;
+    sh = (int)(off & 31);
+    lo = get(lw);
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const uint32_t hi = get(lw + 1);
+    const uint32_t r = __funnelshift_r(lo, hi, sh);
+    lo = hi;
+    lw++;
+    return r;
+  }
+};
+
+// the limbs T[0], T[1], ... of T = RN(P) (left-aligned L limbs): P's bits from
+// S bit offT up, the low zb bits cleared, + inc at bit zb with carry
+struct TGen {
+  BitStream b;
+  int k, zl, zs;
+  uint32_t carry, inc;
+  __device__ __forceinline__ void init(ds::CPtr S, int W, int64_t offT, int zb, uint32_t incr) {
+    b.init(S, W, offT);
+    k = 0;
+    zl = zb >> 5;
+    zs = zb & 31;
+    carry = 0;
+    inc = incr;
+  }
+  __device__ __forceinline__ uint32_t next() {
+    uint32_t v = b.next();
+    uint64_t t;
+    if (k < zl) {
+      t = 0;
+    } else if (k == zl) {
+      v &= ~((1u << zs) - 1u);
+      t = (uint64_t)v + ((uint64_t)inc << zs);
+    } else {
+      t = (uint64_t)v + carry;
+    }
+    carry = (uint32_t)(t >> 32);
+    k++;
+    return (uint32_t)t;
+  }
+};
+
+// a_jk <- RN(a_jk - RN(P_jk)) for the chunk's elements.  Fast path: T = RN(P)
+// is generated limb by limb from the stored product limbs and summed with a in
+// one pass into scratch ([word][thread], L + d/32 + 2 words), then rounded into
+// a's limbs.  Equal exponents with top limbs within one (the order of |a| and
+// |T| unknown before the carry): T materialised and the general add_rn.
+// Undecidable RN(P), or T rounding up to 2^p: the exact fallback list.
+__global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
+                                                    int64_t sthreads) {
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
-  const int L = a.L;
+  const int L = a.L, p = a.p, zb = 32 * L - p;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)w.nrows * a.ncols;
-  ds::Ptr T{scratch + tid, sthreads};
-  ds::Ptr tmp = T.off(L);
+  ds::Ptr tmp{scratch + tid, sthreads};
   for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
     const int k = a.kstart + cidx;
@@ -805,15 +863,25 @@ __global__ void k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratc
       continue;
     }
     const ds::CPtr S{w.tprod + (int64_t)ri * w.ncp + cidx, w.pstride};
-    const int64_t hb = ds::top_bit(S, w.W);
-    const int64_t lsb = hb - a.p + 1;
+    const int W = w.W;
+    const uint32_t stop = S[W - 1];
+    const int64_t hb = 32 * (int64_t)(W - 1) + 31 - __clz(stop);  // P >= 2^(64L-2): top limb nonzero
+    const int64_t lsb = hb - p + 1;
     bool amb = lsb - 1 <= w.eps;
+    uint32_t g = 0;
     if (!amb) {
-      bool ones, zeros, lz, lo_ones;
-      bit_range(S, w.W, w.eps, lsb - 1, &ones, &zeros);
-      const bool g = (ds::bits32(S, w.W, lsb - 1) & 1u) != 0;
-      bit_range(S, w.W, 0, w.eps, &lo_ones, &lz);
+      bool ones, zeros, lo_ones, lz;
+      bit_range(S, W, w.eps, lsb - 1, &ones, &zeros);
+      g = ds::bits32(S, W, lsb - 1) & 1u;
+      bit_range(S, W, 0, w.eps, &lo_ones, &lz);
       amb = ones || (g && zeros && lz);
+    }
+    const int64_t offT = hb + 1 - 32 * (int64_t)L;
+    // rounding T up overflows to 2^p only if its p kept bits are all ones (rare): exact engine
+    if (!amb && g) {
+      bool ones, zeros;
+      bit_range(S, W, lsb, hb + 1, &ones, &zeros);
+      amb = ones;
     }
     if (amb) {
       int slot = atomicAdd(a.fb_count, 1);
@@ -821,16 +889,155 @@ __global__ void k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratc
       else atomicAdd(&a.status[5], 1);
       continue;
     }
-    const int64_t base = (int64_t)a.zexp[zr] + a.bexp[k] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
-    ds::RoundOut ro = ds::round_big(T, L, a.p, S, w.W, base, false);
-    ds::Val t{ds::CPtr{T.p, T.s}, ro.e, (uint8_t)(st ? DS_CLS_NEG : DS_CLS_POS)};
-    ds::Val av{ds::CPtr{a.a_limbs + idx, a.a_count}, a.a_exp[idx], ca};
-    int32_t re;
-    uint8_t rc;
-    if (!ds::add_rn(ds::Ptr{a.a_limbs + idx, a.a_count}, &re, &rc, av, t, true, L, a.p, tmp))
-      atomicAdd(&a.status[2], 1);
-    a.a_exp[idx] = re;
-    a.a_cls[idx] = rc;
+    const int64_t eT = (int64_t)a.zexp[zr] + a.bexp[k] - 64 * (int64_t)L + 32 * (int64_t)w.qlo + hb + 1;
+    const int nT = st ^ 1;  // sign of -T
+    const ds::Ptr out{a.a_limbs + idx, a.a_count};
+    TGen tg;
+    tg.init(S, W, offT, zb, g);
+    if (ca >= DS_CLS_PZERO) {  // 0 - T = -T exactly
+      for (int l = 0; l < L; l++) out[l] = tg.next();
+      a.a_exp[idx] = (int32_t)eT;
+      a.a_cls[idx] = ds::nz_cls(nT);
+      if (!ds::range_ok(eT)) atomicAdd(&a.status[2], 1);
+      continue;
+    }
+    const int na = ca & 1;
+    const int64_t ea = a.a_exp[idx];
+    const ds::CPtr am{a.a_limbs + idx, a.a_count};
+    int xa;  // 1: |a| > |T|, 0: |T| > |a|, -1: undecided here
+    if (ea != eT) {
+      xa = ea > eT ? 1 : 0;
+    } else {
+      const uint32_t at = am[L - 1], tt = ds::bits32(S, W, 32 * (int64_t)(L - 1) + offT);
+      xa = (at > tt && at - tt >= 2u) ? 1 : ((tt > at && tt - at >= 2u) ? 0 : -1);
+    }
+    if (xa < 0) {
+      // general path: T into scratch, add_rn (needs 2L + 4 more words)
+      ds::Ptr T = tmp;
+      for (int l = 0; l < L; l++) T[l] = tg.next();
+      ds::Val t{ds::CPtr{T.p, T.s}, eT, (uint8_t)(st ? DS_CLS_NEG : DS_CLS_POS)};
+      ds::Val av{am, ea, ca};
+      int32_t re;
+      uint8_t rc;
+      if (!ds::add_rn(out, &re, &rc, av, t, true, L, p, tmp.off(L))) atomicAdd(&a.status[2], 1);
+      a.a_exp[idx] = re;
+      a.a_cls[idx] = rc;
+      continue;
+    }
+    const int64_t d = xa ? ea - eT : eT - ea;
+    if (d >= (int64_t)p + 2) {  // RN(X +- Y) = X
+      if (!xa) {
+        for (int l = 0; l < L; l++) out[l] = tg.next();
+        a.a_exp[idx] = (int32_t)eT;
+        a.a_cls[idx] = ds::nz_cls(nT);
+        if (!ds::range_ok(eT)) atomicAdd(&a.status[2], 1);
+      }
+      continue;
+    }
+    const bool sub = na != nT;
+    const int n2 = L + (int)(d >> 5) + 2;
+    // S2 = X 2^d +- Y (X the larger operand) into scratch, 8 limbs per batch so
+    // each thread keeps ~16 independent loads in flight
+    const int64_t lwT = offT >> 5;  // T(i) = low-masked funnel(S[lwT + i], S[lwT + i + 1], shT) + carry
+    const int shT = (int)(offT & 31);
+    const int zl = zb >> 5, zs = zb & 31;
+    uint32_t tcar = 0;
+    auto tval = [&](int64_t i, uint32_t raw) -> uint32_t {
+      if (i < zl || i >= L) return 0u;  // (i < 0 included)
+      uint64_t t;
+      if (i == zl) t = (uint64_t)(raw & ~((1u << zs) - 1u)) + ((uint64_t)g << zs);
+      else t = (uint64_t)raw + tcar;
+      tcar = (uint32_t)(t >> 32);
+      return (uint32_t)t;
+    };
+    auto sget = [&](int64_t i) -> uint32_t { return (i >= 0 && i < W) ? S[i] : 0u; };
+    auto aget = [&](int64_t i) -> uint32_t { return (i >= 0 && i < L) ? am[i] : 0u; };
+    const int64_t lwX = (-d) >> 5;  // X2[q] = funnel(X(q + lwX), X(q + lwX + 1), shX)
+    const int shX = (int)((-d) & 31);
+    uint32_t cb2 = 0;
+    uint32_t tprev = 0;  // X = T: T(q0 + lwX) carried between batches
+    if (!xa) tprev = tval(lwX, __funnelshift_r(sget(lwT + lwX), sget(lwT + lwX + 1), shT));
+    for (int q0 = 0; q0 < n2; q0 += 8) {
+      const int64_t ti0 = xa ? q0 : q0 + lwX + 1;  // first new T index of the batch
+      uint32_t sv[9], av[9], tv[8];
+#pragma unroll
+      for (int u = 0; u < 9; u++) sv[u] = sget(lwT + ti0 + u);
+#pragma unroll
+      for (int u = 0; u < 9; u++) av[u] = xa ? aget(q0 + lwX + u) : aget(q0 + u);
+#pragma unroll
+      for (int u = 0; u < 8; u++) tv[u] = tval(ti0 + u, __funnelshift_r(sv[u], sv[u + 1], shT));
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        uint32_t x, y;
+        if (xa) {
+          x = __funnelshift_r(av[u], av[u + 1], shX);
+          y = tv[u];
+        } else {
+          x = __funnelshift_r(u == 0 ? tprev : tv[u - 1], tv[u], shX);
+          y = av[u];
+        }
+        uint64_t t;
+        if (sub) {
+          t = (uint64_t)x - y - cb2;
+          cb2 = (uint32_t)(t >> 63);
+        } else {
+          t = (uint64_t)x + y + cb2;
+          cb2 = (uint32_t)(t >> 32);
+        }
+        tmp[q0 + u] = (uint32_t)t;
+      }
+      tprev = tv[7];
+    }
+    // round S2 (n2 limbs, nonzero) to p bits into a's limbs
+    const ds::CPtr S2{tmp.p, tmp.s};
+    int64_t hb2 = -1;
+    for (int q = n2 - 1; q >= 0; q--) {
+      const uint32_t v = S2[q];
+      if (v) {
+        hb2 = 32 * (int64_t)q + 31 - __clz(v);
+        break;
+      }
+    }
+    const int64_t lsb2 = hb2 - p + 1;
+    uint32_t inc = 0;
+    if (lsb2 >= 1 && ((ds::bits32(S2, n2, lsb2 - 1) & 1u) != 0)) {
+      const bool sticky = ds::any_below(S2, n2, lsb2 - 1);
+      const bool lsbit = (ds::bits32(S2, n2, lsb2) & 1u) != 0;
+      inc = (sticky || lsbit) ? 1u : 0u;
+    }
+    const int64_t off2 = hb2 + 1 - 32 * (int64_t)L;
+    const int64_t lw2 = off2 >> 5;
+    const int sh2 = (int)(off2 & 31);
+    uint32_t rc2 = 0;
+    for (int l0 = 0; l0 < L; l0 += 8) {
+      uint32_t v[9];
+#pragma unroll
+      for (int u = 0; u < 9; u++) {
+        const int64_t q = lw2 + l0 + u;
+        v[u] = (q >= 0 && q < n2) ? S2[q] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int l = l0 + u;
+        if (l < L) {
+          const uint32_t raw = __funnelshift_r(v[u], v[u + 1], sh2);
+          uint64_t t;
+          if (l < zl) t = 0;
+          else if (l == zl) t = (uint64_t)(raw & ~((1u << zs) - 1u)) + ((uint64_t)inc << zs);
+          else t = (uint64_t)raw + rc2;
+          rc2 = (uint32_t)(t >> 32);
+          out[l] = (uint32_t)t;
+        }
+      }
+    }
+    int64_t e2 = (xa ? eT : ea) - 32 * (int64_t)L + hb2 + 1;
+    if (rc2) {  // the mantissa rounded up to 2^p
+      out[L - 1] = 0x80000000u;
+      e2 += 1;
+    }
+    a.a_exp[idx] = (int32_t)e2;
+    a.a_cls[idx] = ds::nz_cls(xa ? na : nT);
+    if (!ds::range_ok(e2)) atomicAdd(&a.status[2], 1);
   }
 }
 
@@ -942,7 +1149,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   plan->work = w;
   w->fb_cap = 1 << 16;
   w->sthreads = 64 * 128;
-  w->tthreads = 148 * 4 * 128;
+  w->tthreads = 148 * 3 * 256;
   bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bbytes, (size_t)D8p * n) == cudaSuccess &&
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
@@ -951,7 +1158,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
             cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
             cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
             cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W) == cudaSuccess &&
-            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * (3 * (size_t)L + 8)) == cudaSuccess;
+            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * (3 * (size_t)L + 24)) == cudaSuccess;
   if (!ok) return DS_OOM;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return DS_OK;  // no tensor maps: not applicable
