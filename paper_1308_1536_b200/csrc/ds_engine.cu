@@ -927,7 +927,9 @@ static int warp_k(int L) {
   }
 
 static bool fast_real(ds_ctx* ctx) {
-  return ctx->kind == DS_KIND_REAL && ctx->plan.enabled && !force_general() && ctx->L <= 1024;
+  // the fused update or a tensor-core update, plus the DFMA row products
+  return ctx->kind == DS_KIND_REAL && ctx->plan.enabled && (ctx->plan.fused || ctx->tc.enabled) &&
+         !force_general() && ctx->L <= 1024;
 }
 
 static void set_wdiv_attrs(int maxsm) {
@@ -1216,7 +1218,7 @@ int ds_counters(ds_ctx* ctx, int64_t* out, int n) {
   int32_t st[8];
   CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  int64_t v[4] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.enabled && !ctx->tc.enabled) ? 1 : 0,
+  int64_t v[4] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.fused && !ctx->tc.enabled) ? 1 : 0,
                   (int64_t)(uint32_t)st[7]};
   for (int q = 0; q < n && q < 4; q++) out[q] = v[q];
   return DS_OK;

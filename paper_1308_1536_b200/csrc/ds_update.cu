@@ -446,6 +446,7 @@ static int pick_tr(int W, int Db, int L, int maxsm) {
 
 int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
   plan->enabled = 0;
+  plan->fused = 0;
   plan->n = n;
   plan->p = p;
   plan->L = (p + 31) / 32;
@@ -466,13 +467,15 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
     tc = 16;
     TR = 8;
     while (TR > 1 && fused_smem(W, TR, plan->D, plan->L, 16) > maxsm) TR /= 2;
-    if (fused_smem(W, TR, plan->D, plan->L, 16) > maxsm) return DS_OK;  // too wide for one CTA: general engine
+    // too wide for one CTA: no fused update (the wide tensor-core engine or the
+    // general engine updates), the row products still run here
+    if (fused_smem(W, TR, plan->D, plan->L, 16) > maxsm) TR = 0;
   }
   int smsm = 0;  // shared memory per SM
   cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   // two independent 16-column CTAs per SM desynchronise the warps' epilogues
   // (one 256-thread CTA runs all its warps in lockstep phases)
-  if (fused_smem(W, 8, plan->D, plan->L, 16) * 2 + 2048 <= smsm && !getenv("DS_FUSED_TC32")) {
+  if (TR && fused_smem(W, 8, plan->D, plan->L, 16) * 2 + 2048 <= smsm && !getenv("DS_FUSED_TC32")) {
     tc = 16;
     TR = 8;
   }
@@ -493,6 +496,7 @@ int update_plan_init(UpdatePlan* plan, int n, int p, int device) {
     if (clo < 0) clo = 0;
     if (split_smem(4, plan->D, plan->L, top_column(p), clo, 4) > maxsm) return DS_OK;
   }
+  plan->fused = TR > 0 ? 1 : 0;
   plan->enabled = 1;
   return DS_OK;
 }
@@ -558,6 +562,7 @@ int update_launch(UpdatePlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* 
                   int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
                   const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
                   int64_t* launches) {
+  if (!plan->fused) return DS_INVALID;
   int rc = ensure_work(plan, nloc);
   if (rc != DS_OK) return rc;
   UpdateWork* wk = (UpdateWork*)plan->workspace;

@@ -4,7 +4,8 @@
 #include <stdint.h>
 
 struct UpdatePlan {
-  int enabled;
+  int enabled;        // the DFMA kernels are usable (row products k_mul_split)
+  int fused;          // ... and the fused update k_fused fits one CTA
   int n, p, L, D;     // precision, 32-bit limbs, 24-bit digits
   int device, sms;
   int tr, tc, w;       // tile rows/cols, register block

@@ -66,9 +66,10 @@ def test_wide_forced_matches_tc(minors):
     assert results_digest(res_t, fin_t, n, p, steps) == results_digest(res_w, fin_w, n, p, steps)
 
 
-@pytest.mark.parametrize("n,p,steps", [(136, 16384, 2), (40, 16000, 2)])
-def test_wide_native_16k_matches_oracle(n, p, steps):
-    """16384 bits: the wide engine is the default (A no longer fits in TMEM)."""
+@pytest.mark.parametrize("n,p,steps", [(136, 16384, 2), (40, 16000, 2), (40, 32768, 2), (24, 33220, 3)])
+def test_wide_native_matches_oracle(n, p, steps):
+    """16384 bits and up: the wide engine is the default (A no longer fits in TMEM);
+    33220 bits = 10,000 decimal digits, the paper's headline precision."""
     A = random_uniform_soa(n, p, seed=n + 3 * p)
     res_o, fin_o = _oracle(A, n, p, steps)
     res_d, fin_d = _device_run(A, n, p, steps, True)
