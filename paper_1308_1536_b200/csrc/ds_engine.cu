@@ -461,7 +461,7 @@ __global__ void k_scalar_op(int op, int kind, int L, int p, int64_t count, const
 __host__ __device__ static inline int wdiv_kq(int p) { return (p + 2 + 31) / 32; }
 __host__ __device__ static inline int wdiv_words(int L, int p, int K) {
   int nu = L + wdiv_kq(p) + 1;
-  return L + (nu + 32 * K) + (nu - L) + 4;
+  return L + dsw::upad_words(nu + 32 * K) + (nu - L) + 4;
 }
 
 template <int K>
@@ -480,9 +480,9 @@ __device__ void wdiv_rn(Out o, const Val& a, const Val& b, int L, int p, uint32_
   const int nu = L + kq + 1;
   uint32_t* V = sm;
   uint32_t* U = V + L;
-  uint32_t* Q = U + nu + 32 * K;
+  uint32_t* Q = U + dsw::upad_words(nu + 32 * K);
   for (int l = lane; l < L; l += 32) V[l] = b.m[l];
-  for (int k = lane; k < nu + 32 * K; k += 32) U[k] = (k >= kq && k < kq + L) ? a.m[k - kq] : 0u;
+  for (int k = lane; k < nu + 32 * K; k += 32) U[dsw::upad(k)] = (k >= kq && k < kq + L) ? a.m[k - kq] : 0u;
   uint32_t vb[K];
 #pragma unroll
   for (int u = 0; u < K; u++) {

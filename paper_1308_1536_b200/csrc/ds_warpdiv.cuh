@@ -38,14 +38,22 @@ __device__ __forceinline__ uint32_t cla(bool g, bool p, uint32_t& cio, int nvali
 // limb zero), V has n limbs with the MSB of V[n-1] set; the lane-blocked copy
 // vb[] (lane t holds V[t*K .. t*K+K)) lives in registers.  Q gets nu-n limbs.
 // Returns true when the remainder is nonzero.
+// padded U index (one pad word per 32): conflict-free lane blocks
+__host__ __device__ __forceinline__ int upad(int i) { return i + (i >> 5); }
+// words of a padded U of nu limbs
+__host__ __device__ __forceinline__ int upad_words(int nu) { return nu + (nu >> 5) + 1; }
+
 template <int K>
 __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, const uint32_t (&vb)[K], int n) {
   const int lane = threadIdx.x & 31;
+  // U is stored padded (one word after every 32, upad) so that the lanes'
+  // K-limb blocks fall in distinct banks
+#define UP(i) U[upad(i)]
   const uint64_t vtop = V[n - 1];
   const uint64_t vnext = V[n - 2];
   const double vinv = 1.0 / (double)vtop;  // vtop >= 2^31: the estimate below is within 1 of num / vtop
   for (int j = nu - n - 1; j >= 0; j--) {
-    uint64_t num = ((uint64_t)U[j + n] << 32) | U[j + n - 1];
+    uint64_t num = ((uint64_t)UP(j + n) << 32) | UP(j + n - 1);
     // qhat = min(floor(num / vtop), 2^32 - 1): double estimate + exact correction
     uint64_t qhat = (uint64_t)((double)num * vinv);
     if (qhat > 0x1ffffffffull) qhat = 0x1ffffffffull;
@@ -60,7 +68,7 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
     }
     if (qhat > 0xffffffffull) qhat = 0xffffffffull;
     uint64_t rhat = num - qhat * vtop;
-    while (rhat < (1ull << 32) && qhat * vnext > ((rhat << 32) | (uint64_t)U[j + n - 2])) {
+    while (rhat < (1ull << 32) && qhat * vnext > ((rhat << 32) | (uint64_t)UP(j + n - 2))) {
       qhat -= 1;
       rhat += vtop;
     }
@@ -95,11 +103,11 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
     // product top limb: last lane's carry word + carry out of the lane chain
     uint32_t htop = __shfl_sync(FULL, (uint32_t)h, 31) + cio;
     // subtract the block from U[j + lane*K ..]: U + ~pb + 1 (carry chain; borrow = 1 - carry)
-    uint32_t* Ub = U + j + lane * K;
+    const int ub0 = j + lane * K;
     uint32_t ub[K];
 #pragma unroll
     for (int u = 0; u < K; u++) {
-      ub[u] = Ub[u];
+      ub[u] = UP(ub0 + u);
       mk[u] = ~pb[u];
     }
     uint32_t cy = 1u;
@@ -117,16 +125,16 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
     uint32_t c0 = 0u;
     dss::addc_n<K>(ub, ub, mk, c0);
 #pragma unroll
-    for (int u = 0; u < K; u++) Ub[u] = ub[u];
+    for (int u = 0; u < K; u++) UP(ub0 + u) = ub[u];
     __syncwarp();
     // top limb U[j + 32K] (= U[j+n] when n == 32K; the zero-padded tail of V
     // makes the blocks cover n limbs exactly when n < 32K as well)
     int top = j + 32 * K;
     uint64_t ytop = (uint64_t)htop + bio;
-    uint32_t utop = U[top];
+    uint32_t utop = UP(top);
     bool neg = (uint64_t)utop < ytop;
     __syncwarp();
-    if (lane == 0) U[top] = (uint32_t)((uint64_t)utop - ytop);
+    if (lane == 0) UP(top) = (uint32_t)((uint64_t)utop - ytop);
     __syncwarp();
     if (neg) {  // add V back (rare): U[j .. j+32K] += V
       qhat -= 1;
@@ -134,7 +142,7 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
       uint32_t co = 0;
 #pragma unroll
       for (int u = 0; u < K; u++) {
-        uint64_t t = (uint64_t)Ub[u] + vb[u] + co;
+        uint64_t t = (uint64_t)UP(ub0 + u) + vb[u] + co;
         a2[u] = (uint32_t)t;
         co = (uint32_t)(t >> 32);
       }
@@ -151,16 +159,17 @@ __device__ bool wdivrem(uint32_t* Q, uint32_t* U, int nu, const uint32_t* V, con
         }
       }
 #pragma unroll
-      for (int u = 0; u < K; u++) Ub[u] = a2[u];
+      for (int u = 0; u < K; u++) UP(ub0 + u) = a2[u];
       __syncwarp();
-      if (lane == 0) U[top] += cio2;
+      if (lane == 0) UP(top) += cio2;
       __syncwarp();
     }
     if (lane == 0) Q[j] = (uint32_t)qhat;
     __syncwarp();
   }
   bool nz = false;
-  for (int i = lane; i < n; i += 32) nz |= U[i] != 0;
+  for (int i = lane; i < n; i += 32) nz |= UP(i) != 0;
+#undef UP
   return __any_sync(FULL, nz);
 }
 
