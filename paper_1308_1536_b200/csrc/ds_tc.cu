@@ -584,6 +584,7 @@ struct TwArgs {
   int tn, ntiles, kc, nst, brc;  // MMA N, tiles, K steps per stage, stages, bank rows per stage
   int nrows, rbr, kstart, ncp, zwb;
   const uint8_t* zbytes;  // the chunk's rows [nrows][D8p]
+  const uint8_t* apack;   // k_tcw_pack image of the pivot-row digits
   uint32_t* tprod;        // [W][nrows][ncp]
   int64_t pstride;        // nrows * ncp
   int32_t* status;
@@ -594,7 +595,45 @@ __device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(TW_THREADS, 1) k_prod_tcw(TwArgs a, const __grid_constant__ CUtensorMap bmap) {
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// pivot-row digits packed in the MMA A operand's shared-memory image: for column
+// tile ct (128 columns from kstart) and K step ks, 2 halves x 128 rows x 16 B
+// (digits 32 ks + 16 h .. +16 of column kstart + 128 ct + r), so one stage of A
+// is one contiguous bulk copy.  One thread per 16-byte piece (4 limbs).
+__global__ void k_tcw_pack(const uint32_t* b_limbs, int n, int L, int nks, int kstart, int ntile, uint8_t* apack) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)ntile * nks * 2 * TM) return;
+  const int r = (int)(t % TM);
+  const int64_t rest = t / TM;  // (ct * nks + ks) * 2 + h
+  const int h = (int)(rest & 1);
+  const int ks = (int)((rest >> 1) % nks);
+  const int ct = (int)((rest >> 1) / nks);
+  const int col = kstart + ct * TM + r;
+  const int l0 = 8 * ks + 4 * h;
+  uint32_t v[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++) v[u] = (col < n && l0 + u < L) ? b_limbs[(int64_t)(l0 + u) * n + col] : 0u;
+  *(uint4*)(apack + rest * 2048 + (int64_t)r * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+__device__ __forceinline__ void tld32(uint32_t (&v)[32], uint32_t addr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(addr));
+}
+
+__global__ void __launch_bounds__(TW_THREADS, 1) k_prod_tcw(TwArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_full[8];
   __shared__ __align__(8) uint64_t bar_empty[8];
@@ -654,10 +693,9 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_prod_tcw(TwArgs a, const __gr
           uint8_t* A = smem + (size_t)st * SBYTES;
           uint8_t* bank = A + ABYTES;
           if (ptid == 0) {
-            mbar_expect(&bar_full[st], (uint32_t)(kb - ka + 1) * 4096u);
-            for (int ks = ka; ks <= kb; ks++)
-              for (int h = 0; h < 2; h++)
-                tma_load_2d(A + (ks - ka) * 4096 + h * 2048, &bmap, KS * ks + 16 * h, kbase, &bar_full[st]);
+            const uint32_t bytes = (uint32_t)(kb - ka + 1) * 4096u;
+            mbar_expect(&bar_full[st], bytes);
+            bulk_load(A, a.apack + ((int64_t)blockIdx.x * a.nks + ka) * 4096, bytes, &bar_full[st]);
           }
           // bank row r <-> m = c0 - 32 kb + r: half h holds Z[m - 16h - j], j = 0..15
           const int bru = TN + KS * (kb - ka);
@@ -731,30 +769,62 @@ __global__ void __launch_bounds__(TW_THREADS, 1) k_prod_tcw(TwArgs a, const __gr
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * TN);
         const int c0 = a.c_lo + t * TN;
         const int cend = min(TN, 2 * D8p - c0);
-#pragma unroll 1
-        for (int cb = 0; cb < cend; cb += 32) {
-          uint32_t v[32];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-              : "r"(taddr + cb));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-          const int q0 = (c0 + cb) >> 2;
+        // limb q = w_q + hi(w_(q-1)) + carry, w_q = sum_j v[4q+j] 2^(8j) < 2^54: independent
+        // wide multiply-adds, one add.cc chain per 8 limbs; the next 32 columns are
+        // loaded from TMEM while this chunk is converted and stored
+        auto conv = [&](const uint32_t(&v)[32], int cb) {
+          uint32_t lo[8], hi[8], P[8];
 #pragma unroll
           for (int g = 0; g < 8; g++) {
-            // digit sums < 2^31: limb = sum_j v[4g+j] 2^(8j) + carry < 2^56
             uint64_t w = (uint64_t)v[4 * g + 3] * 16777216u;
             w += (uint64_t)v[4 * g + 2] * 65536u;
             w += (uint64_t)v[4 * g + 1] * 256u;
-            w += (uint64_t)v[4 * g] + carry;
-            const int q = q0 + g;
-            if (q < 2 * a.L) out[(int64_t)(q - a.qlo) * a.pstride] = (uint32_t)w;
-            carry = (uint32_t)(w >> 32);
+            w += (uint64_t)v[4 * g] * 1u;
+            lo[g] = (uint32_t)w;
+            hi[g] = (uint32_t)(w >> 32);
+          }
+          asm("add.cc.u32 %0, %9, %8;\n\t"
+              "addc.cc.u32 %1, %10, %17;\n\t"
+              "addc.cc.u32 %2, %11, %18;\n\t"
+              "addc.cc.u32 %3, %12, %19;\n\t"
+              "addc.cc.u32 %4, %13, %20;\n\t"
+              "addc.cc.u32 %5, %14, %21;\n\t"
+              "addc.cc.u32 %6, %15, %22;\n\t"
+              "addc.cc.u32 %7, %16, %23;\n\t"
+              "addc.u32 %8, %24, 0;"
+              : "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]),
+                "+r"(carry)
+              : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]),
+                "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
+          const int q0 = (c0 + cb) >> 2;
+          uint32_t* op = out + (int64_t)(q0 - a.qlo) * a.pstride;
+          if (q0 + 8 <= 2 * a.L) {
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+              *op = P[g];
+              op += a.pstride;
+            }
+          } else {
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+              if (q0 + g < 2 * a.L) *op = P[g];
+              op += a.pstride;
+            }
+          }
+        };
+        uint32_t va[32], vb[32];
+        tld32(va, taddr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll 1
+        for (int cb = 0; cb < cend; cb += 64) {
+          const bool m1 = cb + 32 < cend, m2 = cb + 64 < cend;
+          if (m1) tld32(vb, taddr + cb + 32);
+          conv(va, cb);
+          if (m1) {
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (m2) tld32(va, taddr + cb + 64);
+            conv(vb, cb + 32);
+            if (m2) asm volatile("tcgen05.wait::ld.sync.aligned;");
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1090,7 +1160,6 @@ struct TcWork {
   int64_t sthreads;
   int fb_cap;
   CUtensorMap amap;        // a planes: dims {a_count, L}, box {128, L}
-  CUtensorMap bmap;        // wide: pivot-row digits, dims {D8p, n}, box {16, 128}
   uint32_t* tprod;         // wide: product limbs [W][rows][ncp]
   uint32_t* tscratch;      // wide: finish-kernel scratch [3L + 8][tthreads]
   int64_t tthreads;
@@ -1114,6 +1183,9 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   if (2 * D8p - clo < tn) tn = (2 * D8p - clo + 31) & ~31;
   if (clo + tn <= D8p || clo - D8p + 1 - 31 - TW_ZLO < 0) return DS_OK;  // zw window assumptions
   int kc = 8, nst = 3;
+  if (const char* e = getenv("DS_TCW_KC")) kc = atoi(e);
+  if (const char* e = getenv("DS_TCW_NST")) nst = atoi(e);
+  if (nst > 8) nst = 8;
   const int zwb = (D8p + tn + 256 + 15) & ~15;
   size_t sm = 0;
   for (;;) {
@@ -1134,6 +1206,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   plan->w_W = 2 * L - clo / 4;
   plan->w_zwb = zwb;
   plan->w_rbr = 2;
+  if (const char* e = getenv("DS_TCW_RBR")) plan->w_rbr = atoi(e) > 0 ? atoi(e) : 1;
   plan->smem = sm;
   if (cudaFuncSetAttribute(k_prod_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return DS_CUDA;
@@ -1151,7 +1224,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   w->sthreads = 64 * 128;
   w->tthreads = 148 * 3 * 256;
   bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
-            cudaMalloc(&w->bbytes, (size_t)D8p * n) == cudaSuccess &&
+            cudaMalloc(&w->bbytes, (size_t)D8p * ncp) == cudaSuccess &&  // k_tcw_pack image
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
             cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
@@ -1160,16 +1233,6 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
             cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W) == cudaSuccess &&
             cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * (3 * (size_t)L + 24)) == cudaSuccess;
   if (!ok) return DS_OOM;
-  EncodeTiledFn enc = encode_tiled();
-  if (!enc) return DS_OK;  // no tensor maps: not applicable
-  cuuint64_t dims[2] = {(cuuint64_t)D8p, (cuuint64_t)n};
-  cuuint64_t strides[1] = {(cuuint64_t)D8p};
-  cuuint32_t box[2] = {16, (cuuint32_t)TM};
-  cuuint32_t estr[2] = {1, 1};
-  if (enc(&w->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)w->bbytes, dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return DS_OK;
   plan->enabled = 1;
   return DS_OK;
 }
@@ -1274,7 +1337,8 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   const int W4 = plan->D8p / 4;
   k_tc_bytes<<<(unsigned)(((int64_t)nrows * W4 + 255) / 256), 256, 0, s>>>(z_limbs + jl0, nloc, nrows, L, plan->D8p,
                                                                           w->zbytes, w->zf);
-  k_tc_bytes<<<(unsigned)(((int64_t)n * W4 + 255) / 256), 256, 0, s>>>(b_limbs, n, n, L, plan->D8p, w->bbytes, w->bf);
+  if (!plan->wide)
+    k_tc_bytes<<<(unsigned)(((int64_t)n * W4 + 255) / 256), 256, 0, s>>>(b_limbs, n, n, L, plan->D8p, w->bbytes, w->bf);
   cudaMemsetAsync(w->fb_count, 0, sizeof(int), s);
   TcArgs a;
   a.p = plan->p; a.L = L; a.zb = 32 * L - plan->p; a.D8p = plan->D8p; a.nks = plan->nks; a.ntiles = plan->ntiles;
@@ -1293,6 +1357,8 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     a.tskip = -1;
     const int ntile = (ncols + TM - 1) / TM;
     const int ncp = ntile * TM;
+    const int64_t npieces = (int64_t)ntile * plan->nks * 2 * TM;
+    k_tcw_pack<<<(unsigned)((npieces + 255) / 256), 256, 0, s>>>(b_limbs, n, L, plan->nks, kstart, ntile, w->bbytes);
     for (int r0 = 0; r0 < nrows; r0 += plan->w_rows) {
       const int rc = nrows - r0 < plan->w_rows ? nrows - r0 : plan->w_rows;
       TwArgs tw;
@@ -1301,10 +1367,11 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
       tw.tn = plan->tn; tw.ntiles = plan->ntiles; tw.kc = plan->w_kc; tw.nst = plan->w_nst; tw.brc = plan->w_brc;
       tw.nrows = rc; tw.rbr = plan->w_rbr; tw.kstart = kstart; tw.ncp = ncp; tw.zwb = plan->w_zwb;
       tw.zbytes = w->zbytes + (size_t)r0 * plan->D8p;
+      tw.apack = w->bbytes;
       tw.tprod = w->tprod;
       tw.pstride = (int64_t)rc * ncp;
       tw.status = status; tw.step = i;
-      k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tw, w->bmap);
+      k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tw);
       k_tcw_finish<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch, w->tthreads);
       *launches += 2;
     }
