@@ -918,7 +918,12 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
   const int L = a.L, p = a.p, zb = 32 * L - p;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)w.nrows * a.ncols;
-  ds::Ptr tmp{scratch + tid, sthreads};
+  // per-thread scratch row (contiguous, 32-byte aligned): the S2 limbs are written
+  // as whole sectors and re-read at per-element offsets from L1
+  const int RW = (3 * L + 24 + 7) & ~7;
+  (void)sthreads;
+  uint32_t* row = scratch + tid * (int64_t)RW;
+  ds::Ptr tmp{row, 1};
   for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
     const int k = a.kstart + cidx;
@@ -949,8 +954,12 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     const int64_t offT = hb + 1 - 32 * (int64_t)L;
     // rounding T up overflows to 2^p only if its p kept bits are all ones (rare): exact engine
     if (!amb && g) {
-      bool ones, zeros;
-      bit_range(S, W, lsb, hb + 1, &ones, &zeros);
+      bool ones = true;  // scanned from the top: almost always decided by the first word
+      for (int64_t pos = hb + 1; pos > lsb && ones; pos -= 32) {
+        const int nb = (int)min((int64_t)32, pos - lsb);
+        const uint32_t v = ds::bits32(S, W, pos - nb) | (nb == 32 ? 0u : ~((1u << nb) - 1u));
+        ones = v == 0xffffffffu;
+      }
       amb = ones;
     }
     if (amb) {
@@ -1029,7 +1038,7 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     if (!xa) tprev = tval(lwX, __funnelshift_r(sget(lwT + lwX), sget(lwT + lwX + 1), shT));
     for (int q0 = 0; q0 < n2; q0 += 8) {
       const int64_t ti0 = xa ? q0 : q0 + lwX + 1;  // first new T index of the batch
-      uint32_t sv[9], av[9], tv[8];
+      uint32_t sv[9], av[9], tv[8], s2[8];
 #pragma unroll
       for (int u = 0; u < 9; u++) sv[u] = sget(lwT + ti0 + u);
 #pragma unroll
@@ -1054,9 +1063,11 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
           t = (uint64_t)x + y + cb2;
           cb2 = (uint32_t)(t >> 32);
         }
-        tmp[q0 + u] = (uint32_t)t;
+        s2[u] = (uint32_t)t;
       }
       tprev = tv[7];
+      *(uint4*)(row + q0) = make_uint4(s2[0], s2[1], s2[2], s2[3]);
+      *(uint4*)(row + q0 + 4) = make_uint4(s2[4], s2[5], s2[6], s2[7]);
     }
     // round S2 (n2 limbs, nonzero) to p bits into a's limbs
     const ds::CPtr S2{tmp.p, tmp.s};
@@ -1231,7 +1242,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
             cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
             cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
             cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W) == cudaSuccess &&
-            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * (3 * (size_t)L + 24)) == cudaSuccess;
+            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * ((3 * (size_t)L + 24 + 7) & ~(size_t)7)) == cudaSuccess;
   if (!ok) return DS_OOM;
   plan->enabled = 1;
   return DS_OK;
