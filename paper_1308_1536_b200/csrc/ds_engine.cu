@@ -923,14 +923,19 @@ static int warp_k(int L) {
     case 4: KERNEL<4><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
     case 8: KERNEL<8><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
     case 16: KERNEL<16><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
-    default: KERNEL<32><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    case 32: KERNEL<32><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    default: KERNEL<64><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
   }
 
 static bool fast_real(ds_ctx* ctx) {
   // the fused update or a tensor-core update, plus the DFMA row products
   return ctx->kind == DS_KIND_REAL && ctx->plan.enabled && (ctx->plan.fused || ctx->tc.enabled) &&
-         !force_general() && ctx->L <= 1024;
+         !force_general();
 }
+
+// the warp division holds K = L/32 <= 64 limbs per lane in registers (K = 64:
+// 33220 bits, L = 1039); wider precisions divide with the thread-level engine
+static bool wdiv_ok(const ds_ctx* ctx) { return ctx->L <= 2048; }
 
 static void set_wdiv_attrs(int maxsm) {
   static bool done = false;
@@ -942,7 +947,8 @@ static void set_wdiv_attrs(int maxsm) {
   cudaFuncSetAttribute(KERNEL<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
-  cudaFuncSetAttribute(KERNEL<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  cudaFuncSetAttribute(KERNEL<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   SA(k_mult_w)
   SA(k_emit_norm_w)
 #undef SA
@@ -1013,7 +1019,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     // ---- multipliers z_j = RN(a_ji / piv), a_ji <- -z_j (elim.py:47, 53)
     if (fast && la_have) {
       CK(cudaStreamWaitEvent(s, ctx->ev_mult, 0));  // computed by the previous step's lookahead
-    } else if (fast) {
+    } else if (fast && wdiv_ok(ctx)) {
       int blocks = (nrows + wpb - 1) / wpb;
       size_t smem = (size_t)wpb * wwords * 4;
       WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0, nullptr);
@@ -1093,9 +1099,13 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
                                 ctx->status, &ctx->launches, i, ctx->ws_ex, ctx->ws_ey);
         if (rc != DS_OK) { ctx->err = "minor product launch failed"; return rc; }
         k_emit_last<<<1, 128, 0, ss>>>(k, i);
-        int blocks = (m + wpb - 1) / wpb;
-        size_t smem = (size_t)wpb * wwords * 4;
-        WDIV_DISPATCH(K, k_emit_norm_w, blocks, 32 * wpb, smem, ss, k, i, wwords);
+        if (wdiv_ok(ctx)) {
+          int blocks = (m + wpb - 1) / wpb;
+          size_t smem = (size_t)wpb * wwords * 4;
+          WDIV_DISPATCH(K, k_emit_norm_w, blocks, 32 * wpb, smem, ss, k, i, wwords);
+        } else {
+          k_emit_norm<<<grid_for(ctx, m, 64), 64, 0, ss>>>(k, i);
+        }
         ctx->launches += 2;
       } else {
         k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
@@ -1163,6 +1173,7 @@ int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
 }
 
 int ds_lookahead_enable(ds_ctx* ctx, int limit) {
+  if (limit > 0 && (!fast_real(ctx) || !wdiv_ok(ctx))) return DS_INVALID;  // needs the warp division
   ctx->la_limit = limit;
   ctx->la_ext = limit > 0 ? 1 : 0;
   if (limit <= 0) ctx->la_step = -1;
@@ -1185,7 +1196,7 @@ int ds_lookahead_pivot(ds_ctx* ctx, int i1, void* buf) {
 }
 
 int ds_lookahead_mult(ds_ctx* ctx, int i1, const void* buf) {
-  if (i1 < 0 || i1 >= ctx->n || !fast_real(ctx)) return DS_INVALID;
+  if (i1 < 0 || i1 >= ctx->n || !fast_real(ctx) || !wdiv_ok(ctx)) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
   KArgs k = kargs(ctx);
   k.z_limbs = ctx->zb_limbs[i1 & 1];

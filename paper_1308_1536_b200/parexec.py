@@ -280,6 +280,8 @@ def _lookahead_setup(engine, n: int, pivot):
     if not getattr(pivot, "is_cuda", False) or not engine.counters().get("tc_engine"):
         return None  # only the tensor-core engine splits its update for the lookahead
     torch = _torch()
+    if engine.L > 2048:
+        return None  # the lookahead multipliers need the warp division (L <= 2048 limbs)
     engine.lookahead_enable(n)
     ext = torch.cuda.ExternalStream(engine.lookahead_stream(), device=pivot.device)
     scal = torch.zeros(4 * engine.L + 8, dtype=torch.uint8, device=pivot.device)
