@@ -810,6 +810,14 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
       }
     }
   }
+  if (kind == DS_KIND_COMPLEX) {
+    rc = tc_plan_init_c(&ctx->tc, n, ctx->nloc, ctx->p, device);
+    if (rc != DS_OK) {
+      ctx->err = "complex tensor-core update plan: device allocation or attribute failed";
+      ds_destroy(ctx);
+      return rc;
+    }
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
   return DS_OK;
@@ -1073,6 +1081,12 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         CK(cudaEventRecord(ctx->ev_mult, ctx->la));
         ctx->la_step = i + 1;
       }
+    } else if (ctx->kind == DS_KIND_COMPLEX && ctx->tc.enabled && !force_general()) {
+      // complex: the four component products on the wide tensor-core engine
+      int rc = tc_update_launch(&ctx->tc, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
+                                ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
+                                ctx->status, &ctx->launches);
+      if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
     } else {
       int kfirst = collect_minors ? 0 : i + 1;
       int64_t ncols = n - kfirst - (collect_minors ? 1 : 0);

@@ -59,6 +59,7 @@ struct TcArgs {
   int tile0, tskip;        // column tile of blockIdx.x 0; tile index skipped (-1: none)
   int rbr;                 // rows per CTA
   int jl0;
+  int64_t zstride;         // component stride of the z meta (complex: nloc)
   const uint8_t* zbytes;   // [nrows][D8p]
   const uint8_t* bbytes;   // [n][D8p]
   const double* zf;        // [nrows]
@@ -1122,6 +1123,150 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
   }
 }
 
+// ---------------------------------------------------------------- complex
+// a <- RN(a - RN(z b)) per component on the wide engine (elim.py:49-52 on mpc):
+// Re = RN(zr br - zi bi), Im = RN(zr bi + zi br), each the exact formula rounded
+// once (mpc_mul), then a_c <- RN(a_c - t_c) (mpc_sub).  The four products come
+// from k_prod_tcw as truncated limbs (each short by < 2^eps units of its limb
+// q_lo); their exact aligned sum (ds::exact_sum) is rounded when the bits
+// between the combined error bound and the round bit are neither all zeros nor
+// all ones, so no rounding boundary lies within the error; else the element
+// takes the exact complex fallback.  Scratch row per thread: sum | T_re | T_im |
+// add_rn.
+__global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int row_first, uint32_t* scratch) {
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  const int L = a.L, p = a.p;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)w.nrows * a.ncols;
+  const int RW = (8 * L + 32 + 7) & ~7;
+  uint32_t* row = scratch + tid * (int64_t)RW;
+  const ds::Ptr Ssum{row, 1}, Tre{row + 4 * L + 16, 1}, Tim{row + 5 * L + 16, 1}, tmp{row + 6 * L + 16, 1};
+  const int64_t region = w.pstride * (int64_t)w.W;  // words per product region (c1, c2)
+  for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
+    const int k = a.kstart + cidx;
+    if (k < a.kmin || k == a.skip_col || k >= a.n) continue;
+    const int zr = row_first + ri;  // relative to jl0
+    const int jl = a.jl0 + zr;
+    const int64_t idx = (int64_t)jl * a.n + k;
+    int64_t ze[2], be[2];
+    uint8_t zc[2], bc[2];
+    for (int c = 0; c < 2; c++) {
+      ze[c] = a.zexp[(int64_t)c * a.zstride + zr];
+      zc[c] = a.zcls[(int64_t)c * a.zstride + zr];
+      be[c] = a.bexp[(int64_t)c * a.n + k];
+      bc[c] = a.bcls[(int64_t)c * a.n + k];
+    }
+    auto term = [&](int c1, int c2) -> ds::XTerm {
+      ds::XTerm t;
+      t.m = ds::CPtr{w.tprod + (2 * c1 + c2) * region + (int64_t)ri * w.ncp + cidx, w.pstride};
+      t.n = w.W;
+      t.base = ze[c1] + be[c2] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
+      t.neg = (zc[c1] & 1) ^ (bc[c2] & 1);
+      t.zero = zc[c1] >= DS_CLS_PZERO || bc[c2] >= DS_CLS_PZERO;
+      return t;
+    };
+    bool ok = true;
+    int32_t te[2];
+    uint8_t tcl[2];
+    for (int c = 0; c < 2 && ok; c++) {
+      const ds::XTerm X = c == 0 ? term(0, 0) : term(0, 1);
+      const ds::XTerm Y = c == 0 ? term(1, 1) : term(1, 0);
+      const ds::XSum x = ds::exact_sum(Ssum, X, Y, c == 0, 2 * (int64_t)p + 64);
+      if (x.zero) {
+        ok = X.zero && Y.zero;  // a truncated nonzero sum that cancels: undecided
+      } else {
+        const int64_t H = x.base + ds::top_bit(ds::CPtr{Ssum.p, 1}, x.n);
+        const int64_t R = H - p + 1;  // weight of the result's LSB
+        int64_t bnd = INT64_MIN;
+        int64_t tmin = INT64_MAX;
+        if (!X.zero) {
+          bnd = max(bnd, X.base + w.eps);
+          tmin = min(tmin, X.base + ds::top_bit(X.m, X.n));
+        }
+        if (!Y.zero) {
+          bnd = max(bnd, Y.base + w.eps);
+          tmin = min(tmin, Y.base + ds::top_bit(Y.m, Y.n));
+        }
+        bnd += 1;                                // both errors together < 2^bnd
+        if (x.pert) bnd = max(bnd, tmin + 2);    // the far term only perturbs
+        if (R - 1 <= bnd) {
+          ok = false;
+        } else {
+          bool ones, zeros;
+          bit_range(ds::CPtr{Ssum.p, 1}, x.n, max((int64_t)0, bnd - x.base), R - 1 - x.base, &ones, &zeros);
+          ok = !ones && !zeros;
+        }
+      }
+      if (ok) {
+        const ds::Ptr T = c == 0 ? Tre : Tim;
+        if (!ds::round_xsum(T, &te[c], &tcl[c], Ssum, x, L, p)) atomicAdd(&a.status[2], 1);
+      }
+    }
+    if (!ok) {
+      int slot = atomicAdd(a.fb_count, 1);
+      if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
+      else atomicAdd(&a.status[5], 1);
+      continue;
+    }
+    for (int c = 0; c < 2; c++) {
+      const int64_t off = (int64_t)c * L * a.a_count + idx;
+      const int64_t mo = (int64_t)c * a.a_count + idx;
+      ds::Val av{ds::CPtr{a.a_limbs + off, a.a_count}, a.a_exp[mo], a.a_cls[mo]};
+      ds::Val tv{ds::CPtr{(c == 0 ? Tre : Tim).p, 1}, te[c], tcl[c]};
+      int32_t re;
+      uint8_t rc;
+      if (!ds::add_rn(ds::Ptr{a.a_limbs + off, a.a_count}, &re, &rc, av, tv, true, L, p, tmp))
+        atomicAdd(&a.status[2], 1);
+      a.a_exp[mo] = re;
+      a.a_cls[mo] = rc;
+    }
+  }
+}
+
+// exact complex update of the listed elements: cmul_part x 2 then add_rn x 2
+__global__ void k_tc_fallback_c(TcArgs a, const uint32_t* z_limbs, int64_t z_count, const uint32_t* b_limbs,
+                                uint32_t* scratch, int64_t sthreads) {
+  if (a.status[0] >= 0 && a.status[0] <= a.step) return;
+  int cnt = *a.fb_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && cnt > 0) atomicAdd(&a.status[6], cnt);
+  if (cnt > a.fb_cap) cnt = a.fb_cap;
+  const int L = a.L;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt; q += (int64_t)gridDim.x * blockDim.x) {
+    int2 e = a.fb_list[q];
+    const int jl = e.x, k = e.y;
+    const int zr = jl - a.jl0;
+    const int64_t idx = (int64_t)jl * a.n + k;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ds::Ptr base{scratch + tid, sthreads};
+    ds::Ptr tre = base, tim = base.off(L), work = base.off(2 * (int64_t)L);
+    ds::Val zv[2], bv[2], av[2];
+    for (int c = 0; c < 2; c++) {
+      zv[c] = ds::Val{ds::CPtr{z_limbs + (int64_t)c * L * z_count + jl, z_count}, a.zexp[(int64_t)c * a.zstride + zr],
+                      a.zcls[(int64_t)c * a.zstride + zr]};
+      bv[c] = ds::Val{ds::CPtr{b_limbs + (int64_t)c * L * a.n + k, a.n}, a.bexp[(int64_t)c * a.n + k],
+                      a.bcls[(int64_t)c * a.n + k]};
+      const int64_t mo = (int64_t)c * a.a_count + idx;
+      av[c] = ds::Val{ds::CPtr{a.a_limbs + (int64_t)c * L * a.a_count + idx, a.a_count}, a.a_exp[mo], a.a_cls[mo]};
+    }
+    int32_t te[2];
+    uint8_t tc[2];
+    ds::cmul_part(tre, &te[0], &tc[0], zv[0], bv[0], zv[1], bv[1], true, L, a.p, work);
+    ds::cmul_part(tim, &te[1], &tc[1], zv[0], bv[1], zv[1], bv[0], false, L, a.p, work);
+    for (int c = 0; c < 2; c++) {
+      ds::Val t{ds::CPtr{(c == 0 ? tre : tim).p, sthreads}, te[c], tc[c]};
+      const int64_t mo = (int64_t)c * a.a_count + idx;
+      int32_t re;
+      uint8_t rc;
+      if (!ds::add_rn(ds::Ptr{a.a_limbs + (int64_t)c * L * a.a_count + idx, a.a_count}, &re, &rc, av[c], t, true, L,
+                      a.p, work))
+        atomicAdd(&a.status[2], 1);
+      a.a_exp[mo] = re;
+      a.a_cls[mo] = rc;
+    }
+  }
+}
+
 size_t tc_smem(int L, int br, int ng) {
   const size_t zwl = ((br + 64) + 15) & ~15;
   return ng * ((size_t)br * KS + 4 * (size_t)(L + 2) * TM + zwl);
@@ -1224,7 +1369,8 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   const int64_t ncp = (int64_t)((n + TM - 1) / TM) * TM;
   size_t budget = (size_t)2 << 30;
   if (const char* e = getenv("DS_TCW_BUDGET_MB")) budget = (size_t)atol(e) << 20;
-  int64_t rows = (int64_t)(budget / ((size_t)ncp * plan->w_W * 4));
+  const int nc = plan->ncomp > 1 ? 2 : 1;
+  int64_t rows = (int64_t)(budget / ((size_t)ncp * plan->w_W * 4 * nc * nc));
   if (rows < 1) rows = 1;
   if (rows > nloc) rows = nloc > 0 ? nloc : 1;
   plan->w_rows = (int)rows;
@@ -1234,15 +1380,17 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   w->fb_cap = 1 << 16;
   w->sthreads = 64 * 128;
   w->tthreads = 148 * 3 * 256;
-  bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
-            cudaMalloc(&w->bbytes, (size_t)D8p * ncp) == cudaSuccess &&  // k_tcw_pack image
+  bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1) * nc) == cudaSuccess &&
+            cudaMalloc(&w->bbytes, (size_t)D8p * ncp * nc) == cudaSuccess &&  // k_tcw_pack image(s)
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
             cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
             cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
             cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
-            cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W) == cudaSuccess &&
-            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads * ((3 * (size_t)L + 24 + 7) & ~(size_t)7)) == cudaSuccess;
+            cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W * nc * nc) == cudaSuccess &&
+            cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads *
+                                         (nc == 2 ? ((8 * (size_t)L + 32 + 7) & ~(size_t)7)
+                                                  : ((3 * (size_t)L + 24 + 7) & ~(size_t)7))) == cudaSuccess;
   if (!ok) return DS_OOM;
   plan->enabled = 1;
   return DS_OK;
@@ -1319,6 +1467,23 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   return DS_OK;
 }
 
+// complex elements: the wide engine with the four component products
+int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device) {
+  memset(plan, 0, sizeof(*plan));
+  if (getenv("DS_DISABLE_TC") || getenv("DS_DISABLE_TC_COMPLEX") || p < 256) return DS_OK;
+  plan->p = p;
+  plan->L = (p + 31) / 32;
+  plan->D8p = ((4 * plan->L + KS - 1) / KS) * KS;
+  plan->nks = plan->D8p / KS;
+  int lg = 0;
+  while ((1 << lg) < plan->D8p) lg++;
+  plan->eps = 9 + lg;
+  plan->ncomp = 2;
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return tcw_plan_init(plan, n, nloc, p, device, maxsm);
+}
+
 void tc_plan_free(TcPlan* plan) {
   TcWork* w = (TcWork*)plan->work;
   if (!w) return;
@@ -1342,12 +1507,15 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   const int kstart = kmin & ~3;  // column tiles start 16-byte aligned (tile tensor map)
   const int ncols = n - kstart;
   if (nrows <= 0 || ncols <= 0) return DS_OK;
+  const int nc = plan->ncomp == 2 ? 2 : 1;  // complex: pivot buffer [c][l][k], exp [c][k], cls [c][k]
   const uint32_t* b_limbs = (const uint32_t*)pbuf;
-  const int32_t* b_exp = (const int32_t*)(pbuf + (size_t)4 * L * n);
-  const uint8_t* b_cls = (const uint8_t*)(pbuf + (size_t)4 * L * n + (size_t)4 * n);
+  const int32_t* b_exp = (const int32_t*)(pbuf + (size_t)4 * nc * L * n);
+  const uint8_t* b_cls = (const uint8_t*)(pbuf + (size_t)4 * nc * L * n + (size_t)4 * nc * n);
   const int W4 = plan->D8p / 4;
-  k_tc_bytes<<<(unsigned)(((int64_t)nrows * W4 + 255) / 256), 256, 0, s>>>(z_limbs + jl0, nloc, nrows, L, plan->D8p,
-                                                                          w->zbytes, w->zf);
+  for (int c = 0; c < nc; c++)
+    k_tc_bytes<<<(unsigned)(((int64_t)nrows * W4 + 255) / 256), 256, 0, s>>>(
+        z_limbs + (int64_t)c * L * nloc + jl0, nloc, nrows, L, plan->D8p, w->zbytes + (size_t)c * nloc * plan->D8p,
+        w->zf);
   if (!plan->wide)
     k_tc_bytes<<<(unsigned)(((int64_t)n * W4 + 255) / 256), 256, 0, s>>>(b_limbs, n, n, L, plan->D8p, w->bbytes, w->bf);
   cudaMemsetAsync(w->fb_count, 0, sizeof(int), s);
@@ -1356,7 +1524,7 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   a.c_lo = plan->c_lo; a.eps = plan->eps;
   a.nrows = nrows; a.ncols = ncols; a.kstart = kstart; a.kmin = kmin; a.skip_col = i; a.n = n; a.jl0 = jl0;
   a.zbytes = w->zbytes; a.bbytes = w->bbytes; a.zf = w->zf; a.bf = w->bf;
-  a.zexp = z_exp + jl0; a.zcls = z_cls + jl0; a.bexp = b_exp; a.bcls = b_cls;
+  a.zexp = z_exp + jl0; a.zcls = z_cls + jl0; a.bexp = b_exp; a.bcls = b_cls; a.zstride = nloc;
   a.a_limbs = a_limbs; a.a_exp = a_exp; a.a_cls = a_cls; a.a_count = a_count;
   a.status = status; a.step = i;
   a.fb_count = w->fb_count; a.fb_list = w->fb_list; a.fb_cap = w->fb_cap;
@@ -1369,7 +1537,10 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     const int ntile = (ncols + TM - 1) / TM;
     const int ncp = ntile * TM;
     const int64_t npieces = (int64_t)ntile * plan->nks * 2 * TM;
-    k_tcw_pack<<<(unsigned)((npieces + 255) / 256), 256, 0, s>>>(b_limbs, n, L, plan->nks, kstart, ntile, w->bbytes);
+    const size_t img = (size_t)plan->D8p * (((n + TM - 1) / TM) * TM);  // pack image per component
+    for (int c = 0; c < nc; c++)
+      k_tcw_pack<<<(unsigned)((npieces + 255) / 256), 256, 0, s>>>(b_limbs + (int64_t)c * L * n, n, L, plan->nks,
+                                                                   kstart, ntile, w->bbytes + c * img);
     for (int r0 = 0; r0 < nrows; r0 += plan->w_rows) {
       const int rc = nrows - r0 < plan->w_rows ? nrows - r0 : plan->w_rows;
       TwArgs tw;
@@ -1382,11 +1553,28 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
       tw.tprod = w->tprod;
       tw.pstride = (int64_t)rc * ncp;
       tw.status = status; tw.step = i;
-      k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tw);
-      k_tcw_finish<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch, w->tthreads);
-      *launches += 2;
+      if (nc == 1) {
+        k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tw);
+        k_tcw_finish<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch, w->tthreads);
+        *launches += 2;
+      } else {
+        // the four component products (c1, c2) = z_c1 * b_c2 into regions 2 c1 + c2
+        for (int c1 = 0; c1 < 2; c1++)
+          for (int c2 = 0; c2 < 2; c2++) {
+            TwArgs tc = tw;
+            tc.zbytes = w->zbytes + ((size_t)c1 * nloc + r0) * plan->D8p;
+            tc.apack = w->bbytes + c2 * img;
+            tc.tprod = w->tprod + (size_t)(2 * c1 + c2) * tw.pstride * tw.W;
+            k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tc);
+          }
+        k_tcw_finish_c<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch);
+        *launches += 5;
+      }
     }
-    k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
+    if (nc == 1)
+      k_tc_fallback<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
+    else
+      k_tc_fallback_c<<<64, 128, 0, s>>>(a, z_limbs, nloc, b_limbs, w->scratch, w->sthreads);
     *launches += 3;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DS_OK : DS_CUDA;

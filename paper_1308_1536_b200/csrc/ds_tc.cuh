@@ -12,11 +12,13 @@ struct TcPlan {
   size_t smem;
   // wide precision (pivot-row digits beyond TMEM): product kernel + finish kernel
   int wide;
+  int ncomp;           // 2: complex elements (wide engine, four component products)
   int w_kc, w_nst, w_brc, w_qlo, w_W, w_zwb, w_rows, w_rbr;
   void* work;
 };
 
 int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device);
+int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device);
 void tc_plan_free(TcPlan* plan);
 int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
                      int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,

@@ -87,3 +87,74 @@ def test_wide_16k_matches_dfma():
     assert np.array_equal(fin_f.exp, fin_w.exp)
     assert np.array_equal(fin_f.cls, fin_w.cls)
     assert results_digest(res_f, fin_f, n, p, steps) == results_digest(res_w, fin_w, n, p, steps)
+
+
+# ---------------------------------------------------------------- complex
+# Complex elements (mpc) on the wide engine: the four component products
+# z_c1 * b_c2 on the tensor cores, Re / Im = the exact two-product sums rounded
+# once (mpc_mul), then the per-component subtraction (mpc_sub).
+from test_gpu_parity import _random_matrix, device_eliminate  # noqa: E402
+from paper_1308_1536_b200 import mp  # noqa: E402
+from paper_1308_1536_b200.soa import SoA  # noqa: E402
+
+
+@pytest.mark.parametrize("n,p,special", [(24, 256, True), (30, 1024, False), (20, 2000, True), (14, 4096, True),
+                                          (12, 300, False)])
+def test_wide_complex_full_elimination_matches_oracle(n, p, special):
+    A = _random_matrix(n, p, 77 * n + p, "complex", special)
+    rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
+    rc_d, done_d, res_d, fin_d = device_eliminate(A, n, p, "complex")
+    assert done_o == done_d
+    assert not first_mismatch(fin_o, fin_d, p)
+    assert results_digest(res_o, fin_o, n, p, done_o) == results_digest(res_d, fin_d, n, p, done_d)
+
+
+def test_wide_complex_real_valued_and_imaginary():
+    """Zero imaginary (or real) parts: zero component products, exact zero sums and signed zeros."""
+    n, p = 16, 512
+    rs = mp.random_state(5)
+    with mp.context(precision=p):
+        vals = []
+        for i in range(n * n):
+            x = 2 * mp.mpfr_random(rs) - 1
+            m = i % 3
+            vals.append(mp.mpc(x, 0) if m == 0 else (mp.mpc(0, x) if m == 1 else mp.mpc(x, -x)))
+    A = SoA.from_scalars(vals, p, "complex")
+    rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
+    rc_d, done_d, res_d, fin_d = device_eliminate(A, n, p, "complex")
+    assert done_o == done_d
+    assert not first_mismatch(fin_o, fin_d, p)
+    assert results_digest(res_o, fin_o, n, p, done_o) == results_digest(res_d, fin_d, n, p, done_d)
+
+
+def test_wide_complex_matches_general_engine():
+    """Many column tiles and rows: bit-identical to the exact thread-level engine."""
+    import os
+    from paper_1308_1536_b200.engine import DeviceElimination
+    n, p, steps = 260, 1024, 5
+    A = random_uniform_soa(n, p, seed=31, kind="complex")
+
+    def run(env):
+        old = os.environ.get("DS_DISABLE_TC")
+        if env:
+            os.environ["DS_DISABLE_TC"] = "1"
+        try:
+            with DeviceElimination(n, p, "complex") as eng:
+                eng.load(A)
+                res = HostResults.alloc(n, 2, eng.L, True)
+                eng.run(True, True, 0, steps, res)
+                fin = A.copy()
+                eng.fetch(fin)
+                return res, fin, eng.counters()
+        finally:
+            if old is None:
+                os.environ.pop("DS_DISABLE_TC", None)
+            else:
+                os.environ["DS_DISABLE_TC"] = old
+    res_t, fin_t, cnt = run(False)
+    assert cnt["tc_engine"]
+    res_g, fin_g, _ = run(True)
+    assert np.array_equal(fin_t.cls, fin_g.cls)
+    assert np.array_equal(fin_t.exp, fin_g.exp)
+    assert np.array_equal(fin_t.limbs, fin_g.limbs)
+    assert results_digest(res_t, fin_t, n, p, steps) == results_digest(res_g, fin_g, n, p, steps)
