@@ -20,11 +20,12 @@ for arg in sys.argv[1:]:
     else:
         specs.append(arg)
 for spec in specs:
-    n, p = map(int, spec.split("@"))
-    A = random_uniform_soa(n, p, 1)
+    kind = "complex" if spec.endswith("c") else "real"  # 1000@4096c: complex elements
+    n, p = map(int, spec.rstrip("c").split("@"))
+    A = random_uniform_soa(n, p, 1, kind=kind)
     L = (p + 31) // 32
-    with DeviceElimination(n, p, "real") as eng:
-        res = HostResults.alloc(n, 1, L, True, pinned=True)
+    with DeviceElimination(n, p, kind) as eng:
+        res = HostResults.alloc(n, eng.ncomp, L, True, pinned=True)
         eng.load(A)
         eng.profile(True)
         torch.cuda.synchronize()
@@ -35,7 +36,7 @@ for spec in specs:
         eng.results(n, res)
         t2 = time.perf_counter()
         ms, nl, w = eng.profile_read()
-        work = n * (n - 1) ** 2 / 2 * L * L
-        print(f"n={n} p={p} series={series} done={done} device={t1 - t0:.3f}s results-D2H={t2 - t1:.3f}s "
+        work = n * (n - 1) ** 2 / 2 * L * L * (4 if kind == "complex" else 1)
+        print(f"n={n} p={p} kind={kind} series={series} done={done} device={t1 - t0:.3f}s results-D2H={t2 - t1:.3f}s "
               f"limb-MAC/s={work / (t1 - t0):.3e} update={ms / 1e3:.3f}s ({w / (ms * 1e-3):.3e}/s over {nl} launches) "
               f"launches={eng.launches()} {eng.counters()}", flush=True)
