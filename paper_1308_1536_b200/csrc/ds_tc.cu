@@ -1384,9 +1384,9 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
             cudaMalloc(&w->bbytes, (size_t)D8p * ncp * nc) == cudaSuccess &&  // k_tcw_pack image(s)
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
-            cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
-            cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
-            cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
+            cudaMalloc(&w->fb_count, 2 * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&w->fb_list, 2 * sizeof(int2) * w->fb_cap) == cudaSuccess &&
+            cudaMalloc(&w->scratch, 2 * sizeof(uint32_t) * w->sthreads * (14 * (size_t)L + 96)) == cudaSuccess &&
             cudaMalloc(&w->tprod, sizeof(uint32_t) * (size_t)rows * ncp * plan->w_W * nc * nc) == cudaSuccess &&
             cudaMalloc(&w->tscratch, sizeof(uint32_t) * (size_t)w->tthreads *
                                          (nc == 2 ? ((8 * (size_t)L + 32 + 7) & ~(size_t)7)
@@ -1458,8 +1458,8 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
             cudaMalloc(&w->bbytes, (size_t)plan->D8p * n) == cudaSuccess &&
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
-            cudaMalloc(&w->fb_count, sizeof(int)) == cudaSuccess &&
-            cudaMalloc(&w->fb_list, sizeof(int2) * w->fb_cap) == cudaSuccess &&
+            cudaMalloc(&w->fb_count, 2 * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&w->fb_list, 2 * sizeof(int2) * w->fb_cap) == cudaSuccess &&
             cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)plan->L + 96)) == cudaSuccess;
   plan->work = w;
   if (!ok) return DS_OOM;
@@ -1518,7 +1518,9 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
         w->zf);
   if (!plan->wide)
     k_tc_bytes<<<(unsigned)(((int64_t)n * W4 + 255) / 256), 256, 0, s>>>(b_limbs, n, n, L, plan->D8p, w->bbytes, w->bf);
-  cudaMemsetAsync(w->fb_count, 0, sizeof(int), s);
+  // fallback lists: [0] the main launch, [1] the lookahead tile (its fallbacks must
+  // be applied before the next step's multipliers read column i + 1)
+  cudaMemsetAsync(w->fb_count, 0, 2 * sizeof(int), s);
   TcArgs a;
   a.p = plan->p; a.L = L; a.zb = 32 * L - plan->p; a.D8p = plan->D8p; a.nks = plan->nks; a.ntiles = plan->ntiles;
   a.c_lo = plan->c_lo; a.eps = plan->eps;
@@ -1610,7 +1612,11 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     aa.tile0 = ts;
     aa.tskip = -1;
     aa.rbr = RBR_LA;  // short CTAs: the next step's multipliers wait on this tile only
+    aa.fb_count = w->fb_count + 1;
+    aa.fb_list = w->fb_list + w->fb_cap;
     launch_update(plan->ng, dim3(1, (nrows + RBR_LA - 1) / RBR_LA), plan->smem, la, aa, w->amap);
+    k_tc_fallback<<<64, 128, 0, la>>>(aa, z_limbs, nloc, b_limbs, w->scratch + w->sthreads * (14 * (size_t)L + 96),
+                                     w->sthreads);
     CK_TC(cudaEventRecord(ev_a, la));
     TcArgs ab = a;
     ab.tile0 = 0;

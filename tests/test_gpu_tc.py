@@ -188,3 +188,47 @@ def test_device_resume_from_checkpoint(tmp_path):
             assert np.array_equal(a.limbs[:, :, sl], b.limbs[:, :, sl]) and np.array_equal(a.exp[:, sl], b.exp[:, sl])
             assert np.array_equal(a.cls[:, sl], b.cls[:, sl])
     assert np.array_equal(res_r.dets.limbs[:, :, stop:], res_f.dets.limbs[:, :, stop:])
+
+
+def test_lookahead_tile_fallbacks_applied_before_next_multipliers():
+    """Column 1 (the lookahead tile at step 0) full of undecidable short products:
+    z_j = 1 + 2^(1-p), b_1 = 1.5 makes z_j b_1 an exact tie at p bits, which the
+    tensor-core kernel hands to the exact fallback.  Step 1's multipliers (run on the
+    lookahead stream) read column 1, so those fallbacks must land first."""
+    from paper_1308_1536_b200 import mp
+    from paper_1308_1536_b200.soa import SoA
+    n, p, steps = 300, 1024, 3
+    rs = mp.random_state(12)
+    with mp.context(precision=p):
+        one = mp.mpfr(1)
+        zt = one + mp.mul_2exp(one, 1 - p)
+        vals = []
+        for j in range(n):
+            for k in range(n):
+                if j == 0 and k == 0:
+                    v = one
+                elif j == 0 and k == 1:
+                    v = mp.mpfr(1.5)
+                elif k == 0 and j % 3 != 2:
+                    v = zt
+                else:
+                    v = 2 * mp.mpfr_random(rs) - 1
+                vals.append(v)
+    A = SoA.from_scalars(vals, p, "real")
+    ref = oracle.OracleRank(n, p, "real")
+    ref.load(A)
+    res_o = HostResults.alloc(n, 1, ref.L, True)
+    ref.run(True, True, 0, steps, res_o)
+    fin_o = A.copy()
+    ref.fetch(fin_o)
+    with DeviceElimination(n, p, "real") as eng:
+        eng.load(A)
+        res_d = HostResults.alloc(n, 1, eng.L, True)
+        eng.run(True, True, 0, steps, res_d)
+        fin_d = A.copy()
+        eng.fetch(fin_d)
+        cnt = eng.counters()
+    assert cnt["tc_fallback_elements"] > 0  # the construction does reach the fallback
+    mism = first_mismatch(fin_o, fin_d, p)
+    assert not mism, mism
+    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
