@@ -74,6 +74,7 @@ struct ds_ctx {
   uint32_t* scratch;
   int64_t scratch_threads;
   int64_t scratch_words;  // words per thread
+  uint32_t* scratch_side; // complex tensor-core runs: general kernels on the side stream (det chain, minors)
   // device snapshot of the local rows (ds_snapshot)
   uint32_t* snap_limbs;
   int32_t* snap_exp;
@@ -291,6 +292,22 @@ __global__ void k_pivot(KArgs k, int i) {
   if (k.kind == DS_KIND_COMPLEX) set_val(d1, r1, k.L);
 }
 
+// det_i = RN(det_{i-1} * piv_i) (elim.py:215) by one thread, on the side stream
+// (complex tensor-core runs); from_cur: the ds_set_det seed in cur is det_{i-1}
+__global__ void k_det_step(KArgs k, int i, int from_cur) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
+  Val q0 = from_cur ? val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0)
+                    : val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i - 1);
+  Val q1 = from_cur ? val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0)
+                    : val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i - 1);
+  Val p0 = val_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, 0, k.L, i);
+  Val p1 = val_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, k.ncomp - 1, k.L, i);
+  Out d0 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
+  Out d1 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
+  if (!g_mul(d0, d1, q0, q1, p0, p1, k.kind, k.L, k.p, thread_scratch(k, 0))) atomicAdd(&k.status[2], 1);
+}
+
 // first local row index with global row > i
 __host__ __device__ static inline int first_local_after(int i, int rank, int world) {
   int first = i + 1;
@@ -324,6 +341,89 @@ __global__ void k_mult(KArgs k, int i, int jl0) {
       Out ao1 = out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx);
       neg_copy(ao1, zv1, k.L);
     }
+  }
+}
+
+// complex (tensor-core runs): one thread per (row, component) for the division,
+// twice the parallelism of k_mult; a_ji <- -z_j after all rows (k_neg_z), since
+// both components of a_ji are read by both threads
+__global__ void k_mult_c2(KArgs k, int i, int jl0) {
+  if (k.status[0] >= 0) return;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int nrows = k.nloc - jl0;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  Val b0 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i);
+  Val b1 = val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, i);
+  for (int64_t t = tid; t < 2 * (int64_t)nrows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t & 1);
+    int64_t jl = jl0 + (t >> 1);
+    int64_t idx = jl * k.n + i;
+    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
+    Val a1 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx);
+    Out z = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, c, k.L, jl);
+    if (!cdiv_part(z.m, z.e, z.c, a0, a1, b0, b1, c == 1, k.L, k.p, thread_scratch(k, tid),
+                   (unsigned int*)&k.status[3]))
+      atomicAdd(&k.status[2], 1);
+  }
+}
+
+__global__ void k_neg_z(KArgs k, int i, int jl0) {
+  if (k.status[0] >= 0) return;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int nrows = k.nloc - jl0;
+  for (int64_t t = tid; t < 2 * (int64_t)nrows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t & 1);
+    int64_t jl = jl0 + (t >> 1);
+    Val zv = val_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, c, k.L, jl);
+    neg_copy(out_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, c, k.L, jl * k.n + i), zv, k.L);
+  }
+}
+
+// complex minors, one thread per (entry, component): signed_k = RN(det_i * L_mk)
+// (cmul_part per component), normalized = RN(signed_k / signed_0) (cdiv_part)
+__global__ void k_emit_signed_c2(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int m = i + 2;
+  int64_t jl = (i + 1) / k.world;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Val d0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
+  Val d1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 1, k.L, i);
+  for (int64_t t = tid; t < 2 * (int64_t)m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t & 1);
+    const int64_t kk = t >> 1;
+    int64_t oidx = jl * k.n + kk;
+    Out so = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, c, k.L, oidx);
+    if (kk == m - 1) {
+      set_val(so, c == 0 ? d0 : d1, k.L);
+      continue;
+    }
+    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, oidx);
+    Val a1 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, oidx);
+    bool ok = c == 0 ? cmul_part(so.m, so.e, so.c, d0, a0, d1, a1, true, k.L, k.p, thread_scratch(k, tid))
+                     : cmul_part(so.m, so.e, so.c, d0, a1, d1, a0, false, k.L, k.p, thread_scratch(k, tid));
+    if (!ok) atomicAdd(&k.status[2], 1);
+  }
+}
+
+__global__ void k_emit_norm_c2(KArgs k, int i) {
+  if (k.status[0] >= 0) return;
+  int m = i + 2;
+  int64_t jl = (i + 1) / k.world;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
+  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 1, k.L, jl * k.n);
+  bool lead_zero = is_zero_cls(l0.c) && is_zero_cls(l1.c);
+  if (tid == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
+  if (lead_zero) return;
+  for (int64_t t = tid; t < 2 * (int64_t)m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t & 1);
+    int64_t idx = jl * k.n + (t >> 1);
+    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
+    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 1, k.L, idx);
+    Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, c, k.L, idx);
+    if (!cdiv_part(o.m, o.e, o.c, s0, s1, l0, l1, c == 1, k.L, k.p, thread_scratch(k, tid),
+                   (unsigned int*)&k.status[3]))
+      atomicAdd(&k.status[2], 1);
   }
 }
 
@@ -389,8 +489,8 @@ __global__ void k_emit_signed(KArgs k, int i) {
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  Val d0 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0);
-  Val d1 = val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, k.ncomp - 1, k.L, 0);
+  Val d0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);  // det_i (k_pivot / k_det_step)
+  Val d1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
   for (int64_t kk = tid; kk < m; kk += (int64_t)gridDim.x * blockDim.x) {
     int64_t oidx = jl * k.n + kk;
     Out s0 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, oidx);
@@ -698,6 +798,7 @@ void ds_destroy(ds_ctx* ctx) {
   update_plan_free(&ctx->plan);
   tc_plan_free(&ctx->tc);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
+  if (ctx->scratch_side) cudaFree(ctx->scratch_side);
   if (ctx->ws_dx) cudaFree(ctx->ws_dx);
   if (ctx->ws_dy) cudaFree(ctx->ws_dy);
   if (ctx->ws_ex) cudaFree(ctx->ws_ex);
@@ -816,6 +917,12 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
       ctx->err = "complex tensor-core update plan: device allocation or attribute failed";
       ds_destroy(ctx);
       return rc;
+    }
+    if (ctx->tc.enabled &&
+        cudaMalloc(&ctx->scratch_side, sizeof(uint32_t) * ctx->scratch_threads * ctx->scratch_words) != cudaSuccess) {
+      ctx->scratch_side = nullptr;
+      ds_destroy(ctx);
+      return DS_OOM;
     }
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -984,8 +1091,23 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     set_wdiv_attrs(maxsm);
   }
   PB pb = pb_view(ctx->pbuf, n, L, ctx->ncomp);
+  // complex on the tensor cores: det chain and minors (general kernels) on the side
+  // stream with their own scratch, off the update's critical path
+  const bool cxf = ctx->kind == DS_KIND_COMPLEX && ctx->tc.enabled && ctx->scratch_side && !force_general();
+  KArgs ks = k;
+  ks.scratch = ctx->scratch_side;
   // ---- pivot: zero test, pivots[i], det chain (elim.py:209-215)
-  if (fast) {
+  if (cxf) {
+    int first = ctx->host_have_det ? 0 : 1;
+    k_pivot_lite<<<1, 128, 0, s>>>(k, i, first);
+    ctx->launches++;
+    if (!first) {
+      CK(cudaEventRecord(ctx->ev_piv, s));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_piv, 0));
+      k_det_step<<<1, 32, 0, ctx->side>>>(ks, i, ctx->det_from_cur);
+      ctx->launches++;
+    }
+  } else if (fast) {
     int first = ctx->host_have_det ? 0 : 1;
     k_pivot_lite<<<1, 128, 0, s>>>(k, i, first);
     ctx->launches++;
@@ -1031,6 +1153,10 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
       int blocks = (nrows + wpb - 1) / wpb;
       size_t smem = (size_t)wpb * wwords * 4;
       WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0, nullptr);
+    } else if (cxf) {
+      k_mult_c2<<<grid_for(ctx, 2 * (int64_t)nrows, 64), 64, 0, s>>>(k, i, jl0);
+      k_neg_z<<<grid_for(ctx, 2 * (int64_t)nrows, 64), 64, 0, s>>>(k, i, jl0);
+      ctx->launches++;
     } else {
       k_mult<<<grid_for(ctx, nrows, 64), 64, 0, s>>>(k, i, jl0);
     }
@@ -1120,6 +1246,13 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         } else {
           k_emit_norm<<<grid_for(ctx, m, 64), 64, 0, ss>>>(k, i);
         }
+        ctx->launches += 2;
+      } else if (cxf) {
+        cudaStream_t ss = ctx->side;
+        CK(cudaEventRecord(ctx->ev_upd, s));
+        CK(cudaStreamWaitEvent(ss, ctx->ev_upd, 0));
+        k_emit_signed_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
+        k_emit_norm_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
         ctx->launches += 2;
       } else {
         k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);

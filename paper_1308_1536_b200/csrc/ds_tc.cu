@@ -1460,7 +1460,7 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
             cudaMalloc(&w->bf, sizeof(double) * n) == cudaSuccess &&
             cudaMalloc(&w->fb_count, 2 * sizeof(int)) == cudaSuccess &&
             cudaMalloc(&w->fb_list, 2 * sizeof(int2) * w->fb_cap) == cudaSuccess &&
-            cudaMalloc(&w->scratch, sizeof(uint32_t) * w->sthreads * (14 * (size_t)plan->L + 96)) == cudaSuccess;
+            cudaMalloc(&w->scratch, 2 * sizeof(uint32_t) * w->sthreads * (14 * (size_t)plan->L + 96)) == cudaSuccess;
   plan->work = w;
   if (!ok) return DS_OOM;
   plan->enabled = 1;
