@@ -1016,6 +1016,7 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     }
     const bool sub = na != nT;
     const int n2 = L + (int)(d >> 5) + 2;
+    constexpr int FB = 8;  // limbs per batch (16 measured the same)
     // S2 = X 2^d +- Y (X the larger operand) into scratch, 8 limbs per batch so
     // each thread keeps ~16 independent loads in flight
     const int64_t lwT = offT >> 5;  // T(i) = low-masked funnel(S[lwT + i], S[lwT + i + 1], shT) + carry
@@ -1037,17 +1038,17 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     uint32_t cb2 = 0;
     uint32_t tprev = 0;  // X = T: T(q0 + lwX) carried between batches
     if (!xa) tprev = tval(lwX, __funnelshift_r(sget(lwT + lwX), sget(lwT + lwX + 1), shT));
-    for (int q0 = 0; q0 < n2; q0 += 8) {
+    for (int q0 = 0; q0 < n2; q0 += FB) {
       const int64_t ti0 = xa ? q0 : q0 + lwX + 1;  // first new T index of the batch
-      uint32_t sv[9], av[9], tv[8], s2[8];
+      uint32_t sv[FB + 1], av[FB + 1], tv[FB], s2[FB];
 #pragma unroll
-      for (int u = 0; u < 9; u++) sv[u] = sget(lwT + ti0 + u);
+      for (int u = 0; u < FB + 1; u++) sv[u] = sget(lwT + ti0 + u);
 #pragma unroll
-      for (int u = 0; u < 9; u++) av[u] = xa ? aget(q0 + lwX + u) : aget(q0 + u);
+      for (int u = 0; u < FB + 1; u++) av[u] = xa ? aget(q0 + lwX + u) : aget(q0 + u);
 #pragma unroll
-      for (int u = 0; u < 8; u++) tv[u] = tval(ti0 + u, __funnelshift_r(sv[u], sv[u + 1], shT));
+      for (int u = 0; u < FB; u++) tv[u] = tval(ti0 + u, __funnelshift_r(sv[u], sv[u + 1], shT));
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < FB; u++) {
         uint32_t x, y;
         if (xa) {
           x = __funnelshift_r(av[u], av[u + 1], shX);
@@ -1066,9 +1067,9 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
         }
         s2[u] = (uint32_t)t;
       }
-      tprev = tv[7];
-      *(uint4*)(row + q0) = make_uint4(s2[0], s2[1], s2[2], s2[3]);
-      *(uint4*)(row + q0 + 4) = make_uint4(s2[4], s2[5], s2[6], s2[7]);
+      tprev = tv[FB - 1];
+#pragma unroll
+      for (int u = 0; u < FB; u += 4) *(uint4*)(row + q0 + u) = make_uint4(s2[u], s2[u + 1], s2[u + 2], s2[u + 3]);
     }
     // round S2 (n2 limbs, nonzero) to p bits into a's limbs
     const ds::CPtr S2{tmp.p, tmp.s};
@@ -1091,15 +1092,15 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     const int64_t lw2 = off2 >> 5;
     const int sh2 = (int)(off2 & 31);
     uint32_t rc2 = 0;
-    for (int l0 = 0; l0 < L; l0 += 8) {
-      uint32_t v[9];
+    for (int l0 = 0; l0 < L; l0 += FB) {
+      uint32_t v[FB + 1];
 #pragma unroll
-      for (int u = 0; u < 9; u++) {
+      for (int u = 0; u < FB + 1; u++) {
         const int64_t q = lw2 + l0 + u;
         v[u] = (q >= 0 && q < n2) ? S2[q] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < FB; u++) {
         const int l = l0 + u;
         if (l < L) {
           const uint32_t raw = __funnelshift_r(v[u], v[u + 1], sh2);
@@ -1617,6 +1618,7 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     launch_update(plan->ng, dim3(1, (nrows + RBR_LA - 1) / RBR_LA), plan->smem, la, aa, w->amap);
     k_tc_fallback<<<64, 128, 0, la>>>(aa, z_limbs, nloc, b_limbs, w->scratch + w->sthreads * (14 * (size_t)L + 96),
                                      w->sthreads);
+    *launches += 1;
     CK_TC(cudaEventRecord(ev_a, la));
     TcArgs ab = a;
     ab.tile0 = 0;
