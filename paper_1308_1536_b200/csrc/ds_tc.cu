@@ -1038,33 +1038,41 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     uint32_t cb2 = 0;
     uint32_t tprev = 0;  // X = T: T(q0 + lwX) carried between batches
     if (!xa) tprev = tval(lwX, __funnelshift_r(sget(lwT + lwX), sget(lwT + lwX + 1), shT));
+    // X - Y as X + ~Y + 1: one branch-free carry chain for both signs
+    const uint32_t ym = sub ? 0xffffffffu : 0u;
+    cb2 = sub ? 1u : 0u;
     for (int q0 = 0; q0 < n2; q0 += FB) {
       const int64_t ti0 = xa ? q0 : q0 + lwX + 1;  // first new T index of the batch
+      const int64_t ai0 = xa ? q0 + lwX : q0;      // first a index of the batch
       uint32_t sv[FB + 1], av[FB + 1], tv[FB], s2[FB];
+      if (lwT + ti0 >= 0 && lwT + ti0 + FB < W && ti0 > zl && ti0 + FB <= L && ai0 >= 0 && ai0 + FB < L) {
+        // interior batch: no bounds, no low mask
 #pragma unroll
-      for (int u = 0; u < FB + 1; u++) sv[u] = sget(lwT + ti0 + u);
+        for (int u = 0; u < FB + 1; u++) sv[u] = S[lwT + ti0 + u];
 #pragma unroll
-      for (int u = 0; u < FB + 1; u++) av[u] = xa ? aget(q0 + lwX + u) : aget(q0 + u);
+        for (int u = 0; u < FB + 1; u++) av[u] = am[ai0 + u];
 #pragma unroll
-      for (int u = 0; u < FB; u++) tv[u] = tval(ti0 + u, __funnelshift_r(sv[u], sv[u + 1], shT));
+        for (int u = 0; u < FB; u++) {
+          const uint64_t t = (uint64_t)__funnelshift_r(sv[u], sv[u + 1], shT) + tcar;
+          tcar = (uint32_t)(t >> 32);
+          tv[u] = (uint32_t)t;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < FB + 1; u++) sv[u] = sget(lwT + ti0 + u);
+#pragma unroll
+        for (int u = 0; u < FB + 1; u++) av[u] = aget(ai0 + u);
+#pragma unroll
+        for (int u = 0; u < FB; u++) tv[u] = tval(ti0 + u, __funnelshift_r(sv[u], sv[u + 1], shT));
+      }
 #pragma unroll
       for (int u = 0; u < FB; u++) {
-        uint32_t x, y;
-        if (xa) {
-          x = __funnelshift_r(av[u], av[u + 1], shX);
-          y = tv[u];
-        } else {
-          x = __funnelshift_r(u == 0 ? tprev : tv[u - 1], tv[u], shX);
-          y = av[u];
-        }
-        uint64_t t;
-        if (sub) {
-          t = (uint64_t)x - y - cb2;
-          cb2 = (uint32_t)(t >> 63);
-        } else {
-          t = (uint64_t)x + y + cb2;
-          cb2 = (uint32_t)(t >> 32);
-        }
+        const uint32_t lo = xa ? av[u] : (u == 0 ? tprev : tv[u - 1]);
+        const uint32_t hi = xa ? av[u + 1] : tv[u];
+        const uint32_t x = __funnelshift_r(lo, hi, shX);
+        const uint32_t y = (xa ? tv[u] : av[u]) ^ ym;
+        const uint64_t t = (uint64_t)x + y + cb2;
+        cb2 = (uint32_t)(t >> 32);
         s2[u] = (uint32_t)t;
       }
       tprev = tv[FB - 1];
@@ -1094,6 +1102,17 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
     uint32_t rc2 = 0;
     for (int l0 = 0; l0 < L; l0 += FB) {
       uint32_t v[FB + 1];
+      if (lw2 + l0 >= 0 && lw2 + l0 + FB < n2 && l0 > zl && l0 + FB <= L) {  // interior batch
+#pragma unroll
+        for (int u = 0; u < FB + 1; u++) v[u] = S2[lw2 + l0 + u];
+#pragma unroll
+        for (int u = 0; u < FB; u++) {
+          const uint64_t t = (uint64_t)__funnelshift_r(v[u], v[u + 1], sh2) + rc2;
+          rc2 = (uint32_t)(t >> 32);
+          out[l0 + u] = (uint32_t)t;
+        }
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < FB + 1; u++) {
         const int64_t q = lw2 + l0 + u;
