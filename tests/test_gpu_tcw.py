@@ -127,8 +127,10 @@ def test_wide_complex_real_valued_and_imaginary():
     assert results_digest(res_o, fin_o, n, p, done_o) == results_digest(res_d, fin_d, n, p, done_d)
 
 
-def test_wide_complex_matches_general_engine():
-    """Many column tiles and rows: bit-identical to the exact thread-level engine."""
+@pytest.mark.parametrize("budget_mb", [None, "16"])
+def test_wide_complex_matches_general_engine(budget_mb):
+    """Many column tiles and rows (and, with a small product buffer, several row
+    chunks): bit-identical to the exact thread-level engine."""
     import os
     from paper_1308_1536_b200.engine import DeviceElimination
     n, p, steps = 260, 1024, 5
@@ -136,8 +138,11 @@ def test_wide_complex_matches_general_engine():
 
     def run(env):
         old = os.environ.get("DS_DISABLE_TC")
+        oldb = os.environ.get("DS_TCW_BUDGET_MB")
         if env:
             os.environ["DS_DISABLE_TC"] = "1"
+        elif budget_mb:
+            os.environ["DS_TCW_BUDGET_MB"] = budget_mb
         try:
             with DeviceElimination(n, p, "complex") as eng:
                 eng.load(A)
@@ -151,6 +156,10 @@ def test_wide_complex_matches_general_engine():
                 os.environ.pop("DS_DISABLE_TC", None)
             else:
                 os.environ["DS_DISABLE_TC"] = old
+            if oldb is None:
+                os.environ.pop("DS_TCW_BUDGET_MB", None)
+            else:
+                os.environ["DS_TCW_BUDGET_MB"] = oldb
     res_t, fin_t, cnt = run(False)
     assert cnt["tc_engine"]
     res_g, fin_g, _ = run(True)
