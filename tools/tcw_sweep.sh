@@ -1,5 +1,7 @@
+# wide product kernel tuning sweep (K steps per stage, stages, rows per CTA) at one size
 mkdir -p gpurun_out
-for cfg in "KC=8 NST=3 RBR=2" "KC=4 NST=6 RBR=2" "KC=8 NST=4 RBR=2" "KC=16 NST=2 RBR=2" "KC=8 NST=3 RBR=8" "KC=4 NST=4 RBR=4"; do
+SPEC=${1:-600@32768}
+for cfg in "KC=8 NST=3 RBR=2" "KC=16 NST=2 RBR=2" "KC=16 NST=2 RBR=1" "KC=20 NST=2 RBR=2" "KC=12 NST=3 RBR=2"; do
   set -- $cfg
-  env DS_TCW_${1} DS_TCW_${2} DS_TCW_${3} timeout 300 python tools/probe_perf.py --no-series 600@16384 2>&1 | grep "^n=" | sed "s/^/$cfg /" | cut -c1-200
+  env DS_TCW_${1} DS_TCW_${2} DS_TCW_${3} timeout 300 python tools/probe_perf.py --no-series $SPEC 2>&1 | grep "^n=" | sed "s/^/$cfg /" | cut -c1-160
 done
