@@ -113,6 +113,17 @@ int ds_fetch(ds_ctx *ctx, ds_soa *host_matrix);
 int ds_run(ds_ctx *ctx, int collect_minors, int series, int start_step, int stop_step,
            ds_results *res, int *steps_done);
 
+/* pivot_mode of elim.eliminate (elim.py:159, 184-208): mode 0 = "none",
+ * mode 1 = "partial" -- before each step of ds_run, the first row j >= i of
+ * maximal |a_ji| (exact magnitude comparison, elim.py:205) is swapped with
+ * row i on the device (elim.py:206-207).  Serial real engine only (world 1,
+ * kind real; complex abs() is a rounded modulus); ds_run rejects
+ * collect_minors with DS_INVALID (elim.py:186-187). */
+int ds_set_pivot_mode(ds_ctx *ctx, int mode);
+/* swapped[i] = 1 when step i swapped rows (the det sign flips, elim.py:207,
+ * 216), for steps [0, upto_step).  Synchronises the context stream. */
+int ds_swaps_fetch(ds_ctx *ctx, int upto_step, uint8_t *swapped);
+
 /* --- sharded engine building blocks (world > 1; the caller broadcasts) ---
  * Per step i: the owner of row i calls ds_pivot_stage (copies the
  * unnormalized row i into the pivot buffer: parexec.py:307-309), every rank

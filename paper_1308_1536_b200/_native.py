@@ -26,7 +26,7 @@ EXPORTS = ("ds_version", "ds_create", "ds_destroy", "ds_load", "ds_fetch", "ds_r
            "ds_pivot_stage", "ds_step", "ds_status", "ds_results_fetch", "ds_set_det", "ds_stream",
            "ds_launch_count", "ds_last_error", "ds_scalar_op", "ds_set_stream", "ds_use_pivot_buffer",
            "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters", "ds_lookahead_enable", "ds_lookahead_stream",
-           "ds_lookahead_pivot", "ds_lookahead_mult")
+           "ds_lookahead_pivot", "ds_lookahead_mult", "ds_set_pivot_mode", "ds_swaps_fetch")
 
 
 class ds_results(ctypes.Structure):
@@ -74,6 +74,8 @@ def load_library(path: str = LIB_PATH):
         "ds_lookahead_stream": (I, [VP, P(VP)]),
         "ds_lookahead_pivot": (I, [VP, I, VP]),
         "ds_lookahead_mult": (I, [VP, I, VP]),
+        "ds_set_pivot_mode": (I, [VP, I]),
+        "ds_swaps_fetch": (I, [VP, I, P(ctypes.c_uint8)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -91,6 +91,10 @@ struct ds_ctx {
   int64_t launches;
   int host_have_det;   // a det chain value exists (first step sets det = piv)
   int det_from_cur;    // next det product reads the ds_set_det seed in `cur`
+  // pivot_mode="partial" (elim.py:204-208): per-step row swap flags [n] and the selected row
+  int pivot_partial;
+  uint8_t* swaps;
+  int32_t* pbest;
   std::string err;
 };
 
@@ -247,6 +251,83 @@ __global__ void k_stage(KArgs k, int i) {
       pb.exp[(int64_t)c * k.n + col] = k.a_exp[(int64_t)c * k.a_count + src];
     else
       pb.cls[(int64_t)c * k.n + col] = k.a_cls[(int64_t)c * k.a_count + src];
+  }
+}
+
+// ---- pivot_mode="partial" (elim.py:204-208, det-only; world 1, real) ----
+// |a_x| < |a_y| for two real matrix elements (abs() comparison of elim.py:205,
+// exact): zeros are the smallest magnitude, then exponent, then the mantissa
+// limbs from the most significant (limb L-1) down
+__device__ __forceinline__ bool abs_less(const KArgs& k, int64_t ix, int64_t iy) {
+  if (is_zero_cls(k.a_cls[iy])) return false;
+  if (is_zero_cls(k.a_cls[ix])) return true;
+  int32_t ex = k.a_exp[ix], ey = k.a_exp[iy];
+  if (ex != ey) return ex < ey;
+  for (int l = k.L - 1; l >= 0; l--) {
+    uint32_t x = k.a_limbs[(int64_t)l * k.a_count + ix], y = k.a_limbs[(int64_t)l * k.a_count + iy];
+    if (x != y) return x < y;
+  }
+  return false;
+}
+
+// best = the first row j >= i of maximal |a_ji| (Python max() keeps the first
+// maximum); one block, strided scan then a tree reduction with index tie-break
+__global__ void k_pivot_select(KArgs k, int i, int32_t* best, uint8_t* swaps) {
+  __shared__ int cand[1024];
+  const int t = threadIdx.x;
+  if (k.status[0] >= 0) {  // an earlier step aborted: nothing moves
+    if (t == 0) { *best = i; swaps[i] = 0; }
+    return;
+  }
+  int b = -1;
+  for (int j = i + t; j < k.n; j += blockDim.x)
+    if (b < 0 || abs_less(k, (int64_t)b * k.n + i, (int64_t)j * k.n + i)) b = j;
+  cand[t] = b;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (t < h) {
+      int x = cand[t], y = cand[t + h];
+      if (y >= 0) {
+        bool take = x < 0;
+        if (!take) {
+          int64_t ix = (int64_t)x * k.n + i, iy = (int64_t)y * k.n + i;
+          take = abs_less(k, ix, iy) || (y < x && !abs_less(k, iy, ix));
+        }
+        if (take) cand[t] = y;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    int bb = cand[0] < 0 ? i : cand[0];
+    *best = bb;
+    swaps[i] = bb != i;
+  }
+}
+
+// rows[i], rows[best] = rows[best], rows[i] (elim.py:206-207): every limb plane,
+// exponent and class of both full-width rows, coalesced along the rows
+__global__ void k_swap_rows(KArgs k, int i, const int32_t* best) {
+  const int b = *best;
+  if (b == i) return;
+  const int64_t planes = (int64_t)k.ncomp * (k.L + 2);
+  const int64_t tot = planes * k.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(t % k.n);
+    const int64_t pl = t / k.n;
+    const int c = (int)(pl / (k.L + 2));
+    const int l = (int)(pl % (k.L + 2));
+    const int64_t x = (int64_t)i * k.n + col, y = (int64_t)b * k.n + col;
+    if (l < k.L) {
+      uint32_t* a = k.a_limbs + ((int64_t)c * k.L + l) * k.a_count;
+      uint32_t u = a[x]; a[x] = a[y]; a[y] = u;
+    } else if (l == k.L) {
+      int32_t* a = k.a_exp + (int64_t)c * k.a_count;
+      int32_t u = a[x]; a[x] = a[y]; a[y] = u;
+    } else {
+      uint8_t* a = k.a_cls + (int64_t)c * k.a_count;
+      uint8_t u = a[x]; a[x] = a[y]; a[y] = u;
+    }
   }
 }
 
@@ -785,7 +866,7 @@ void ds_destroy(ds_ctx* ctx) {
   void* ptrs[] = {ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->own_pbuf, ctx->zb_limbs[0], ctx->zb_exp[0], ctx->zb_cls[0],
                   ctx->piv_limbs, ctx->det_limbs, ctx->cur_limbs, ctx->piv_exp, ctx->det_exp, ctx->cur_exp,
                   ctx->piv_cls, ctx->det_cls, ctx->cur_cls, ctx->sig_limbs, ctx->nrm_limbs, ctx->sig_exp,
-                  ctx->nrm_exp, ctx->sig_cls, ctx->nrm_cls, ctx->row_flags, ctx->status, ctx->scratch};
+                  ctx->nrm_exp, ctx->sig_cls, ctx->nrm_cls, ctx->row_flags, ctx->status, ctx->scratch, ctx->swaps, ctx->pbest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* zb1[] = {ctx->zb_limbs[1], ctx->zb_exp[1], ctx->zb_cls[1]};
@@ -961,6 +1042,7 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
   ctx->la_step = -1;
   ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
+  if (ctx->swaps) CK(cudaMemsetAsync(ctx->swaps, 0, n, ctx->stream));
   int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1516,10 +1598,44 @@ static int results_fetch_from(ds_ctx* ctx, int upto, ds_results* r, int minors_f
 
 int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) { return results_fetch_from(ctx, upto, r, 0); }
 
+int ds_set_pivot_mode(ds_ctx* ctx, int mode) {
+  if (mode != 0 && mode != 1) return DS_INVALID;
+  if (mode == 1 && (ctx->world != 1 || ctx->kind != DS_KIND_REAL)) {
+    ctx->err = "pivot_mode='partial' runs on the serial real engine only (world 1, kind real)";
+    return DS_INVALID;
+  }
+  CK(cudaSetDevice(ctx->device));
+  if (mode == 1 && !ctx->swaps) {
+    int rc;
+    if ((rc = dmalloc(ctx, &ctx->swaps, (size_t)ctx->n)) != DS_OK) return rc;
+    if ((rc = dmalloc(ctx, &ctx->pbest, 1)) != DS_OK) return rc;
+    CK(cudaMemsetAsync(ctx->swaps, 0, ctx->n, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->pivot_partial = mode;
+  return DS_OK;
+}
+
+int ds_swaps_fetch(ds_ctx* ctx, int upto_step, uint8_t* swapped) {
+  if (upto_step < 0 || upto_step > ctx->n) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (!ctx->swaps) {
+    memset(swapped, 0, (size_t)upto_step);
+    return DS_OK;
+  }
+  CK(cudaMemcpy(swapped, ctx->swaps, (size_t)upto_step, cudaMemcpyDeviceToHost));
+  return DS_OK;
+}
+
 int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop_step, ds_results* res,
            int* steps_done) {
   if (ctx->world != 1) return DS_INVALID;
   if (start_step < 0 || stop_step > ctx->n || start_step > stop_step) return DS_INVALID;
+  if (ctx->pivot_partial && collect_minors) {  // elim.py:186-187
+    ctx->err = "partial pivoting cannot be combined with minors collection";
+    return DS_INVALID;
+  }
   int rc;
   // progressive D2H of the minors (pinned host buffers): rows finalised by
   // the emission are copied in batches on the side stream while the
@@ -1532,8 +1648,17 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
   const int BATCH = 64;
   int copied = 0;
   ctx->la_ext = 0;  // single-rank run: the engine chains the lookahead itself
-  ctx->la_limit = stop_step;
+  // row swaps change column i+1's owner rows after the update: no lookahead
+  ctx->la_limit = ctx->pivot_partial ? -1 : stop_step;
   for (int i = start_step; i < stop_step; i++) {
+    if (ctx->pivot_partial) {
+      KArgs k = kargs(ctx);
+      k_pivot_select<<<1, 1024, 0, ctx->stream>>>(k, i, ctx->pbest, ctx->swaps);
+      k_swap_rows<<<grid_for(ctx, (int64_t)ctx->ncomp * (ctx->L + 2) * ctx->n, 256), 256, 0, ctx->stream>>>(
+          k, i, ctx->pbest);
+      ctx->launches += 2;
+      CK(cudaGetLastError());
+    }
     if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) { ctx->la_limit = -1; return rc; }
     if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) { ctx->la_limit = -1; return rc; }
     if (prog && (i + 1 - start_step) % BATCH == 0) {

@@ -118,6 +118,17 @@ class DeviceElimination:
         _check(rc, self.ctx, "ds_run", self.rank)
         return rc, done.value
 
+    def set_pivot_mode(self, mode: str):
+        """pivot_mode of elim.eliminate (elim.py:184-208): "none" or "partial"."""
+        code = {"none": 0, "partial": 1}[mode]
+        _check(self.lib.ds_set_pivot_mode(self.ctx, code), self.ctx, "ds_set_pivot_mode", self.rank)
+
+    def swaps(self, upto: int) -> list[bool]:
+        """Per-step row-swap flags of a partial-pivoting run, steps [0, upto)."""
+        buf = (ctypes.c_uint8 * max(upto, 1))()
+        _check(self.lib.ds_swaps_fetch(self.ctx, upto, buf), self.ctx, "ds_swaps_fetch", self.rank)
+        return [bool(buf[i]) for i in range(upto)]
+
     # -- sharded building blocks ---------------------------------------------
     def pivot_buffer(self):
         p = ctypes.c_void_p()
