@@ -1373,6 +1373,7 @@ int ds_snapshot(ds_ctx* ctx, int save) {
   ctx->la_step = -1;
   ctx->det_from_cur = 0;
   CK(cudaMemsetAsync(ctx->row_flags, 0, ctx->n, ctx->stream));
+  if (ctx->swaps) CK(cudaMemsetAsync(ctx->swaps, 0, ctx->n, ctx->stream));
   CK(cudaMemsetAsync(ctx->status + 1, 0, 7 * sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->status, 0xff, sizeof(int32_t), ctx->stream));  // -1
   return DS_OK;

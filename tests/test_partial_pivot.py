@@ -115,5 +115,24 @@ def test_partial_wide_column_scan():
     tD, _ = eliminate(D, collect_minors=False)
     tB, _ = eliminate(B, collect_minors=False, pivot_mode="partial")
     assert [canonical_bits(x) for x in tB.pivots] == [canonical_bits(x) for x in tD.pivots]
-    assert [canonical_bits(x) for x in tB.det_series] == [canonical_bits(-x) for x in tD.det_series]
+    with Precision(p).context():
+        flipped = [canonical_bits(-x) for x in tD.det_series]
+    assert [canonical_bits(x) for x in tB.det_series] == flipped
     assert [canonical_bits(x) for r in B.rows for x in r] == [canonical_bits(x) for r in D.rows for x in r]
+
+
+def test_swap_signs_keep_full_precision():
+    """The sign applied to the fetched det chain is an exact negation at p bits
+    (not a rounding to the ambient default precision)."""
+    from paper_1308_1536_b200.elim import EliminationTrace, _apply_swap_signs
+    P = Precision(512)
+    with P.context():
+        third = mp.mpfr(1) / 3
+        dets = [third, third * 7, third * 11]
+    tr = EliminationTrace(n=3, prec=P)
+    tr.det_series = list(dets)
+    _apply_swap_signs(tr, [True, False, True], 0)
+    with P.context():
+        want = [-dets[0], -dets[1], dets[2]]
+    assert [canonical_bits(x) for x in tr.det_series] == [canonical_bits(x) for x in want]
+    assert tr.det_series[0].precision == 512
