@@ -13,9 +13,12 @@ from paper_1308_1536_b200.engine import DeviceElimination, HostResults  # noqa: 
 from paper_1308_1536_b200.synth import random_uniform_soa  # noqa: E402
 
 series = True
+fetch = True
 specs = []
 for arg in sys.argv[1:]:
-    if arg == "--no-series":
+    if arg == "--no-fetch":
+        fetch = False  # results stay in HBM (no pinned host copy of the minors)
+    elif arg == "--no-series":
         series = False  # minors emitted only at the last step (same update work)
     else:
         specs.append(arg)
@@ -25,7 +28,7 @@ for spec in specs:
     A = random_uniform_soa(n, p, 1, kind=kind)
     L = (p + 31) // 32
     with DeviceElimination(n, p, kind) as eng:
-        res = HostResults.alloc(n, eng.ncomp, L, True, pinned=True)
+        res = HostResults.alloc(n, eng.ncomp, L, True, pinned=True) if fetch else None
         eng.load(A)
         eng.profile(True)
         torch.cuda.synchronize()
@@ -33,7 +36,8 @@ for spec in specs:
         rc, done = eng.run(True, series, 0, n, None)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        eng.results(n, res)
+        if fetch:
+            eng.results(n, res)
         t2 = time.perf_counter()
         ms, nl, w = eng.profile_read()
         work = n * (n - 1) ** 2 / 2 * L * L * (4 if kind == "complex" else 1)
