@@ -18,6 +18,8 @@ import sys
 
 import numpy as np
 
+sys.set_int_max_str_digits(0)  # fingerprints / digests of >4300-digit mantissas (p >= 16384)
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 
@@ -78,6 +80,10 @@ def main():
              gen=["random_uniform", 48, 6, 1024])
     run_case("pp_uniform24_s2_p4096", synth_matrix("random_uniform", 24, 2, Precision(4096)),
              gen=["random_uniform", 24, 2, 4096])
+    run_case("pp_uniform16_s1_p8192", synth_matrix("random_uniform", 16, 1, Precision(8192)),
+             gen=["random_uniform", 16, 1, 8192])
+    run_case("pp_uniform10_s2_p16384", synth_matrix("random_uniform", 10, 2, Precision(16384)),
+             gen=["random_uniform", 10, 2, 16384])
     run_case("pp_uniform140_s9_p256", synth_matrix("random_uniform", 140, 9, P256),
              gen=["random_uniform", 140, 9, 256])
 
