@@ -1514,6 +1514,41 @@ void tc_plan_free(TcPlan* plan) {
   plan->work = nullptr;
 }
 
+// Rows per CTA of the main update launch (one CTA per SM).  At a fixed 16 the
+// grid runs in ceil(CTAs / SMs) waves, so late steps (few rows) lose part of a
+// wave to quantisation.  pick_rbr (opt-in, DS_TC_RBR_ADAPT=1) picks the rbr in
+// {16,12,8,6,4} minimising waves x (rbr + per-CTA setup).  Measured on B200: it
+// lowers the summed update-kernel time (N=1000 @8192: 0.85 -> 0.79 s) but not the
+// elimination (0.88 -> 0.90 s; N=2000 @4096: 2.10 -> 2.17 s): the lookahead tile
+// on its own stream then finds no free SM.  So the default stays 16.
+// DS_TC_RBR=r fixes r.
+static int pick_rbr(int ntiles, int nrows, int ng) {
+  static int sms = 0, fixed = -1, adapt_all = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+    const char* e = getenv("DS_TC_RBR");
+    fixed = e ? atoi(e) : 0;
+    adapt_all = getenv("DS_TC_RBR_ADAPT") ? 1 : 0;
+  }
+  if (fixed > 0) return fixed < RBR ? fixed : RBR;
+  (void)ng;
+  if (!adapt_all) return RBR;
+  if (ntiles < 1) ntiles = 1;
+  const int cand[5] = {16, 12, 8, 6, 4};
+  int best = RBR;
+  double best_cost = 1e300;
+  for (int c : cand) {
+    const long ctas = (long)ntiles * ((nrows + c - 1) / c);
+    const long waves = (ctas + sms - 1) / sms;
+    const double cost = (double)waves * (c + 0.5);  // +0.5 row: TMEM A load, barriers, TMA descriptors
+    if (cost < best_cost * 0.98) { best_cost = cost; best = c; }
+  }
+  return best;
+}
+
 int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a_exp, uint8_t* a_cls,
                      int64_t a_count, const uint8_t* pbuf, const uint32_t* z_limbs, const int32_t* z_exp,
                      const uint8_t* z_cls, int nloc, int n, int i, int jl0, int collect_minors, int32_t* status,
@@ -1618,10 +1653,10 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     }
   }
   a.tma_ok = w->amap_ok;
-  a.rbr = RBR;
   a.no_direct = getenv("DS_TC_NO_DIRECT") ? 1 : 0;
   const int ntile = (ncols + TM - 1) / TM;
-  const int nrg = (nrows + RBR - 1) / RBR;
+  a.rbr = pick_rbr(ntile - (la_col >= 0 && ntile >= 2 ? 1 : 0), nrows, plan->ng);
+  const int nrg = (nrows + a.rbr - 1) / a.rbr;
   const int ts = la_col >= 0 ? (la_col - kstart) / TM : -1;  // tile holding the lookahead column
   if (ts >= 0 && ts < ntile && ntile >= 2 && la) {
     // A: that tile on the lookahead stream (the caller chains the next multipliers
