@@ -139,6 +139,13 @@ int ds_status(ds_ctx *ctx, int *failed_step);
 /* Copy trace (replicated on every rank) and the minors rows this rank owns
  * (row m-1 owned when (m-1) % world == rank) into `res`. */
 int ds_results_fetch(ds_ctx *ctx, int upto_step, ds_results *res);
+/* Incremental form of ds_results_fetch for a serial context (world 1):
+ * trace entries [t0, t1) (pivots / det_series) and the minors rows of leading
+ * sizes [m0, m1) (row m-1, its first m entries, plus row_flags[m-1]) into the
+ * same positions of `res` (counts n and n*n).  Lets the drop-in eliminate()
+ * hand each MinorRow to its sink as the row finalises (elim.py:220-226)
+ * instead of after the whole run.  Synchronises the context streams. */
+int ds_results_fetch_range(ds_ctx *ctx, int t0, int t1, int m0, int m1, ds_results *res);
 /* Seed the device det chain (resume, elim.py:201): det = host scalar. */
 int ds_set_det(ds_ctx *ctx, const ds_soa *det1);
 

@@ -26,7 +26,8 @@ EXPORTS = ("ds_version", "ds_create", "ds_destroy", "ds_load", "ds_fetch", "ds_r
            "ds_pivot_stage", "ds_step", "ds_status", "ds_results_fetch", "ds_set_det", "ds_stream",
            "ds_launch_count", "ds_last_error", "ds_scalar_op", "ds_set_stream", "ds_use_pivot_buffer",
            "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters", "ds_lookahead_enable", "ds_lookahead_stream",
-           "ds_lookahead_pivot", "ds_lookahead_mult", "ds_set_pivot_mode", "ds_swaps_fetch")
+           "ds_lookahead_pivot", "ds_lookahead_mult", "ds_set_pivot_mode", "ds_swaps_fetch",
+           "ds_results_fetch_range")
 
 
 class ds_results(ctypes.Structure):
@@ -58,6 +59,7 @@ def load_library(path: str = LIB_PATH):
         "ds_step": (I, [VP, I, I, I]),
         "ds_status": (I, [VP, P(I)]),
         "ds_results_fetch": (I, [VP, I, P(ds_results)]),
+        "ds_results_fetch_range": (I, [VP, I, I, I, I, P(ds_results)]),
         "ds_set_det": (I, [VP, S]),
         "ds_stream": (VP, [VP]),
         "ds_launch_count": (ctypes.c_int64, [VP]),

@@ -1599,6 +1599,52 @@ static int results_fetch_from(ds_ctx* ctx, int upto, ds_results* r, int minors_f
 
 int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) { return results_fetch_from(ctx, upto, r, 0); }
 
+// trace entries [t0, t1) and minors rows of leading sizes [m0, m1) (row m-1,
+// its first m entries) with their flags: the incremental fetch the drop-in
+// eliminate() streams rows to its sink with (world 1)
+int ds_results_fetch_range(ds_ctx* ctx, int t0, int t1, int m0, int m1, ds_results* r) {
+  if (ctx->world != 1) return DS_INVALID;
+  if (t0 < 0 || t1 > ctx->n || m0 < 2 || m1 > ctx->n + 1) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int n = ctx->n, L = ctx->L;
+  if (t1 > t0) {
+    const int64_t cnt = t1 - t0;
+    ds_soa* vs[2] = {&r->pivots, &r->dets};
+    uint32_t* sl[2] = {ctx->piv_limbs, ctx->det_limbs};
+    int32_t* se[2] = {ctx->piv_exp, ctx->det_exp};
+    uint8_t* sc[2] = {ctx->piv_cls, ctx->det_cls};
+    for (int v = 0; v < 2; v++) {
+      ds_soa* d = vs[v];
+      if (!d->limbs) continue;
+      for (int c = 0; c < ctx->ncomp; c++) {
+        for (int l = 0; l < L; l++)
+          CK(cudaMemcpyAsync(d->limbs + ((int64_t)c * L + l) * d->count + t0, sl[v] + ((int64_t)c * L + l) * n + t0,
+                             sizeof(uint32_t) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(d->exp + (int64_t)c * d->count + t0, se[v] + (int64_t)c * n + t0, sizeof(int32_t) * cnt,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(d->cls + (int64_t)c * d->count + t0, sc[v] + (int64_t)c * n + t0, cnt,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+  }
+  if (m1 > m0) {
+    int rc;
+    if ((rc = copy_row_range(ctx, &r->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, m0 - 1, m1 - 1, m1 - 1,
+                             ctx->stream)) != DS_OK)
+      return rc;
+    if ((rc = copy_row_range(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls, m0 - 1, m1 - 1, m1 - 1,
+                             ctx->stream)) != DS_OK)
+      return rc;
+    if (r->row_flags)
+      CK(cudaMemcpyAsync(r->row_flags + (m0 - 1), ctx->row_flags + (m0 - 1), (size_t)(m1 - m0),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
 int ds_set_pivot_mode(ds_ctx* ctx, int mode) {
   if (mode != 0 && mode != 1) return DS_INVALID;
   if (mode == 1 && (ctx->world != 1 || ctx->kind != DS_KIND_REAL)) {

@@ -346,3 +346,17 @@ int dsh_read_mpmat(const char *path, int n, int kind, int L, long p, ds_soa *out
   free(buf);
   return rc;
 }
+
+/* ---- boundary conversion: ds SoA -> mpfr_t (batch) ----------------------
+ * Initialise `count` caller-allocated mpfr_t structs at precision p from the
+ * SoA elements [start, start + count) of component c (exact copies of the
+ * limbs, exponent and sign class).  The Python scalar objects (mp.mpfr) wrap
+ * these structs, so one call replaces count per-scalar ctypes round trips
+ * when the drop-in eliminate() hands rows to its caller. */
+int dsh_soa_to_mpfr(__mpfr_struct *out, const ds_soa *s, int c, int64_t start, int64_t count, int L, long p) {
+  for (int64_t k = 0; k < count; k++) {
+    mpfr_init2(&out[k], p);
+    dsh_get_soa(&out[k], s, c, start + k, L);
+  }
+  return 0;
+}

@@ -153,6 +153,12 @@ class DeviceElimination:
         _check(self.lib.ds_results_fetch(self.ctx, upto, ctypes.byref(r)), self.ctx, "ds_results_fetch",
                self.rank)
 
+    def results_range(self, t0: int, t1: int, m0: int, m1: int, res: HostResults):
+        """Trace entries [t0, t1) and minors rows of sizes [m0, m1) (ds_results_fetch_range)."""
+        r = res.c()
+        _check(self.lib.ds_results_fetch_range(self.ctx, int(t0), int(t1), int(m0), int(m1), ctypes.byref(r)),
+               self.ctx, "ds_results_fetch_range", self.rank)
+
     def snapshot(self, save: bool):
         """save=True: keep a device copy of this rank's rows; save=False:
         restore it and reset the run state (resident re-runs)."""

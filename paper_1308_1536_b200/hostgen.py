@@ -35,6 +35,9 @@ def _load():
         L.dsh_beta_gammas.restype = ctypes.c_int
         L.dsh_beta_gammas.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(ds_soa)]
+        L.dsh_soa_to_mpfr.restype = ctypes.c_int
+        L.dsh_soa_to_mpfr.argtypes = [ctypes.c_void_p, ctypes.POINTER(ds_soa), ctypes.c_int, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int, ctypes.c_long]
         _lib = L
     return _lib
 

@@ -13,11 +13,16 @@ Transports:
   * "local"  -- T virtual shards in this process, one device context each
                 (round-robin over the visible GPUs); the broadcast is a
                 device-to-device / peer copy of the pivot buffer.
-  * "process" / "nccl" -- one process per GPU under torch.distributed (the
-                caller ran init_process_group, e.g. via torchrun); the
-                broadcast is torch.distributed.broadcast of a device tensor
-                that IS the pivot buffer (NCCL over NVLink), stream-ordered
-                with the kernels on torch's current stream.
+  * "process" / "nccl" -- one process per GPU.  Inside an initialised
+                torch.distributed group (torchrun) every rank calls
+                par_eliminate and the broadcast is torch.distributed.broadcast
+                of a device tensor that IS the pivot buffer (NCCL over
+                NVLink), stream-ordered with the kernels on torch's current
+                stream.  From a plain process, par_eliminate forks the worker
+                ranks itself (torch.multiprocessing spawn, TCP rendezvous on
+                127.0.0.1) like the reference coordinator (parexec.py:350-405):
+                NCCL when every rank has its own GPU, else gloo with a pinned
+                host staging copy (ranks sharing a GPU).
 The wire format of the reference (pack_row / unpack_row, MPRW v1 with CRC32,
 parexec.py:72-157) is kept for API compatibility; the device path does not
 serialize -- HBM already holds the binary limb layout.
@@ -229,11 +234,12 @@ def _local_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool
     finally:
         for e in ranks:
             e.close()
-    A.assign_soa(soa)
+    A._set_lazy(soa)
     return res, done
 
 
-def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcast, stats: CommStats | None = None):
+def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcast, stats: CommStats | None = None,
+             lookahead: bool = True):
     """Generic per-rank step loop of the message-passing executor.
 
     engine    -- this rank's context (stage/step/status), a DeviceElimination
@@ -244,7 +250,7 @@ def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcas
     """
     world, rank = engine.world, engine.rank
     nbytes = pivot.numel() * pivot.element_size()
-    la = _lookahead_setup(engine, n, pivot)
+    la = _lookahead_setup(engine, n, pivot) if lookahead else None
     for i in range(n):
         owner = i % world
         if rank == owner:
@@ -330,28 +336,58 @@ def allreduce_gather(res: HostResults, soa: SoA | None, rank: int, world: int, a
         allreduce(soa.cls)
 
 
-def _process_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats):
+def _rank_setup(eng, backend: str, rank: int):
+    """Pivot tensor + broadcast callable for one device rank.  NCCL broadcasts the
+    device buffer in place on torch's current stream (the context launches there);
+    gloo (ranks sharing a GPU, or CPU-only process groups) stages it through a
+    pinned host copy.  Returns (pivot, broadcast, lookahead_ok)."""
     import torch
     import torch.distributed as dist
-    if not dist.is_available() or not dist.is_initialized():
-        raise RuntimeError("transport='process' needs torch.distributed initialized (one process per GPU, "
-                           "e.g. torchrun); use transport='local' for in-process shards")
+    dev = torch.cuda.current_device()
+    _, pbytes = eng.pivot_buffer()
+    pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+    _native_check(eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes), "ds_use_pivot_buffer")
+    _native_check(eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream), "ds_set_stream")
+    if backend == "nccl":
+        return pivot, (lambda t, src: dist.broadcast(t, src=src)), True
+    staging = {}
+
+    def bcast(t, src):
+        host = staging.get(t.numel())
+        if host is None:
+            host = staging[t.numel()] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+        if rank == src:
+            host.copy_(t)  # synchronous w.r.t. the current stream: after the staging kernel
+        dist.broadcast(host, src=src)
+        if rank != src:
+            t.copy_(host)
+    return pivot, bcast, False
+
+
+def _native_check(rc: int, what: str):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed with code {rc}")
+
+
+def _group_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats):
+    """Every rank of an already-initialised process group (e.g. torchrun) calls
+    par_eliminate; each returns the full result, like the reference coordinator."""
+    import torch
+    import torch.distributed as dist
     world, rank = dist.get_world_size(), dist.get_rank()
     if world != workers:
         raise ValueError(f"workers={workers} but the process group has {world} ranks")
     n, p = A.n, A.prec.bits
     dev = torch.cuda.current_device()
+    backend = dist.get_backend()
     eng = DeviceElimination(n, p, A.kind, dev, rank, world)
     try:
         soa = A.to_soa()
         eng.load(soa)
-        _, pbytes = eng.pivot_buffer()
-        pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{dev}")
-        eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
-        eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream)
-        failed = dist_run(eng, n, collect_minors, series, pivot, lambda t, src: dist.broadcast(t, src=src), stats)
+        pivot, bcast, la_ok = _rank_setup(eng, backend, rank)
+        failed = dist_run(eng, n, collect_minors, series, pivot, bcast, stats, lookahead=la_ok)
         # agree on the failed step (identical on every rank by construction)
-        f = torch.tensor([failed], dtype=torch.int64, device=f"cuda:{dev}")
+        f = torch.tensor([failed], dtype=torch.int64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
         dist.all_reduce(f, op=dist.ReduceOp.MAX)
         failed = int(f.item())
         done = failed if failed >= 0 else n
@@ -364,17 +400,173 @@ def _process_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bo
         eng.close()
 
     def allreduce(arr):
-        t = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{dev}")
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if backend == "nccl":
+            t = t.to(f"cuda:{dev}")
         dist.all_reduce(t)
         arr[...] = t.cpu().numpy()
 
     allreduce_gather(res, soa, rank, world, allreduce)
-    A.assign_soa(soa)
+    A._set_lazy(soa)
     return res, done
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _spawn_worker(rank: int, world: int, port: int, d: str, n: int, p: int, kind: str, collect_minors: bool,
+                  series: bool, engine_factory=None):
+    """One worker process of par_eliminate(transport="process") without a process
+    group (ref parexec.py:290-333): one GPU per rank when there are enough (NCCL),
+    else ranks share the visible GPUs and broadcast over gloo.  Reads the input
+    from the coordinator's scratch directory, writes back its owned rows."""
+    import json
+    import traceback
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        ncomp = 2 if kind == "complex" else 1
+        L = (p + 31) // 32
+        src = SoA(ncomp, L, n * n, np.load(os.path.join(d, "limbs.npy")), np.load(os.path.join(d, "exp.npy")),
+                  np.load(os.path.join(d, "cls.npy")))
+        if engine_factory is None:
+            ndev = torch.cuda.device_count()
+            if ndev == 0:
+                from .errors import DeviceUnavailable
+                raise DeviceUnavailable("par_eliminate(transport='process') needs a CUDA device")
+            dev = rank % ndev
+            torch.cuda.set_device(dev)
+            backend = "nccl" if ndev >= world and not os.environ.get("DS_PAR_FORCE_GLOO") else "gloo"
+            kw = {"device_id": torch.device(f"cuda:{dev}")} if backend == "nccl" else {}
+            dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+            eng = DeviceElimination(n, p, kind, dev, rank, world)
+            eng.load(src)
+            pivot, bcast, la_ok = _rank_setup(eng, backend, rank)
+        else:  # test hook: a CPU engine with the same interface (gloo)
+            backend = "gloo"
+            dist.init_process_group(backend, rank=rank, world_size=world)
+            eng = engine_factory(n, p, kind, rank, world)
+            eng.load(src)
+            pivot = torch.from_numpy(eng.pivot_array())
+            bcast, la_ok = (lambda t, s_: dist.broadcast(t, src=s_)), False
+        stats = CommStats()
+        failed = dist_run(eng, n, collect_minors, series, pivot, bcast, stats, lookahead=la_ok)
+        f = torch.tensor([failed], dtype=torch.int64, device=pivot.device if backend == "nccl" else "cpu")
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+        failed = int(f.item())
+        done = failed if failed >= 0 else n
+        res = HostResults.alloc(n, eng.ncomp, eng.L, collect_minors)
+        eng.results(done, res)
+        fin = SoA.like(src)
+        eng.fetch(fin)
+        if hasattr(eng, "lib") and engine_factory is None:
+            eng.lib.ds_set_stream(eng.ctx, None)
+            eng.lib.ds_use_pivot_buffer(eng.ctx, None, 0)
+        rows = np.arange(rank, n, world)
+
+        def own(a: SoA):
+            return (a.limbs.reshape(ncomp, L, n, n)[:, :, rows, :], a.exp.reshape(ncomp, n, n)[:, rows, :],
+                    a.cls.reshape(ncomp, n, n)[:, rows, :])
+
+        out = {}
+        out["m_limbs"], out["m_exp"], out["m_cls"] = own(fin)
+        if collect_minors:
+            out["s_limbs"], out["s_exp"], out["s_cls"] = own(res.signed)
+            out["n_limbs"], out["n_exp"], out["n_cls"] = own(res.normalized)
+        out["flags"] = res.row_flags[rows]
+        if rank == 0:
+            for name, a in (("piv", res.pivots), ("det", res.dets)):
+                out[name + "_limbs"], out[name + "_exp"], out[name + "_cls"] = a.limbs, a.exp, a.cls
+            with open(os.path.join(d, "meta.json"), "w") as fh:
+                json.dump({"done": done, "broadcasts": stats.broadcasts, "bytes_total": stats.bytes_total,
+                           "per_step_bytes": stats.per_step_bytes[:1], "backend": backend}, fh)
+        np.savez(os.path.join(d, f"out{rank}.npz"), **out)
+        eng.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException:
+        with open(os.path.join(d, f"err{rank}.txt"), "w") as fh:
+            fh.write(traceback.format_exc())
+        raise
+
+
+def _spawn_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats,
+               engine_factory=None):
+    """par_eliminate(transport="process") from a plain process: fork `workers` ranks
+    (torch.multiprocessing, spawn), as the reference's coordinator does
+    (ref parexec.py:350-405), and assemble their owned rows."""
+    import json
+    import tempfile
+    import torch.multiprocessing as tmp
+    from .errors import WorkerFailure
+    n, p = A.n, A.prec.bits
+    soa = A.to_soa()
+    nc, L = soa.ncomp, soa.L
+    with tempfile.TemporaryDirectory(prefix="ds_par_") as d:
+        np.save(os.path.join(d, "limbs.npy"), soa.limbs)
+        np.save(os.path.join(d, "exp.npy"), soa.exp)
+        np.save(os.path.join(d, "cls.npy"), soa.cls)
+        ctx = tmp.get_context("spawn")
+        port = _free_port()
+        procs = [ctx.Process(target=_spawn_worker,
+                             args=(r, workers, port, d, n, p, A.kind, collect_minors, series, engine_factory))
+                 for r in range(workers)]
+        for pr in procs:
+            pr.start()
+        for pr in procs:
+            pr.join()
+        for r, pr in enumerate(procs):
+            if pr.exitcode != 0:
+                msg = ""
+                ep = os.path.join(d, f"err{r}.txt")
+                if os.path.exists(ep):
+                    msg = open(ep).read().strip().splitlines()[-1]
+                raise WorkerFailure(r + 1, f"worker exited with code {pr.exitcode}: {msg}")
+        meta = json.load(open(os.path.join(d, "meta.json")))
+        done = int(meta["done"])
+        res = HostResults.alloc(n, nc, L, collect_minors)
+        fin = SoA(nc, L, n * n)
+        for r in range(workers):
+            z = np.load(os.path.join(d, f"out{r}.npz"))
+            rows = np.arange(r, n, workers)
+            targets = [("m", fin)] + ([("s", res.signed), ("n", res.normalized)] if collect_minors else [])
+            for key, a in targets:
+                a.limbs.reshape(nc, L, n, n)[:, :, rows, :] = z[key + "_limbs"]
+                a.exp.reshape(nc, n, n)[:, rows, :] = z[key + "_exp"]
+                a.cls.reshape(nc, n, n)[:, rows, :] = z[key + "_cls"]
+            res.row_flags[rows] = z["flags"]
+            if r == 0:
+                for key, a in (("piv", res.pivots), ("det", res.dets)):
+                    a.limbs[...] = z[key + "_limbs"]
+                    a.exp[...] = z[key + "_exp"]
+                    a.cls[...] = z[key + "_cls"]
+    stats.broadcasts = int(meta["broadcasts"])
+    stats.bytes_total = int(meta["bytes_total"])
+    stats.per_step_bytes = list(meta["per_step_bytes"]) * stats.broadcasts
+    stats.fanout_deliveries = stats.broadcasts * workers
+    stats.minor_messages = sum(1 for m in range(2, n + 1) if res.row_flags[m - 1] & 1)
+    A._set_lazy(fin)
+    return res, done
+
+
+def _process_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool, stats: CommStats,
+                 engine_factory=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return _group_run(A, workers, collect_minors, series, stats)
+    return _spawn_run(A, workers, collect_minors, series, stats, engine_factory)
+
+
 def par_eliminate(A: MatrixBuffer, workers: int, transport: str = "local", collect_minors: bool = True,
-                  series: bool = True, sink=None, devices=None):
+                  series: bool = True, sink=None, devices=None, _engine_factory=None):
     """Sharded elimination of A in place over `workers` ranks
     (parexec.py:408-424).  Returns (trace, minor_series, comm_stats), bit-
     identical to eliminate() for every worker count and transport."""
@@ -387,7 +579,7 @@ def par_eliminate(A: MatrixBuffer, workers: int, transport: str = "local", colle
     if transport == "local":
         res, done = _local_run(A, topo.workers, collect_minors, series, stats, devices)
     else:
-        res, done = _process_run(A, topo.workers, collect_minors, series, stats)
+        res, done = _process_run(A, topo.workers, collect_minors, series, stats, _engine_factory)
     _assemble(A, trace, res, done, collect_minors, sink, out)
     if done < A.n:
         raise ZeroPivot(done + 1, trace=trace, series=out)

@@ -77,6 +77,25 @@ class SoA:
                  for c in range(self.ncomp)]
         return parts[0] if self.ncomp == 1 else mp.mpc_from_parts(parts[0], parts[1])
 
+    def scalars(self, start: int, count: int, prec: int) -> list:
+        """Scalar objects for the contiguous elements [start, start+count): the
+        mpfr_t structs are filled by one native call (libds_hostgen.so,
+        dsh_soa_to_mpfr) and wrapped, instead of one ctypes round trip per
+        scalar -- the boundary conversion of whole minors rows."""
+        if count <= 0:
+            return []
+        from .hostgen import _load
+        lib = _load()
+        c_soa = self.c()
+        parts = []
+        for c in range(self.ncomp):
+            arr = (mp._MPFR_T * count)()
+            lib.dsh_soa_to_mpfr(arr, ctypes.byref(c_soa), c, start, count, self.L, prec)
+            parts.append(mp.wrap_structs(arr, count))
+        if self.ncomp == 1:
+            return parts[0]
+        return [mp.mpc_from_parts(a, b) for a, b in zip(parts[0], parts[1])]
+
     def set(self, idx: int, x, prec: int):
         comps = (x,) if self.ncomp == 1 else (x.real, x.imag)
         for c, v in enumerate(comps):

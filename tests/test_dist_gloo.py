@@ -77,3 +77,35 @@ def test_gloo_sharded_matches_reference(name, world, tmp_path):
         assert int(bcast) == meta["n"]  # one broadcast per step (test_acceptance.py:157)
         if meta["zero_pivot_step"] is not None:
             assert int(done) + 1 == meta["zero_pivot_step"]
+
+
+@pytest.mark.parametrize("name,world", [("uniform13_s5_p192", 2), ("complex8_s9_p192", 3), ("zero_pivot3", 2),
+                                        ("nominors_u9_p320", 2), ("series_false_u6", 3)])
+def test_spawned_process_transport_matches_reference(name, world):
+    """par_eliminate(transport="process") from a plain process forks its own ranks (ref
+    parexec.py:350-405), rendezvous over TCP, broadcasts per step over gloo and reassembles
+    the owned rows into the caller's buffer -- oracle engines stand in for the GPUs here."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle_engine
+    from _util import build_input, load_golden
+    from golden.digest import digest_parts
+    from paper_1308_1536_b200 import MatrixBuffer, Precision, ZeroPivot, par_eliminate
+    from paper_1308_1536_b200.scalars import canonical_bits
+    meta, arrays = load_golden(name)
+    A = MatrixBuffer.from_soa(meta["n"], meta["kind"], Precision(meta["prec"]), build_input(meta, arrays))
+    got = []
+    try:
+        trace, minors, stats = par_eliminate(A, world, transport="process", collect_minors=meta["collect_minors"],
+                                             series=meta["series"], sink=got.append,
+                                             _engine_factory=_oracle_engine.make)
+        assert stats.broadcasts == meta["n"]
+    except ZeroPivot as exc:
+        assert exc.step == meta["zero_pivot_step"]
+        trace = exc.trace
+    rows = [(r.n, [canonical_bits(x) for x in r.signed],
+             None if r.normalized is None else [canonical_bits(x) for x in r.normalized]) for r in got]
+    assert [r[0] for r in rows] == meta["emitted"]
+    dig = digest_parts([canonical_bits(x) for x in trace.pivots], [canonical_bits(x) for x in trace.det_series],
+                       rows, [canonical_bits(x) for row in A.rows for x in row])
+    assert dig == meta["digest"]
