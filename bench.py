@@ -46,14 +46,15 @@ def measured_hbm_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def committed_traffic(n, prec, elems_per_launch):
-    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of an average update launch, scaled from the
-    committed ncu --set full capture of one launch of this workload (profiles/update_traffic.json)."""
+def committed_profile(n, prec):
+    """The committed ncu --set full capture of one update launch of this workload
+    (profiles/update_traffic.json): DRAM bytes per element (dram__bytes_read.sum +
+    dram__bytes_write.sum), issue-active and tensor-pipe fractions, limiter."""
     try:
         with open(os.path.join(ROOT, "profiles", "update_traffic.json")) as f:
             d = json.load(f)
         if d.get("n") == n and d.get("prec_bits") == prec:
-            return d["dram_bytes_per_element"] * elems_per_launch
+            return d
     except Exception:
         pass
     return None
@@ -69,6 +70,8 @@ def parse():
     ap.add_argument("--bits", dest="prec", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg (outside the timed region)")
+    ap.add_argument("--parity-m", type=int, default=256, help="leading block size of the prefix parity check")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed (NCCL) step loop even at world size 1 (testing)")
@@ -116,17 +119,21 @@ def build_input(args, pinned: bool, rank: int = 0, world: int = 1, agree=None):
         if est <= args.gen_budget:
             bb.fill(args.n)
             A = bb.out
-            desc = (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
-                    f"@{args.prec}b, zeros data/zeta_zeros_4096.txt" + (", cached column Gammas" if gammas else ""))
-            return A, desc, time.perf_counter() - t0
+            return A, workload_desc(args), time.perf_counter() - t0
         print(f"[bench] beta matrix generation would take ~{est:.0f}s > --gen-budget {args.gen_budget:.0f}s "
               f"on this host: using random_uniform (same shape, same work)", file=sys.stderr)
         args.family = "random"
     if args.family == "random":
         from paper_1308_1536_b200.synth import random_uniform_soa
         A = random_uniform_soa(args.n, args.prec, 2000, pinned=pinned)
-        desc = f"N={args.n} random_uniform real matrix @{args.prec}b (SURVEY 8d config 3')"
-    return A, desc, time.perf_counter() - t0
+    return A, workload_desc(args), time.perf_counter() - t0
+
+
+def workload_desc(args) -> str:
+    if args.family == "beta":
+        return (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
+                f"@{args.prec}b, zeros data/zeta_zeros_4096.txt")
+    return f"N={args.n} random_uniform real matrix @{args.prec}b (SURVEY 8d config 3')"
 
 
 def work_limb_macs(n: int, L: int, complex_: bool = False) -> float:
@@ -189,25 +196,47 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(n: int, p: int, seconds: float, A):
-    """Time the reference hot loop (oracle = elim.py:37-53 over MPFR) on a
-    bounded sample of the workload: pivot row 0 applied to the next `rows`
-    full-width rows of A, repeated for steps i = 0, 1, ... until ~`seconds`
-    of wall time; all host threads."""
+class _Soa:
+    """Minimal ds SoA holder (limbs/exp/cls/count) for the CPU legs: they import
+    nothing from the product package."""
+
+    def __init__(self, limbs, exp, cls):
+        self.limbs, self.exp, self.cls, self.count = limbs, exp, cls, limbs.shape[2]
+
+
+def cpu_sample(n: int, p: int, rows: int, seed: int = 2000):
+    """Pivot row + `rows` full-width rows at p bits in the ds SoA layout, drawn with
+    numpy from the random_uniform family's distribution (genmat.py:242-246: sign
+    uniform, |x| = U with a full p-bit mantissa).  MPFR's mul/sub cost at fixed p
+    does not depend on the values, and this keeps the CPU legs free of the product's
+    builders (the reference arm runs first, on a fresh box)."""
+    import numpy as np
+    L = (p + 31) // 32
+    rng = np.random.default_rng(seed)
+    out = []
+    for count in (n, rows * n):
+        limbs = rng.integers(0, 2 ** 32, size=(1, L, count), dtype=np.uint32)
+        zb = 32 * L - p
+        if zb:
+            limbs[0, zb // 32] &= np.uint32((0xFFFFFFFF << (zb % 32)) & 0xFFFFFFFF)
+            limbs[0, :zb // 32] = 0
+        limbs[0, L - 1] |= np.uint32(0x80000000)
+        exp = (1 - rng.geometric(0.5, size=(1, count))).astype(np.int32)
+        cls = rng.integers(0, 2, size=(1, count)).astype(np.uint8)
+        out.append(_Soa(np.ascontiguousarray(limbs), np.ascontiguousarray(exp), np.ascontiguousarray(cls)))
+    return out
+
+
+def cpu_reference(n: int, p: int, seconds: float):
+    """Time the reference hot loop (oracle = elim.py:37-53 restated over MPFR) on a
+    bounded sample of the workload: pivot step i applied to `rows` full-width rows,
+    i = 0, 1, ... until ~`seconds` of timed MPFR work; all host threads."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
-    from paper_1308_1536_b200.soa import SoA
     L = (p + 31) // 32
     threads = len(os.sched_getaffinity(0))
     rows_per_call = min(max(threads * 4, 64), n - 1)
-    prow = SoA(1, L, n)
-    rows = SoA(1, L, rows_per_call * n)
-    prow.limbs[:] = A.limbs[:, :, :n]
-    prow.exp[:] = A.exp[:, :n]
-    prow.cls[:] = A.cls[:, :n]
-    rows.limbs[:] = A.limbs[:, :, n:n + rows_per_call * n]
-    rows.exp[:] = A.exp[:, n:n + rows_per_call * n]
-    rows.cls[:] = A.cls[:, n:n + rows_per_call * n]
+    prow, rows = cpu_sample(n, p, rows_per_call)
     total_t, total_macs, calls, i = 0.0, 0.0, 0, 0
     while total_t < seconds and i < n - 1:
         # step i touches all n-1 columns of every sampled row (L and U slots)
@@ -218,9 +247,9 @@ def cpu_reference(n: int, p: int, seconds: float, A):
         i += 1
     rate = total_macs * L * L / total_t
     return {"value": rate, "unit": "limb-MAC/s", "cores": threads, "kind": "port",
-            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}) of the workload matrix, "
-                      f"elim.py:37-53 restated over MPFR 4.2.1 (oracle/ds_oracle.c), {total_macs:.3g} MACs in "
-                      f"{total_t:.2f}s on {threads} threads",
+            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}, p={p}, random_uniform "
+                      f"distribution, numpy seed 2000), elim.py:37-53 restated over MPFR 4.2.1 "
+                      f"(oracle/ds_oracle.c), {total_macs:.3g} element MACs in {total_t:.2f}s on {threads} threads",
             "seconds_to_all_minors_extrapolated": work_limb_macs(n, L) / rate}
 
 
@@ -233,13 +262,13 @@ def run_reference(args):
     # MPFR values outside the timed region (measured: ~7x the timed seconds on the B200
     # box), so this keeps the whole --impl reference run to a few minutes
     per = max(2.0, min(args.cpu_seconds, 24.0 / max(1, args.steps + args.warmup)))
-    A, desc, _ = build_input(args, pinned=False)
+    desc = workload_desc(args)
     for _ in range(args.warmup):
-        cpu_reference(args.n, args.prec, per / 4, A)
+        cpu_reference(args.n, args.prec, per / 4)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference(args.n, args.prec, per, A))
+        vals.append(cpu_reference(args.n, args.prec, per))
     wall = time.perf_counter() - t0
     rate = sum(v["value"] for v in vals) / len(vals)
     base = vals[-1]
@@ -248,7 +277,7 @@ def run_reference(args):
            "value": rate, "unit": "limb-MAC/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "mpfr (u64 limbs)",
-           "data": "Artless beta matrix from data/ zeta zeros" if desc.startswith("Artless") else "synthetic",
+           "data": "synthetic (random_uniform sample rows; MPFR cost is value-independent at fixed p)",
            "impl": "reference",
            "config": workload(args, desc),
            "seconds_to_all_minors": work_limb_macs(args.n, L) / rate,
@@ -258,11 +287,64 @@ def run_reference(args):
     emit_json(out)
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-exec under
+    torch.distributed.run with N ranks (one per GPU), forwarding the JSON line."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        emit_json({"error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {torch.cuda.device_count()}",
+                   "n_gpus": args.gpus})
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's transport choice (NVLS / P2P) goes to the log
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, env=env, text=True)
+    for line in r.stdout.splitlines():
+        if line.startswith("{"):
+            emit_json(json.loads(line))
+    return r.returncode
+
+
+def parity_leg(args, A, res, final, eng_factory):
+    """Bit parity of THIS run against the oracle (tests/parity_check.py), outside every
+    timed region: leading-steps state (a fresh device run of the first steps), the
+    prefix property on the leading m x m block, and Laplace residuals."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import parity_check as pc
+    from paper_1308_1536_b200.engine import HostResults
+    t0 = time.perf_counter()
+    n, p = args.n, args.prec
+    out = {"checker": "oracle/ds_oracle.c (elim.py:37-229 over MPFR, pinned by tests/golden)"}
+    head = 4 if p > 8192 else 8
+    with eng_factory() as e2:
+        e2.load(A)
+        rh = HostResults.alloc(n, 1, e2.L, False)
+        e2.run(True, True, 0, head, rh)
+        fh = A.copy()
+        e2.fetch(fh)
+    out["leading_steps"] = pc.leading_steps(A, n, p, "real", head, fh, rh)
+    out["prefix"] = pc.prefix(A, n, p, "real", min(args.parity_m, n), res, final)
+    sizes = sorted({n, n - 1, max(2, n // 2)})
+    out["laplace"] = pc.laplace(A, n, p, res, sizes)
+    out["ok"] = bool(out["leading_steps"]["ok"] and out["prefix"]["ok"])
+    out["seconds"] = time.perf_counter() - t0
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -274,6 +356,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+    from paper_1308_1536_b200.soa import SoA
 
     n, p = args.n, args.prec
     L = (p + 31) // 32
@@ -294,6 +377,7 @@ def main():
         eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
     eng.lib.ds_set_stream(eng.ctx, stream.cuda_stream)
     res = HostResults.alloc(n, 1, L, True, pinned=True)
+    final = SoA(1, L, n * n, pinned=True)
 
     def one_pass(resident: bool):
         if resident:
@@ -305,10 +389,12 @@ def main():
                 eng.run_resident(True, True, 0, n)
             else:
                 eng.run(True, True, 0, n, res)
+                eng.fetch(final)  # the in-place L\\U state is part of the result (elim.py:19-22)
         else:
             dist_run(eng, n, True, True, pivot, lambda t, src: dist.broadcast(t, src=src))
             if not resident:
                 eng.results(n, res)
+                eng.fetch(final)
 
     def barrier():
         torch.cuda.synchronize()
@@ -346,20 +432,25 @@ def main():
     gpu_launches = eng.launches() - launches0
     total_work = work_limb_macs(n, L)
     value = total_work / (ms / 1e3)
-    # ---- timed: end to end through the C ABI with host buffers
+    # ---- timed: end to end through the C ABI with host buffers (pinned): H2D of the
+    # matrix, the elimination, D2H of trace + minors (progressive) + final matrix
     e2e = None
     if not args.no_e2e:
         one_pass(False)
         barrier()
+        c0 = eng.counters()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             one_pass(False)
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
-        h2d = A.nbytes if world == 1 else A.nbytes  # each rank copies its rows; host buffer is the full matrix
-        d2h = res.pivots.nbytes + res.dets.nbytes + res.signed.nbytes + res.normalized.nbytes + res.row_flags.nbytes
-        e2e = {"value": total_work / e2e_s, "unit": "limb-MAC/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "seconds_to_all_minors": e2e_s}
+        c1 = eng.counters()
+        e2e = {"value": total_work / e2e_s, "unit": "limb-MAC/s",
+               "h2d_bytes_per_step": int((c1["h2d_bytes"] - c0["h2d_bytes"]) / args.steps),
+               "d2h_bytes_per_step": int((c1["d2h_bytes"] - c0["d2h_bytes"]) / args.steps),
+               "bytes_counted_by": "ds_counters (every ABI host<->device copy of this context)",
+               "seconds_to_all_minors": e2e_s,
+               "includes": "H2D matrix, elimination, D2H pivots/dets/signed+normalized minors/final L\\U matrix"}
     # ---- roofline of the dominant kernel: the update (tensor-core engine)
     # algorithmic bytes per updated element: read + write a_jk (L limbs + exp + cls)
     elems = upd_work / (L * L) if L else 0.0
@@ -370,33 +461,47 @@ def main():
     counters = eng.counters()
     engine_name = ("k_update_tc (ds_tc.cu): tcgen05.mma kind::i8 digit products in TMEM + rounding epilogue"
                    if counters.get("tc_engine") else "k_fused (ds_update.cu): FP64 digit products + rounding epilogue")
+    prof = committed_profile(n, p)
     roof = {"kernel": engine_name, "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved_gbs / hbm_peak if hbm_peak else None, "traffic": committed_traffic(n, p, elems / upd_launches if upd_launches else 0.0),
+            "frac": achieved_gbs / hbm_peak if hbm_peak else None,
+            "traffic": (prof["dram_bytes_per_element"] * elems / upd_launches) if prof and upd_launches else None,
+            "traffic_per_element": prof.get("dram_bytes_per_element") if prof else None,
             "algorithmic_bytes_per_element": 2 * (4 * L + 5),
             "elements_per_step": elems / args.steps if args.steps else None,
             "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
             "launches_per_step": upd_launches / args.steps,
             "limb_mac_rate": upd_work / upd_s if upd_s > 0 else None,
             "peak_source": peak_src,
+            "limiter": prof.get("limiter") if prof else None,
+            "issue_active_frac": prof.get("issue_active_frac") if prof else None,
+            "tensor_pipe_frac": prof.get("tensor_pipe_frac") if prof else None,
+            "ncu_source": prof.get("source") if prof else None,
             "tc_fallback_elements": counters.get("tc_fallback_elements"),
             "note": "achieved = algorithmic bytes (read+write of every updated a_jk) / summed update-kernel time "
-                    "(CUDA events on the launch stream); the kernel is bound by integer issue in the rounding "
-                    "epilogue, not by HBM or the tensor cores -- see profiles/ for issue/pipe utilisation"}
+                    "(CUDA events on the launch stream); bound = the HBM roof the kernel is measured against; "
+                    "limiter / issue / tensor-pipe fractions from the committed ncu --set full capture"}
+    parity = None
+    if world == 1 and not args.no_parity and not args.no_e2e:
+        try:
+            parity = parity_leg(args, A, res, final, lambda: DeviceElimination(n, p, "real", local))
+        except Exception as exc:  # reported, never hidden
+            parity = {"ok": False, "error": repr(exc)}
     out = None
     if rank == 0:
         cpu = None
         if not args.no_cpu and world == 1:  # rank 0 at N=1 only
             try:
-                cpu = cpu_reference(n, p, args.cpu_seconds, A)
+                cpu = cpu_reference(n, p, args.cpu_seconds)
             except Exception as exc:  # never fail the GPU line on the baseline
                 cpu = {"error": repr(exc)}
         out = {"metric": f"limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N={n} @{p}b",
                "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "u8 digit products (tcgen05 kind::i8, s32 accumulate) + u32 limbs", "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
+               "dtype": "u8 digit products (tcgen05 kind::i8, s32 accumulate) + u32 limbs",
+               "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
                "config": workload(args, desc), "seconds_to_all_minors": ms / 1e3,
                "input_generation_s": gen_s,
-               "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
+               "e2e": e2e, "roofline": roof, "parity": parity, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
                "clocks": clk.summary(), "parallelism": f"row-cyclic x{world}"}
         emit_json(out)
     eng.close()

@@ -96,12 +96,17 @@ int ds_create(ds_ctx **out, int n, long prec_bits, int kind, int device, int ran
               int world);
 void ds_destroy(ds_ctx *ctx);
 
-/* Copy the rows this rank owns from a full host matrix (count = n*n) into
- * HBM.  Replaces the initial row scatter of parexec.py:367-368. */
+/* Copy the rows this rank owns into HBM.  The host matrix is either the full
+ * n x n matrix (count = n*n; global row r at idx r*n + col) or only this
+ * rank's rows (count = nloc*n with nloc = #{r < n : r % world == rank}; local
+ * row jl = global row rank + jl*world at idx jl*n + col), so a rank of a
+ * sharded run never needs host memory for the other ranks' rows.  Replaces
+ * the initial row scatter of parexec.py:367-368. */
 int ds_load(ds_ctx *ctx, const ds_soa *host_matrix);
 
-/* Copy the rows this rank owns back into a full host matrix (count = n*n):
- * the in-place L\U state (elim.py:19-22; parexec.py:395-398). */
+/* Copy the rows this rank owns back into a host matrix -- full (count n*n)
+ * or owned rows only (count nloc*n), as for ds_load: the in-place L\U state
+ * (elim.py:19-22; parexec.py:395-398). */
 int ds_fetch(ds_ctx *ctx, ds_soa *host_matrix);
 
 /* Serial engine (world == 1): run pivot steps [start_step, stop_step) of
@@ -137,7 +142,8 @@ int ds_step(ds_ctx *ctx, int step, int collect_minors, int series);
  * seen, else the 0-based step.  Synchronises the context stream. */
 int ds_status(ds_ctx *ctx, int *failed_step);
 /* Copy trace (replicated on every rank) and the minors rows this rank owns
- * (row m-1 owned when (m-1) % world == rank) into `res`. */
+ * (row m-1 owned when (m-1) % world == rank) into `res`; the minors buffers
+ * are full (count n*n) or owned rows only (count nloc*n), as for ds_load. */
 int ds_results_fetch(ds_ctx *ctx, int upto_step, ds_results *res);
 /* Incremental form of ds_results_fetch for a serial context (world 1):
  * trace entries [t0, t1) (pivots / det_series) and the minors rows of leading
@@ -196,7 +202,9 @@ int ds_lookahead_mult(ds_ctx *ctx, int i1, const void *buf);
  * (short product undecided / normalisation uncertain), out[1] = 1 if the
  * tensor-core update engine is active, out[2] = 1 if the DFMA engine is,
  * out[3] = elements whose predicted normalisation (single-pass rounding) was
- * wrong and which went to the exact fallback.  Writes min(n, 4) values. */
+ * wrong and which went to the exact fallback, out[4] / out[5] = bytes copied
+ * host->device / device->host by this context's ABI calls since creation
+ * (ds_load, ds_fetch, results; the e2e accounting).  Writes min(n, 6) values. */
 int ds_counters(ds_ctx *ctx, int64_t *out, int n);
 
 /* Last error message of this context (or of the last failed ds_create when

@@ -89,6 +89,7 @@ struct ds_ctx {
   UpdatePlan plan;
   TcPlan tc;  // tensor-core update (tcgen05 kind::i8), preferred when enabled
   int64_t launches;
+  int64_t h2d_bytes, d2h_bytes;  // host<->device bytes moved by the ABI copies (e2e accounting)
   int host_have_det;   // a det chain value exists (first step sets det = piv)
   int det_from_cur;    // next det product reads the ds_set_det seed in `cur`
   // pivot_mode="partial" (elim.py:204-208): per-step row swap flags [n] and the selected row
@@ -1011,32 +1012,53 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   return DS_OK;
 }
 
+// host matrix layouts accepted by ds_load / ds_fetch / ds_results_fetch: the
+// full n x n matrix (count n*n; this rank's row jl is global row rank +
+// jl*world) or only the rows this rank owns (count nloc*n, row jl at jl*n).
+// Returns the first host row and the host row stride of local row 0, 1, ...
+static bool host_rows(const ds_ctx* ctx, int64_t count, int64_t* r0, int64_t* rs) {
+  const int64_t n = ctx->n;
+  if (count == n * n) {
+    *r0 = ctx->rank;
+    *rs = ctx->world;
+    return true;
+  }
+  if (count == (int64_t)ctx->nloc * n) {
+    *r0 = 0;
+    *rs = 1;
+    return true;
+  }
+  return false;
+}
+
 int ds_load(ds_ctx* ctx, const ds_soa* h) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
   int n = ctx->n, L = ctx->L;
-  if (h->count != (int64_t)n * n) return DS_INVALID;
+  int64_t r0, rs;
+  if (!host_rows(ctx, h->count, &r0, &rs)) return DS_INVALID;
   // gather owned rows (row-cyclic) plane by plane; contiguous when world == 1
+  // or when the caller passes only its owned rows
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++) {
       const uint32_t* src = h->limbs + ((int64_t)c * L + l) * h->count;
       uint32_t* dst = ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count;
-      if (ctx->world == 1) {
-        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * h->count, cudaMemcpyHostToDevice, ctx->stream));
+      if (rs == 1) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * ctx->a_count, cudaMemcpyHostToDevice, ctx->stream));
       } else {
-        CK(cudaMemcpy2DAsync(dst, sizeof(uint32_t) * n, src + (int64_t)ctx->rank * n,
-                             sizeof(uint32_t) * n * ctx->world, sizeof(uint32_t) * n, ctx->nloc,
-                             cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpy2DAsync(dst, sizeof(uint32_t) * n, src + r0 * n, sizeof(uint32_t) * n * rs,
+                             sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
       }
     }
     const int32_t* se = h->exp + (int64_t)c * h->count;
     const uint8_t* sc = h->cls + (int64_t)c * h->count;
-    CK(cudaMemcpy2DAsync(ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, se + (int64_t)ctx->rank * n,
-                         sizeof(int32_t) * n * ctx->world, sizeof(int32_t) * n, ctx->nloc, cudaMemcpyHostToDevice,
+    CK(cudaMemcpy2DAsync(ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, se + r0 * n,
+                         sizeof(int32_t) * n * rs, sizeof(int32_t) * n, ctx->nloc, cudaMemcpyHostToDevice,
                          ctx->stream));
-    CK(cudaMemcpy2DAsync(ctx->a_cls + (int64_t)c * ctx->a_count, n, sc + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+    CK(cudaMemcpy2DAsync(ctx->a_cls + (int64_t)c * ctx->a_count, n, sc + r0 * n, (size_t)n * rs,
                          n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
   }
+  ctx->h2d_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
   // reset run state
   ctx->host_have_det = 0;
   ctx->la_step = -1;
@@ -1052,20 +1074,22 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
 int ds_fetch(ds_ctx* ctx, ds_soa* h) {
   CK(cudaSetDevice(ctx->device));
   int n = ctx->n, L = ctx->L;
-  if (h->count != (int64_t)n * n) return DS_INVALID;
+  int64_t r0, rs;
+  if (!host_rows(ctx, h->count, &r0, &rs)) return DS_INVALID;
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++) {
       uint32_t* dst = h->limbs + ((int64_t)c * L + l) * h->count;
       const uint32_t* src = ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count;
-      CK(cudaMemcpy2DAsync(dst + (int64_t)ctx->rank * n, sizeof(uint32_t) * n * ctx->world, src, sizeof(uint32_t) * n,
+      CK(cudaMemcpy2DAsync(dst + r0 * n, sizeof(uint32_t) * n * rs, src, sizeof(uint32_t) * n,
                            sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    CK(cudaMemcpy2DAsync(h->exp + (int64_t)c * h->count + (int64_t)ctx->rank * n, sizeof(int32_t) * n * ctx->world,
+    CK(cudaMemcpy2DAsync(h->exp + (int64_t)c * h->count + r0 * n, sizeof(int32_t) * n * rs,
                          ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
                          cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpy2DAsync(h->cls + (int64_t)c * h->count + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+    CK(cudaMemcpy2DAsync(h->cls + (int64_t)c * h->count + r0 * n, (size_t)n * rs,
                          ctx->a_cls + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
   }
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
   CK(cudaStreamSynchronize(ctx->stream));
   return DS_OK;
 }
@@ -1459,9 +1483,9 @@ int ds_counters(ds_ctx* ctx, int64_t* out, int n) {
   int32_t st[8];
   CK(cudaMemcpyAsync(st, ctx->status, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  int64_t v[4] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.fused && !ctx->tc.enabled) ? 1 : 0,
-                  (int64_t)(uint32_t)st[7]};
-  for (int q = 0; q < n && q < 4; q++) out[q] = v[q];
+  int64_t v[6] = {(int64_t)(uint32_t)st[6], ctx->tc.enabled ? 1 : 0, (ctx->plan.fused && !ctx->tc.enabled) ? 1 : 0,
+                  (int64_t)(uint32_t)st[7], ctx->h2d_bytes, ctx->d2h_bytes};
+  for (int q = 0; q < n && q < 6; q++) out[q] = v[q];
   return DS_OK;
 }
 
@@ -1506,6 +1530,7 @@ static int copy_vec(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32
                     int64_t src_count, int64_t n_items) {
   if (!dst || !dst->limbs || n_items <= 0) return DS_OK;
   int L = ctx->L;
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * n_items;
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++)
       CK(cudaMemcpyAsync(dst->limbs + ((int64_t)c * L + l) * dst->count, limbs + ((int64_t)c * L + l) * src_count,
@@ -1526,6 +1551,7 @@ static int copy_row_range(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const
   const int n = ctx->n, L = ctx->L;
   const size_t rows = (size_t)(r1 - r0);
   const int64_t o = (int64_t)r0 * n;
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * (int64_t)rows * width;
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++)
       CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + o, sizeof(uint32_t) * n,
@@ -1553,17 +1579,20 @@ static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int3
   // full n*n host matrix
   if (!dst || !dst->limbs) return DS_OK;
   int n = ctx->n, L = ctx->L;
+  int64_t r0, rs;
+  if (!host_rows(ctx, dst->count, &r0, &rs)) return DS_INVALID;
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++)
-      CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + (int64_t)ctx->rank * n,
-                           sizeof(uint32_t) * n * ctx->world, limbs + ((int64_t)c * L + l) * ctx->a_count,
+      CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + r0 * n,
+                           sizeof(uint32_t) * n * rs, limbs + ((int64_t)c * L + l) * ctx->a_count,
                            sizeof(uint32_t) * n, sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + (int64_t)ctx->rank * n, sizeof(int32_t) * n * ctx->world,
+    CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + r0 * n, sizeof(int32_t) * n * rs,
                          ex + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
                          cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + (int64_t)ctx->rank * n, (size_t)n * ctx->world,
+    CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + r0 * n, (size_t)n * rs,
                          cl + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
   }
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
   return DS_OK;
 }
 
@@ -1589,6 +1618,7 @@ static int results_fetch_from(ds_ctx* ctx, int upto, ds_results* r, int minors_f
     // flags of rows this rank owns (m-1 % world == rank)
     uint8_t* tmp = (uint8_t*)malloc(ctx->n);
     CK(cudaMemcpyAsync(tmp, ctx->row_flags, ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->d2h_bytes += ctx->n;
     CK(cudaStreamSynchronize(ctx->stream));
     for (int m1 = ctx->rank; m1 < ctx->n; m1 += ctx->world) r->row_flags[m1] = tmp[m1];
     free(tmp);
@@ -1618,6 +1648,7 @@ int ds_results_fetch_range(ds_ctx* ctx, int t0, int t1, int m0, int m1, ds_resul
     for (int v = 0; v < 2; v++) {
       ds_soa* d = vs[v];
       if (!d->limbs) continue;
+      ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * cnt;
       for (int c = 0; c < ctx->ncomp; c++) {
         for (int l = 0; l < L; l++)
           CK(cudaMemcpyAsync(d->limbs + ((int64_t)c * L + l) * d->count + t0, sl[v] + ((int64_t)c * L + l) * n + t0,
@@ -1637,9 +1668,11 @@ int ds_results_fetch_range(ds_ctx* ctx, int t0, int t1, int m0, int m1, ds_resul
     if ((rc = copy_row_range(ctx, &r->normalized, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls, m0 - 1, m1 - 1, m1 - 1,
                              ctx->stream)) != DS_OK)
       return rc;
-    if (r->row_flags)
+    if (r->row_flags) {
       CK(cudaMemcpyAsync(r->row_flags + (m0 - 1), ctx->row_flags + (m0 - 1), (size_t)(m1 - m0),
                          cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->d2h_bytes += m1 - m0;
+    }
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return DS_OK;

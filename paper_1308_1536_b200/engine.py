@@ -183,10 +183,10 @@ class DeviceElimination:
 
     def counters(self) -> dict:
         """Internal engine counters (ds_counters): tensor-core fallback elements, active update engine."""
-        out = (ctypes.c_int64 * 4)()
-        _check(self.lib.ds_counters(self.ctx, out, 4), self.ctx, "ds_counters", self.rank)
+        out = (ctypes.c_int64 * 6)()
+        _check(self.lib.ds_counters(self.ctx, out, 6), self.ctx, "ds_counters", self.rank)
         return {"tc_fallback_elements": int(out[0]), "tc_engine": bool(out[1]), "dfma_engine": bool(out[2]),
-                "direct_mispredictions": int(out[3])}
+                "direct_mispredictions": int(out[3]), "h2d_bytes": int(out[4]), "d2h_bytes": int(out[5])}
 
     # -- multi-rank lookahead (ds_lookahead_*) ------------------------------
     def lookahead_enable(self, limit: int):

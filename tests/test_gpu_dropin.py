@@ -142,3 +142,81 @@ def test_par_eliminate_sink_order():
     got = []
     par_eliminate(A, 3, transport="local", sink=got.append)
     assert [r.n for r in got] == list(range(2, A.n + 1))
+
+
+@pytest.mark.parametrize("name,workers", [("uniform30_s4_p256", 2), ("complex8_s9_p192", 3), ("zero_pivot3", 2)])
+def test_par_eliminate_process_spawns_its_own_ranks(name, workers):
+    """transport="process" from a plain process forks the worker ranks itself (ref
+    parexec.py:350-405); with fewer GPUs than ranks they share the GPU and broadcast over gloo
+    through a pinned staging copy."""
+    meta, A = _buffer(name)
+    try:
+        trace, minors, stats = par_eliminate(A, workers, transport="process")
+        assert stats.broadcasts == A.n
+    except ZeroPivot as exc:
+        assert exc.step == meta["zero_pivot_step"]
+        trace, minors = exc.trace, exc.series
+    assert _digest(trace, minors, A) == meta["digest"]
+
+
+def test_owned_rows_only_host_buffers():
+    """ds_load / ds_fetch / ds_results_fetch with owned-rows-only host buffers (count nloc*n):
+    three virtual shards driven step by step give the serial engine's bits."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_1308_1536_b200.engine import DeviceElimination, HostResults
+    from paper_1308_1536_b200.soa import SoA
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    n, p, world = 150, 1024, 3
+    A = random_uniform_soa(n, p, seed=5)
+    with DeviceElimination(n, p, "real") as e:
+        e.load(A)
+        ref = HostResults.alloc(n, 1, e.L, True)
+        e.run(True, True, 0, n, ref)
+        fin_ref = A.copy()
+        e.fetch(fin_ref)
+    L = (p + 31) // 32
+    ranks = [DeviceElimination(n, p, "real", 0, r, world) for r in range(world)]
+    try:
+        for r, e in enumerate(ranks):
+            rows = np.arange(r, n, world)
+            own = SoA(1, L, len(rows) * n,
+                      np.ascontiguousarray(A.limbs.reshape(1, L, n, n)[:, :, rows, :].reshape(1, L, -1)),
+                      np.ascontiguousarray(A.exp.reshape(1, n, n)[:, rows, :].reshape(1, -1)),
+                      np.ascontiguousarray(A.cls.reshape(1, n, n)[:, rows, :].reshape(1, -1)))
+            e.load(own)
+        for i in range(n):
+            owner = ranks[i % world]
+            owner.stage(i)
+            for e in ranks:
+                if e is not owner:
+                    assert e.lib.ds_pivot_copy(e.ctx, owner.ctx) == 0
+            for e in ranks:
+                e.step(i, True, True)
+        for r, e in enumerate(ranks):
+            rows = np.arange(r, n, world)
+            nloc = len(rows)
+            fin = SoA(1, L, nloc * n)
+            e.fetch(fin)
+            res = HostResults(SoA(1, L, n), SoA(1, L, n), SoA(1, L, nloc * n), SoA(1, L, nloc * n),
+                              np.zeros(n, dtype=np.uint8))
+            e.results(n, res)
+            assert np.array_equal(fin.limbs.reshape(1, L, nloc, n), fin_ref.limbs.reshape(1, L, n, n)[:, :, rows])
+            assert np.array_equal(fin.exp.reshape(1, nloc, n), fin_ref.exp.reshape(1, n, n)[:, rows])
+            assert np.array_equal(res.dets.limbs, ref.dets.limbs)
+            for jl, g in enumerate(rows):
+                m = g + 1
+                if m < 2:
+                    continue
+                sl = slice(jl * n, jl * n + m)
+                gl = slice(g * n, g * n + m)
+                assert res.row_flags[g] == ref.row_flags[g]
+                assert np.array_equal(res.signed.limbs[:, :, sl], ref.signed.limbs[:, :, gl])
+                assert np.array_equal(res.normalized.exp[:, sl], ref.normalized.exp[:, gl])
+            c = e.counters()
+            assert c["h2d_bytes"] == nloc * n * (4 * L + 5)
+    finally:
+        for e in ranks:
+            e.close()
