@@ -368,7 +368,10 @@ def main():
             return float(t.item())
     A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world, agree=agree)  # this rank's rows
     eng = DeviceElimination(n, p, "real", local, rank, world)
-    stream = torch.cuda.current_stream()
+    # a dedicated stream (the legacy default stream's handle 0 would mean "own stream" to
+    # ds_set_stream): kernels, NCCL broadcasts and the timing events share its order
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     pivot = None
     if use_dist:
         from paper_1308_1536_b200.parexec import dist_run

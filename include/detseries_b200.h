@@ -104,6 +104,22 @@ void ds_destroy(ds_ctx *ctx);
  * the initial row scatter of parexec.py:367-368. */
 int ds_load(ds_ctx *ctx, const ds_soa *host_matrix);
 
+/* Copy host rows into HBM like ds_load but keep the run state (det chain,
+ * emitted rows, abort flag): a step_hook that edited the in-place buffer
+ * mid-run (elim.py:227-228) hands its rows back before the next step. */
+int ds_update_rows(ds_ctx *ctx, const ds_soa *host_matrix);
+
+/* Device-side builder (no host matrix): fill this rank's rows with family
+ * `family` -- DS_FAMILY_RANDOM_UNIFORM: x = 2U - 1, U a p-bit uniform
+ * (genmat.synth_matrix("random_uniform"), genmat.py:242-246) -- drawn from
+ * the counter-based "ds-splitmix" generator (element (row, col)
+ * is a pure function of seed, row, col and p, so every rank count and the
+ * host twin synth.counter_uniform_soa give the same matrix).  The bits differ
+ * from gmpy2's Mersenne-twister stream; the distribution is the reference's.
+ * Resets the run state like ds_load.  Real matrices only. */
+#define DS_FAMILY_RANDOM_UNIFORM 0
+int ds_generate(ds_ctx *ctx, int family, uint64_t seed);
+
 /* Copy the rows this rank owns back into a host matrix -- full (count n*n)
  * or owned rows only (count nloc*n), as for ds_load: the in-place L\U state
  * (elim.py:19-22; parexec.py:395-398). */
@@ -152,6 +168,26 @@ int ds_results_fetch(ds_ctx *ctx, int upto_step, ds_results *res);
  * hand each MinorRow to its sink as the row finalises (elim.py:220-226)
  * instead of after the whole run.  Synchronises the context streams. */
 int ds_results_fetch_range(ds_ctx *ctx, int t0, int t1, int m0, int m1, ds_results *res);
+/* Streaming of the minors rows to the host (the output
+ * volume equals the matrix, ~416 GB at config 5, so it cannot stay resident).
+ * After ds_stream_minors(ctx, batch_steps, cb, user) the context keeps only a
+ * ring of minors rows in HBM (3 flush intervals) and every flush -- ds_run
+ * calls it every batch_steps steps and at its end, a multi-rank driver calls
+ * it itself at least every batch_steps steps -- copies the owned rows
+ * finalised since the previous flush into pinned staging on the side stream
+ * and hands the PREVIOUS batch to cb (so the copy overlaps the caller's
+ * work).  cb(g0, stride, nrows, signed, normalized, flags, user): rows of
+ * leading sizes m_r = g0 + r*stride + 1 (r < nrows; g is the global row,
+ * stride = world) hold their m_r entries at [r*n, r*n + m_r) of signed /
+ * normalized (ds SoA, valid only during the call); flags[r] = row_flags of
+ * that size (bit0 emitted, bit1 normalized defined).  Rows arrive in
+ * increasing size, like sink calls (elim.py:220-226).  batch_steps <= 0 turns
+ * streaming off (minors resident again, fetched by ds_results_fetch).
+ * final = 1 waits for and delivers everything up to upto_step. */
+typedef void (*ds_rows_cb)(int g0, int stride, int nrows, const ds_soa *signed_rows,
+                           const ds_soa *normalized_rows, const uint8_t *flags, void *user);
+int ds_stream_minors(ds_ctx *ctx, int batch_steps, ds_rows_cb cb, void *user);
+int ds_stream_flush(ds_ctx *ctx, int upto_step, int final);
 /* Seed the device det chain (resume, elim.py:201): det = host scalar. */
 int ds_set_det(ds_ctx *ctx, const ds_soa *det1);
 

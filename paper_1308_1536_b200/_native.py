@@ -27,7 +27,8 @@ EXPORTS = ("ds_version", "ds_create", "ds_destroy", "ds_load", "ds_fetch", "ds_r
            "ds_launch_count", "ds_last_error", "ds_scalar_op", "ds_set_stream", "ds_use_pivot_buffer",
            "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters", "ds_lookahead_enable", "ds_lookahead_stream",
            "ds_lookahead_pivot", "ds_lookahead_mult", "ds_set_pivot_mode", "ds_swaps_fetch",
-           "ds_results_fetch_range")
+           "ds_results_fetch_range", "ds_generate", "ds_stream_minors", "ds_stream_flush",
+           "ds_update_rows")
 
 
 class ds_results(ctypes.Structure):
@@ -60,6 +61,10 @@ def load_library(path: str = LIB_PATH):
         "ds_status": (I, [VP, P(I)]),
         "ds_results_fetch": (I, [VP, I, P(ds_results)]),
         "ds_results_fetch_range": (I, [VP, I, I, I, I, P(ds_results)]),
+        "ds_generate": (I, [VP, I, ctypes.c_uint64]),
+        "ds_stream_minors": (I, [VP, I, VP, VP]),
+        "ds_stream_flush": (I, [VP, I, I]),
+        "ds_update_rows": (I, [VP, P(ds_soa)]),
         "ds_set_det": (I, [VP, S]),
         "ds_stream": (VP, [VP]),
         "ds_launch_count": (ctypes.c_int64, [VP]),

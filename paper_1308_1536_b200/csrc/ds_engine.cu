@@ -18,6 +18,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "ds_mp.cuh"
@@ -68,6 +69,23 @@ struct ds_ctx {
   int32_t *sig_exp, *nrm_exp;
   uint8_t *sig_cls, *nrm_cls;
   uint8_t* row_flags;  // [n]
+  // minors storage: m_rows local rows (all nloc, or a ring while streaming), plane stride m_count
+  int m_rows;
+  int64_t m_count;
+  // streaming of minors rows to the host (ds_stream_minors / ds_stream_flush)
+  int st_batch;              // max steps between flushes (ring sized for it); 0 = off
+  ds_rows_cb st_cb;
+  void* st_user;
+  int st_next;               // first global row not yet copied
+  int st_set;                // staging set of the copy in flight
+  int st_pending;            // a copy is in flight in set st_set
+  int st_pend_g0, st_pend_rows, st_pend_width;
+  int st_rows_cap;           // rows per staging set
+  uint32_t* st_limbs[2][2];  // [set][signed / normalized] pinned host staging
+  int32_t* st_exp[2][2];
+  uint8_t* st_cls[2][2];
+  uint8_t* st_flags[2];
+  cudaEvent_t st_ev[2];
   // status: [0] failed step (-1), [1] have_det, [2] range error count, [3] warnings
   int32_t* status;
   // per-thread scratch for the general engine
@@ -210,6 +228,7 @@ struct KArgs {
   uint8_t* row_flags;
   int32_t* status;
   uint32_t* scratch; int64_t scratch_threads; int64_t scratch_words;
+  int64_t m_count; int m_rows;  // minors storage: plane stride, ring rows (local row jl -> slot jl % m_rows)
 };
 
 static KArgs kargs(ds_ctx* c) {
@@ -225,8 +244,12 @@ static KArgs kargs(ds_ctx* c) {
   k.sig_limbs = c->sig_limbs; k.nrm_limbs = c->nrm_limbs; k.sig_exp = c->sig_exp; k.nrm_exp = c->nrm_exp;
   k.sig_cls = c->sig_cls; k.nrm_cls = c->nrm_cls; k.row_flags = c->row_flags; k.status = c->status;
   k.scratch = c->scratch; k.scratch_threads = c->scratch_threads; k.scratch_words = c->scratch_words;
+  k.m_count = c->m_count; k.m_rows = c->m_rows;
   return k;
 }
+
+// first element of local row jl's minors slot (ring of m_rows rows)
+__device__ __forceinline__ int64_t mrow(const KArgs& k, int64_t jl) { return (jl % k.m_rows) * k.n; }
 
 __device__ __forceinline__ Ptr thread_scratch(const KArgs& k, int64_t tid) {
   return Ptr{k.scratch + tid, k.scratch_threads};
@@ -464,7 +487,9 @@ __global__ void k_neg_z(KArgs k, int i, int jl0) {
 // complex minors, one thread per (entry, component): signed_k = RN(det_i * L_mk)
 // (cmul_part per component), normalized = RN(signed_k / signed_0) (cdiv_part)
 __global__ void k_emit_signed_c2(KArgs k, int i) {
-  if (k.status[0] >= 0) return;
+  // side stream: a zero pivot found by a LATER step must not cancel this row (elim.py:220-226
+  // emits size i+2 before step i+1 raises)
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -474,7 +499,7 @@ __global__ void k_emit_signed_c2(KArgs k, int i) {
     const int c = (int)(t & 1);
     const int64_t kk = t >> 1;
     int64_t oidx = jl * k.n + kk;
-    Out so = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, c, k.L, oidx);
+    Out so = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, c, k.L, mrow(k, jl) + kk);
     if (kk == m - 1) {
       set_val(so, c == 0 ? d0 : d1, k.L);
       continue;
@@ -488,21 +513,22 @@ __global__ void k_emit_signed_c2(KArgs k, int i) {
 }
 
 __global__ void k_emit_norm_c2(KArgs k, int i) {
-  if (k.status[0] >= 0) return;
+  if (k.status[0] >= 0 && k.status[0] <= i) return;  // see k_emit_signed_c2
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
-  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 1, k.L, jl * k.n);
+  const int64_t r0 = mrow(k, jl);
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
+  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, r0);
   bool lead_zero = is_zero_cls(l0.c) && is_zero_cls(l1.c);
   if (tid == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
   if (lead_zero) return;
   for (int64_t t = tid; t < 2 * (int64_t)m; t += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(t & 1);
-    int64_t idx = jl * k.n + (t >> 1);
-    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
-    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 1, k.L, idx);
-    Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, c, k.L, idx);
+    int64_t idx = r0 + (t >> 1);
+    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx);
+    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, idx);
+    Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, c, k.L, idx);
     if (!cdiv_part(o.m, o.e, o.c, s0, s1, l0, l1, c == 1, k.L, k.p, thread_scratch(k, tid),
                    (unsigned int*)&k.status[3]))
       atomicAdd(&k.status[2], 1);
@@ -574,9 +600,9 @@ __global__ void k_emit_signed(KArgs k, int i) {
   Val d0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);  // det_i (k_pivot / k_det_step)
   Val d1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
   for (int64_t kk = tid; kk < m; kk += (int64_t)gridDim.x * blockDim.x) {
-    int64_t oidx = jl * k.n + kk;
-    Out s0 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, oidx);
-    Out s1 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, oidx);
+    int64_t oidx = mrow(k, jl) + kk;
+    Out s0 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, oidx);
+    Out s1 = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, k.ncomp - 1, k.L, oidx);
     if (kk == m - 1) {
       set_val(s0, d0, k.L);
       if (k.kind == DS_KIND_COMPLEX) set_val(s1, d1, k.L);
@@ -596,17 +622,18 @@ __global__ void k_emit_norm(KArgs k, int i) {
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
-  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, jl * k.n);
+  const int64_t r0 = mrow(k, jl);
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
+  Val l1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, k.ncomp - 1, k.L, r0);
   bool lead_zero = is_zero_cls(l0.c) && (k.kind == DS_KIND_REAL || is_zero_cls(l1.c));
   if (tid == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
   if (lead_zero) return;
   for (int64_t kk = tid; kk < m; kk += (int64_t)gridDim.x * blockDim.x) {
-    int64_t idx = jl * k.n + kk;
-    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
-    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, k.ncomp - 1, k.L, idx);
-    Out o0 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, 0, k.L, idx);
-    Out o1 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, k.ncomp - 1, k.L, idx);
+    int64_t idx = r0 + kk;
+    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx);
+    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, k.ncomp - 1, k.L, idx);
+    Out o0 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, 0, k.L, idx);
+    Out o1 = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, k.ncomp - 1, k.L, idx);
     Ptr tmp = thread_scratch(k, tid);
     if (!g_div(o0, o1, s0, s1, l0, l1, k.kind, k.L, k.p, tmp, (unsigned int*)&k.status[3]))
       atomicAdd(&k.status[2], 1);
@@ -735,13 +762,14 @@ __global__ void k_emit_norm_w(KArgs k, int i, int wwords) {
   int m = i + 2;
   int64_t jl = (i + 1) / k.world;
   const int64_t kk = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, jl * k.n);
+  const int64_t r0 = mrow(k, jl);
+  Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
   bool lead_zero = is_zero_cls(l0.c);
   if (blockIdx.x == 0 && threadIdx.x == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
   if (lead_zero || kk >= m) return;
-  int64_t idx = jl * k.n + kk;
-  Val s = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, 0, k.L, idx);
-  Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.a_count, 0, k.L, idx);
+  int64_t idx = r0 + kk;
+  Val s = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx);
+  Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, 0, k.L, idx);
   wdiv_rn<K>(o, s, l0, k.L, k.p, wsm + warp * wwords, k.status);
 }
 
@@ -780,10 +808,10 @@ __global__ void k_pivot_lite(KArgs k, int i, int first) {
 __global__ void k_emit_last(KArgs k, int i) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;
   int64_t jl = (i + 1) / k.world;
-  int64_t idx = jl * k.n + (i + 1);
+  int64_t idx = mrow(k, jl) + (i + 1);
   for (int c = 0; c < k.ncomp; c++) {
     Val d = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, c, k.L, i);
-    Out o = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.a_count, c, k.L, idx);
+    Out o = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, c, k.L, idx);
     for (int l = threadIdx.x; l < k.L; l += blockDim.x) o.m[l] = d.m[l];
     if (threadIdx.x == 0) {
       *o.e = (int32_t)d.e;
@@ -813,6 +841,47 @@ static int dmalloc(ds_ctx* ctx, T** p, size_t count) {
     return e == cudaErrorMemoryAllocation ? DS_OOM : DS_CUDA;
   }
   return DS_OK;
+}
+
+static int ensure_minors(ds_ctx* ctx) {
+  if (ctx->sig_limbs) return DS_OK;
+  const int64_t nc = ctx->ncomp, L = ctx->L, cnt = ctx->m_count;
+  int rc;
+  if ((rc = dmalloc(ctx, &ctx->sig_limbs, (size_t)(nc * L * cnt))) != DS_OK ||
+      (rc = dmalloc(ctx, &ctx->sig_exp, (size_t)(nc * cnt))) != DS_OK ||
+      (rc = dmalloc(ctx, &ctx->sig_cls, (size_t)(nc * cnt))) != DS_OK ||
+      (rc = dmalloc(ctx, &ctx->nrm_limbs, (size_t)(nc * L * cnt))) != DS_OK ||
+      (rc = dmalloc(ctx, &ctx->nrm_exp, (size_t)(nc * cnt))) != DS_OK ||
+      (rc = dmalloc(ctx, &ctx->nrm_cls, (size_t)(nc * cnt))) != DS_OK)
+    return rc;
+  return DS_OK;
+}
+
+static void minors_free(ds_ctx* ctx) {
+  void* ptrs[] = {ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  ctx->sig_limbs = ctx->nrm_limbs = nullptr;
+  ctx->sig_exp = ctx->nrm_exp = nullptr;
+  ctx->sig_cls = ctx->nrm_cls = nullptr;
+}
+
+static void stream_free(ds_ctx* ctx) {
+  for (int st = 0; st < 2; st++) {
+    for (int v = 0; v < 2; v++) {
+      if (ctx->st_limbs[st][v]) cudaFreeHost(ctx->st_limbs[st][v]);
+      if (ctx->st_exp[st][v]) cudaFreeHost(ctx->st_exp[st][v]);
+      if (ctx->st_cls[st][v]) cudaFreeHost(ctx->st_cls[st][v]);
+      ctx->st_limbs[st][v] = nullptr;
+      ctx->st_exp[st][v] = nullptr;
+      ctx->st_cls[st][v] = nullptr;
+    }
+    if (ctx->st_flags[st]) cudaFreeHost(ctx->st_flags[st]);
+    ctx->st_flags[st] = nullptr;
+    if (ctx->st_ev[st]) cudaEventDestroy(ctx->st_ev[st]);
+    ctx->st_ev[st] = nullptr;
+  }
+  ctx->st_batch = 0;
 }
 
 extern "C" {
@@ -892,6 +961,7 @@ void ds_destroy(ds_ctx* ctx) {
   if (ctx->snap_exp) cudaFree(ctx->snap_exp);
   if (ctx->snap_cls) cudaFree(ctx->snap_cls);
   for (cudaEvent_t ev : ctx->prof_ev) cudaEventDestroy(ev);
+  stream_free(ctx);
   if (ctx->ev) cudaEventDestroy(ctx->ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -954,12 +1024,10 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   AL(ctx->piv_limbs, (int64_t)nc * L * n); AL(ctx->piv_exp, (int64_t)nc * n); AL(ctx->piv_cls, (int64_t)nc * n);
   AL(ctx->det_limbs, (int64_t)nc * L * n); AL(ctx->det_exp, (int64_t)nc * n); AL(ctx->det_cls, (int64_t)nc * n);
   AL(ctx->cur_limbs, (int64_t)nc * L); AL(ctx->cur_exp, nc); AL(ctx->cur_cls, nc);
-  AL(ctx->sig_limbs, (int64_t)nc * L * ctx->a_count);
-  AL(ctx->sig_exp, (int64_t)nc * ctx->a_count);
-  AL(ctx->sig_cls, (int64_t)nc * ctx->a_count);
-  AL(ctx->nrm_limbs, (int64_t)nc * L * ctx->a_count);
-  AL(ctx->nrm_exp, (int64_t)nc * ctx->a_count);
-  AL(ctx->nrm_cls, (int64_t)nc * ctx->a_count);
+  // minors storage is allocated on first use (ensure_minors): all owned rows, or
+  // the ring set up by ds_stream_minors
+  ctx->m_rows = ctx->nloc > 0 ? ctx->nloc : 1;
+  ctx->m_count = ctx->a_count > 0 ? ctx->a_count : 32;
   AL(ctx->row_flags, n);
   AL(ctx->status, 8);
   int sms = 148;
@@ -1031,6 +1099,128 @@ static bool host_rows(const ds_ctx* ctx, int64_t count, int64_t* r0, int64_t* rs
   return false;
 }
 
+// fresh run state after new matrix contents (ds_load, ds_generate)
+static int reset_run_state(ds_ctx* ctx) {
+  const int n = ctx->n;
+  ctx->host_have_det = 0;
+  ctx->la_step = -1;
+  ctx->det_from_cur = 0;
+  CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
+  if (ctx->swaps) CK(cudaMemsetAsync(ctx->swaps, 0, n, ctx->stream));
+  int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->st_next = 1;
+  ctx->st_pending = 0;
+  return DS_OK;
+}
+
+static int copy_row_range_to(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
+                             int r0, int r1, int width, cudaStream_t s, int hrow0);
+
+// ---- streaming of minors rows (ds_stream_minors / ds_stream_flush)
+int ds_stream_minors(ds_ctx* ctx, int batch_steps, ds_rows_cb cb, void* user) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->side));
+  stream_free(ctx);
+  int ring = ctx->nloc > 0 ? ctx->nloc : 1;
+  const int per = batch_steps > 0 ? batch_steps / ctx->world + 2 : 0;
+  if (batch_steps > 0 && cb) ring = std::min(ring, 3 * per);
+  if (ring != ctx->m_rows) {
+    minors_free(ctx);
+    ctx->m_rows = ring;
+    ctx->m_count = (((int64_t)ring * ctx->n) + 31) & ~(int64_t)31;
+  }
+  if (batch_steps <= 0 || !cb) return DS_OK;
+  const size_t cnt = (size_t)per * ctx->n, nc = ctx->ncomp, L = ctx->L;
+  for (int st = 0; st < 2; st++) {
+    for (int v = 0; v < 2; v++) {
+      if (cudaMallocHost((void**)&ctx->st_limbs[st][v], sizeof(uint32_t) * nc * L * cnt) != cudaSuccess ||
+          cudaMallocHost((void**)&ctx->st_exp[st][v], sizeof(int32_t) * nc * cnt) != cudaSuccess ||
+          cudaMallocHost((void**)&ctx->st_cls[st][v], nc * cnt) != cudaSuccess) {
+        cudaGetLastError();
+        stream_free(ctx);
+        ctx->err = "pinned staging for the minors stream could not be allocated";
+        return DS_OOM;
+      }
+    }
+    CK(cudaMallocHost((void**)&ctx->st_flags[st], (size_t)per));
+    CK(cudaEventCreateWithFlags(&ctx->st_ev[st], cudaEventDisableTiming));
+  }
+  ctx->st_rows_cap = per;
+  ctx->st_batch = batch_steps;
+  ctx->st_cb = cb;
+  ctx->st_user = user;
+  ctx->st_next = 1;
+  ctx->st_pending = 0;
+  return DS_OK;
+}
+
+static void st_deliver(ds_ctx* ctx, int set, int g0, int nrows) {
+  const int64_t cnt = (int64_t)ctx->st_rows_cap * ctx->n;
+  ds_soa sg{ctx->st_limbs[set][0], ctx->st_exp[set][0], ctx->st_cls[set][0], cnt};
+  ds_soa nm{ctx->st_limbs[set][1], ctx->st_exp[set][1], ctx->st_cls[set][1], cnt};
+  ctx->st_cb(g0, ctx->world, nrows, &sg, &nm, ctx->st_flags[set], ctx->st_user);
+}
+
+int ds_stream_flush(ds_ctx* ctx, int upto_step, int final) {
+  if (!ctx->st_batch) return DS_OK;
+  CK(cudaSetDevice(ctx->device));
+  const int n = ctx->n, world = ctx->world, rank = ctx->rank;
+  // global rows g in [st_next, hi] are final after steps [0, upto_step)
+  const int hi = std::min(upto_step, n - 1);
+  int jl_a = ctx->st_next <= rank ? 0 : (ctx->st_next - rank + world - 1) / world;
+  int jl_b = hi < rank ? 0 : (hi - rank) / world + 1;
+  if (jl_b < jl_a) jl_b = jl_a;
+  const int nrows = jl_b - jl_a;
+  if (nrows > ctx->st_rows_cap) {
+    ctx->err = "ds_stream_flush: more rows finalised since the last flush than the stream batch allows";
+    return DS_INVALID;
+  }
+  int set = ctx->st_pending ? ctx->st_set ^ 1 : ctx->st_set;
+  const int g0 = rank + jl_a * world;
+  if (nrows > 0 && ctx->sig_limbs) {
+    // emission may have run on either stream: the copies (side stream) follow both
+    CK(cudaEventRecord(ctx->ev, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev, 0));
+    const int width = rank + (jl_b - 1) * world + 1;
+    const int64_t cnt = (int64_t)ctx->st_rows_cap * n;
+    ds_soa sg{ctx->st_limbs[set][0], ctx->st_exp[set][0], ctx->st_cls[set][0], cnt};
+    ds_soa nm{ctx->st_limbs[set][1], ctx->st_exp[set][1], ctx->st_cls[set][1], cnt};
+    int rc;
+    if ((rc = copy_row_range_to(ctx, &sg, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, jl_a, jl_b, width, ctx->side,
+                                0)) != DS_OK ||
+        (rc = copy_row_range_to(ctx, &nm, ctx->nrm_limbs, ctx->nrm_exp, ctx->nrm_cls, jl_a, jl_b, width, ctx->side,
+                                0)) != DS_OK)
+      return rc;
+    CK(cudaMemcpy2DAsync(ctx->st_flags[set], 1, ctx->row_flags + g0, world, 1, nrows, cudaMemcpyDeviceToHost,
+                         ctx->side));
+    ctx->d2h_bytes += nrows;
+    CK(cudaEventRecord(ctx->st_ev[set], ctx->side));
+  }
+  // hand the previous batch to the caller while this one copies
+  if (ctx->st_pending) {
+    const int old = ctx->st_set;
+    CK(cudaEventSynchronize(ctx->st_ev[old]));
+    st_deliver(ctx, old, ctx->st_pend_g0, ctx->st_pend_rows);
+    ctx->st_pending = 0;
+  }
+  if (nrows > 0 && ctx->sig_limbs) {
+    ctx->st_set = set;
+    ctx->st_pending = 1;
+    ctx->st_pend_g0 = g0;
+    ctx->st_pend_rows = nrows;
+  }
+  if (hi + 1 > ctx->st_next) ctx->st_next = hi + 1;
+  if (final && ctx->st_pending) {
+    CK(cudaEventSynchronize(ctx->st_ev[ctx->st_set]));
+    st_deliver(ctx, ctx->st_set, ctx->st_pend_g0, ctx->st_pend_rows);
+    ctx->st_pending = 0;
+  }
+  return DS_OK;
+}
+
 int ds_load(ds_ctx* ctx, const ds_soa* h) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
@@ -1044,7 +1234,7 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
       const uint32_t* src = h->limbs + ((int64_t)c * L + l) * h->count;
       uint32_t* dst = ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count;
       if (rs == 1) {
-        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * ctx->a_count, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * ctx->nloc * n, cudaMemcpyHostToDevice, ctx->stream));
       } else {
         CK(cudaMemcpy2DAsync(dst, sizeof(uint32_t) * n, src + r0 * n, sizeof(uint32_t) * n * rs,
                              sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
@@ -1058,17 +1248,57 @@ int ds_load(ds_ctx* ctx, const ds_soa* h) {
     CK(cudaMemcpy2DAsync(ctx->a_cls + (int64_t)c * ctx->a_count, n, sc + r0 * n, (size_t)n * rs,
                          n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
   }
-  ctx->h2d_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
-  // reset run state
-  ctx->host_have_det = 0;
-  ctx->la_step = -1;
-  ctx->det_from_cur = 0;
-  CK(cudaMemsetAsync(ctx->row_flags, 0, n, ctx->stream));
-  if (ctx->swaps) CK(cudaMemsetAsync(ctx->swaps, 0, n, ctx->stream));
-  int32_t st[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
-  CK(cudaMemcpyAsync(ctx->status, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->nloc * n;
+  return reset_run_state(ctx);
+}
+
+// ds_load without the run-state reset: the rows a step hook edited go back to
+// the device mid-run (elim.eliminate with step_hook)
+int ds_update_rows(ds_ctx* ctx, const ds_soa* h) {
+  const int have = ctx->host_have_det, dfc = ctx->det_from_cur;
+  const int nxt = ctx->st_next, pend = ctx->st_pending;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
+  int n = ctx->n, L = ctx->L;
+  int64_t r0, rs;
+  if (!host_rows(ctx, h->count, &r0, &rs)) return DS_INVALID;
+  for (int c = 0; c < ctx->ncomp; c++) {
+    for (int l = 0; l < L; l++)
+      CK(cudaMemcpy2DAsync(ctx->a_limbs + ((int64_t)c * L + l) * ctx->a_count, sizeof(uint32_t) * n,
+                           h->limbs + ((int64_t)c * L + l) * h->count + r0 * n, sizeof(uint32_t) * n * rs,
+                           sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpy2DAsync(ctx->a_exp + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, h->exp + (int64_t)c * h->count + r0 * n,
+                         sizeof(int32_t) * n * rs, sizeof(int32_t) * n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpy2DAsync(ctx->a_cls + (int64_t)c * ctx->a_count, n, h->cls + (int64_t)c * h->count + r0 * n, (size_t)n * rs,
+                         n, ctx->nloc, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  ctx->h2d_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->nloc * n;
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->host_have_det = have;
+  ctx->det_from_cur = dfc;
+  ctx->st_next = nxt;
+  ctx->st_pending = pend;
+  ctx->la_step = -1;  // multipliers computed ahead from the old rows are stale
   return DS_OK;
+}
+
+int gen_uniform_launch(cudaStream_t s, uint32_t* limbs, int32_t* ex, uint8_t* cl, int64_t count, int n, int L, int p,
+                       int rank, int world, int nloc, uint64_t seed);
+
+int ds_generate(ds_ctx* ctx, int family, uint64_t seed) {
+  if (family != DS_FAMILY_RANDOM_UNIFORM || ctx->kind != DS_KIND_REAL) {
+    ctx->err = "ds_generate: only the real random_uniform family is generated on the device";
+    return DS_INVALID;
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->side));
+  if (gen_uniform_launch(ctx->stream, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->n, ctx->L, ctx->p,
+                         ctx->rank, ctx->world, ctx->nloc, seed) != 0) {
+    ctx->err = "k_gen_uniform launch failed";
+    return DS_CUDA;
+  }
+  ctx->launches++;
+  return reset_run_state(ctx);
 }
 
 int ds_fetch(ds_ctx* ctx, ds_soa* h) {
@@ -1089,7 +1319,7 @@ int ds_fetch(ds_ctx* ctx, ds_soa* h) {
     CK(cudaMemcpy2DAsync(h->cls + (int64_t)c * h->count + r0 * n, (size_t)n * rs,
                          ctx->a_cls + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->nloc * n;
   CK(cudaStreamSynchronize(ctx->stream));
   return DS_OK;
 }
@@ -1333,15 +1563,21 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   if (collect_minors && i + 1 < n) {
     int m = i + 2;
     if ((series || m == n) && (i + 1) % ctx->world == ctx->rank) {
+      int mrc = ensure_minors(ctx);
+      if (mrc != DS_OK) return mrc;
+      k = kargs(ctx);  // minors pointers
+      ks = k;
+      ks.scratch = ctx->scratch_side;
       int64_t jl = (i + 1) / ctx->world;
       if (fast) {
         // outputs only: run on the side stream after this step's update
         cudaStream_t ss = ctx->side;
         CK(cudaEventRecord(ctx->ev_upd, s));
         CK(cudaStreamWaitEvent(ss, ctx->ev_upd, 0));
+        const int64_t mo = (jl % ctx->m_rows) * n;
         int rc = mul_row_launch(&ctx->plan, ss, ctx->det_limbs + i, n, ctx->det_exp + i, ctx->det_cls + i,
                                 ctx->a_limbs + jl * n, ctx->a_count, ctx->a_exp + jl * n, ctx->a_cls + jl * n, i + 1,
-                                ctx->sig_limbs + jl * n, ctx->a_count, ctx->sig_exp + jl * n, ctx->sig_cls + jl * n,
+                                ctx->sig_limbs + mo, ctx->m_count, ctx->sig_exp + mo, ctx->sig_cls + mo,
                                 ctx->status, &ctx->launches, i, ctx->ws_ex, ctx->ws_ey);
         if (rc != DS_OK) { ctx->err = "minor product launch failed"; return rc; }
         k_emit_last<<<1, 128, 0, ss>>>(k, i);
@@ -1400,6 +1636,8 @@ int ds_snapshot(ds_ctx* ctx, int save) {
   if (ctx->swaps) CK(cudaMemsetAsync(ctx->swaps, 0, ctx->n, ctx->stream));
   CK(cudaMemsetAsync(ctx->status + 1, 0, 7 * sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->status, 0xff, sizeof(int32_t), ctx->stream));  // -1
+  ctx->st_next = 1;
+  ctx->st_pending = 0;
   return DS_OK;
 }
 
@@ -1545,24 +1783,38 @@ static int copy_vec(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32
 
 // minors rows [r0, r1) of a world-1 context, the first `width` entries of each
 // (row m-1 holds m entries), on stream s: one 2D copy per limb plane
-static int copy_row_range(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
-                          int r0, int r1, int width, cudaStream_t s) {
+// local minors rows [r0, r1) (ring slots r % m_rows; split where the ring wraps)
+// into host rows starting at hrow0 (row pitch n) of dst
+static int copy_row_range_to(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
+                             int r0, int r1, int width, cudaStream_t s, int hrow0) {
   if (!dst || !dst->limbs || r1 <= r0 || width <= 0) return DS_OK;
+  if (!limbs) return DS_OK;  // nothing emitted yet
   const int n = ctx->n, L = ctx->L;
-  const size_t rows = (size_t)(r1 - r0);
-  const int64_t o = (int64_t)r0 * n;
-  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * (int64_t)rows * width;
-  for (int c = 0; c < ctx->ncomp; c++) {
-    for (int l = 0; l < L; l++)
-      CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + o, sizeof(uint32_t) * n,
-                           limbs + ((int64_t)c * L + l) * ctx->a_count + o, sizeof(uint32_t) * n,
-                           sizeof(uint32_t) * width, rows, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + o, sizeof(int32_t) * n, ex + (int64_t)c * ctx->a_count + o,
-                         sizeof(int32_t) * n, sizeof(int32_t) * width, rows, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + o, n, cl + (int64_t)c * ctx->a_count + o, n, width, rows,
-                         cudaMemcpyDeviceToHost, s));
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * (int64_t)(r1 - r0) * width;
+  for (int a = r0; a < r1;) {
+    const int slot = a % ctx->m_rows;
+    const int b = std::min(r1, a + (ctx->m_rows - slot));
+    const size_t rows = (size_t)(b - a);
+    const int64_t o = (int64_t)slot * n, ho = (int64_t)(hrow0 + (a - r0)) * n;
+    for (int c = 0; c < ctx->ncomp; c++) {
+      for (int l = 0; l < L; l++)
+        CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + ho, sizeof(uint32_t) * n,
+                             limbs + ((int64_t)c * L + l) * ctx->m_count + o, sizeof(uint32_t) * n,
+                             sizeof(uint32_t) * width, rows, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + ho, sizeof(int32_t) * n,
+                           ex + (int64_t)c * ctx->m_count + o, sizeof(int32_t) * n, sizeof(int32_t) * width, rows,
+                           cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + ho, n, cl + (int64_t)c * ctx->m_count + o, n, width,
+                           rows, cudaMemcpyDeviceToHost, s));
+    }
+    a = b;
   }
   return DS_OK;
+}
+
+static int copy_row_range(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl,
+                          int r0, int r1, int width, cudaStream_t s) {
+  return copy_row_range_to(ctx, dst, limbs, ex, cl, r0, r1, width, s, r0);
 }
 
 static bool host_pinned(const void* p) {
@@ -1577,22 +1829,26 @@ static bool host_pinned(const void* p) {
 static int copy_rows(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, const int32_t* ex, const uint8_t* cl) {
   // owned minors rows (local index jl <-> global row rank + jl*world) into a
   // full n*n host matrix
-  if (!dst || !dst->limbs) return DS_OK;
+  if (!dst || !dst->limbs || !limbs) return DS_OK;
+  if (ctx->m_rows < ctx->nloc) {
+    ctx->err = "minors are streamed (ds_stream_minors): they are not resident for a full fetch";
+    return DS_INVALID;
+  }
   int n = ctx->n, L = ctx->L;
   int64_t r0, rs;
   if (!host_rows(ctx, dst->count, &r0, &rs)) return DS_INVALID;
   for (int c = 0; c < ctx->ncomp; c++) {
     for (int l = 0; l < L; l++)
       CK(cudaMemcpy2DAsync(dst->limbs + ((int64_t)c * L + l) * dst->count + r0 * n,
-                           sizeof(uint32_t) * n * rs, limbs + ((int64_t)c * L + l) * ctx->a_count,
+                           sizeof(uint32_t) * n * rs, limbs + ((int64_t)c * L + l) * ctx->m_count,
                            sizeof(uint32_t) * n, sizeof(uint32_t) * n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpy2DAsync(dst->exp + (int64_t)c * dst->count + r0 * n, sizeof(int32_t) * n * rs,
-                         ex + (int64_t)c * ctx->a_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
+                         ex + (int64_t)c * ctx->m_count, sizeof(int32_t) * n, sizeof(int32_t) * n, ctx->nloc,
                          cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpy2DAsync(dst->cls + (int64_t)c * dst->count + r0 * n, (size_t)n * rs,
-                         cl + (int64_t)c * ctx->a_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
+                         cl + (int64_t)c * ctx->m_count, n, n, ctx->nloc, cudaMemcpyDeviceToHost, ctx->stream));
   }
-  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->a_count;
+  ctx->d2h_bytes += (int64_t)ctx->ncomp * (4 * L + 5) * ctx->nloc * n;
   return DS_OK;
 }
 
@@ -1720,7 +1976,9 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
   // progressive D2H of the minors (pinned host buffers): rows finalised by
   // the emission are copied in batches on the side stream while the
   // elimination runs -- row m-1 holds m entries (triangle)
-  const bool prog = res && collect_minors && series && res->signed_minors.limbs && res->normalized.limbs &&
+  const bool streaming = ctx->st_batch > 0 && collect_minors;
+  if (streaming && start_step + 1 > ctx->st_next) ctx->st_next = start_step + 1;
+  const bool prog = !streaming && res && collect_minors && series && res->signed_minors.limbs && res->normalized.limbs &&
                     host_pinned(res->signed_minors.limbs) && host_pinned(res->normalized.limbs) &&
                     host_pinned(res->signed_minors.exp) && host_pinned(res->signed_minors.cls) &&
                     host_pinned(res->normalized.exp) && host_pinned(res->normalized.cls) &&
@@ -1741,6 +1999,11 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
     }
     if ((rc = ds_pivot_stage(ctx, i)) != DS_OK) { ctx->la_limit = -1; return rc; }
     if ((rc = ds_step(ctx, i, collect_minors, series)) != DS_OK) { ctx->la_limit = -1; return rc; }
+    if (streaming && (i + 1 - start_step) % ctx->st_batch == 0 &&
+        (rc = ds_stream_flush(ctx, i + 1, 0)) != DS_OK) {
+      ctx->la_limit = -1;
+      return rc;
+    }
     if (prog && (i + 1 - start_step) % BATCH == 0) {
       const int r1 = i + 2 < ctx->n ? i + 2 : ctx->n;  // rows 0 .. i+1 are final after step i
       if ((rc = copy_row_range(ctx, &res->signed_minors, ctx->sig_limbs, ctx->sig_exp, ctx->sig_cls, copied, r1, r1,
@@ -1761,8 +2024,12 @@ int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop
   rc = ds_status(ctx, &failed);
   int upto = failed >= 0 ? failed : stop_step;
   *steps_done = upto;
+  if (streaming) {
+    int rc2 = ds_stream_flush(ctx, upto, 1);
+    if (rc2 != DS_OK) return rc2;
+  }
   if (res) {
-    int rc2 = results_fetch_from(ctx, upto, res, prog ? copied : 0);
+    int rc2 = results_fetch_from(ctx, upto, res, streaming ? ctx->n : (prog ? copied : 0));
     if (rc2 != DS_OK) return rc2;
   }
   if (rc != DS_OK) return rc;

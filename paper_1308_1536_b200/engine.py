@@ -104,6 +104,17 @@ class DeviceElimination:
         s = matrix.c()
         _check(self.lib.ds_fetch(self.ctx, ctypes.byref(s)), self.ctx, "ds_fetch", self.rank)
 
+    def generate(self, seed: int, family: str = "random_uniform"):
+        """Fill this rank's rows on the device (ds_generate): the counter-based twin of
+        genmat.synth_matrix(family, n, seed) -- see synth.counter_uniform_soa."""
+        code = {"random_uniform": 0}[family]
+        _check(self.lib.ds_generate(self.ctx, code, int(seed) & (2 ** 64 - 1)), self.ctx, "ds_generate", self.rank)
+
+    def update_rows(self, matrix: SoA):
+        """Rows back into HBM without resetting the run (ds_update_rows)."""
+        s = matrix.c()
+        _check(self.lib.ds_update_rows(self.ctx, ctypes.byref(s)), self.ctx, "ds_update_rows", self.rank)
+
     def set_det(self, det: SoA):
         s = det.c()
         _check(self.lib.ds_set_det(self.ctx, ctypes.byref(s)), self.ctx, "ds_set_det", self.rank)
@@ -116,6 +127,7 @@ class DeviceElimination:
         rp = ctypes.byref(res.c()) if res is not None else None
         rc = self.lib.ds_run(self.ctx, int(collect_minors), int(series), start, stop, rp, ctypes.byref(done))
         _check(rc, self.ctx, "ds_run", self.rank)
+        self.raise_stream_error()
         return rc, done.value
 
     def set_pivot_mode(self, mode: str):
@@ -158,6 +170,53 @@ class DeviceElimination:
         r = res.c()
         _check(self.lib.ds_results_fetch_range(self.ctx, int(t0), int(t1), int(m0), int(m1), ctypes.byref(r)),
                self.ctx, "ds_results_fetch_range", self.rank)
+
+    # -- streaming of minors rows (ds_stream_minors / ds_stream_flush) ------------
+    _ROWS_CB = ctypes.CFUNCTYPE(None, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_native.ds_soa),
+                                ctypes.POINTER(_native.ds_soa), ctypes.POINTER(ctypes.c_uint8), ctypes.c_void_p)
+
+    def stream_minors(self, batch_steps: int, callback):
+        """Stream the minors rows off the device as they finalise (only a ring of rows
+        stays in HBM).  callback(g0, stride, nrows, signed, normalized, flags) gets SoA
+        VIEWS of pinned staging memory (valid during the call only): row r, leading size
+        m = g0 + r*stride + 1, holds its m entries at [r*n, r*n + m).  batch_steps <= 0 or
+        callback None turns streaming off."""
+        if batch_steps <= 0 or callback is None:
+            _check(self.lib.ds_stream_minors(self.ctx, 0, None, None), self.ctx, "ds_stream_minors", self.rank)
+            self._stream_cb = None
+            return
+        nc, L = self.ncomp, self.L
+
+        def view(sp):
+            s = sp.contents
+            cnt = int(s.count)
+            limbs = np.ctypeslib.as_array(ctypes.cast(s.limbs, ctypes.POINTER(ctypes.c_uint32)), (nc, L, cnt))
+            ex = np.ctypeslib.as_array(ctypes.cast(s.exp, ctypes.POINTER(ctypes.c_int32)), (nc, cnt))
+            cl = np.ctypeslib.as_array(ctypes.cast(s.cls, ctypes.POINTER(ctypes.c_uint8)), (nc, cnt))
+            return SoA(nc, L, cnt, limbs, ex, cl)
+
+        def trampoline(g0, stride, nrows, sp, np_, fp, user):
+            flags = np.ctypeslib.as_array(fp, (nrows,)) if nrows else np.zeros(0, np.uint8)
+            try:
+                callback(g0, stride, nrows, view(sp), view(np_), flags)
+            except BaseException as exc:  # cannot propagate through C: keep it for the caller
+                self._stream_exc = exc
+
+        self._stream_exc = None
+        self._stream_cb = self._ROWS_CB(trampoline)
+        _check(self.lib.ds_stream_minors(self.ctx, int(batch_steps), self._stream_cb, None), self.ctx,
+               "ds_stream_minors", self.rank)
+
+    def stream_flush(self, upto_step: int, final: bool = False):
+        _check(self.lib.ds_stream_flush(self.ctx, int(upto_step), int(final)), self.ctx, "ds_stream_flush",
+               self.rank)
+        self.raise_stream_error()
+
+    def raise_stream_error(self):
+        exc = getattr(self, "_stream_exc", None)
+        if exc is not None:
+            self._stream_exc = None
+            raise exc
 
     def snapshot(self, save: bool):
         """save=True: keep a device copy of this rank's rows; save=False:

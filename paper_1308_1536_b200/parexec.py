@@ -239,13 +239,15 @@ def _local_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool
 
 
 def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcast, stats: CommStats | None = None,
-             lookahead: bool = True):
+             lookahead: bool = True, stream_every: int = 0):
     """Generic per-rank step loop of the message-passing executor.
 
     engine    -- this rank's context (stage/step/status), a DeviceElimination
                  on a GPU; the CPU tests pass the C oracle's context instead.
     pivot     -- the tensor holding the pivot buffer bytes (device or host).
     broadcast -- callable(tensor, src_rank) (torch.distributed.broadcast).
+    stream_every -- > 0 when the engine streams its minors rows (ds_stream_minors):
+                 flush every that many steps and at the end.
     Returns the failed step (-1 if none).
     """
     world, rank = engine.world, engine.rank
@@ -273,9 +275,14 @@ def dist_run(engine, n: int, collect_minors: bool, series: bool, pivot, broadcas
                     engine.lookahead_pivot(i + 1, scal.data_ptr())
                 broadcast(scal, o1)
             engine.lookahead_mult(i + 1, scal.data_ptr())
+        if stream_every and (i + 1) % stream_every == 0:
+            engine.stream_flush(i + 1)
     if la is not None:
         engine.lookahead_enable(0)
-    return engine.status()
+    failed = engine.status()
+    if stream_every:
+        engine.stream_flush(failed if failed >= 0 else n, final=True)
+    return failed
 
 
 def _lookahead_setup(engine, n: int, pivot):
@@ -347,7 +354,13 @@ def _rank_setup(eng, backend: str, rank: int):
     _, pbytes = eng.pivot_buffer()
     pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{dev}")
     _native_check(eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes), "ds_use_pivot_buffer")
-    _native_check(eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream), "ds_set_stream")
+    cur = torch.cuda.current_stream()
+    if cur.cuda_stream == 0:
+        # the legacy default stream has handle 0, which ds_set_stream reads as "own stream":
+        # run on a dedicated torch stream so collectives and kernels share one stream order
+        cur = torch.cuda.Stream()
+        torch.cuda.set_stream(cur)
+    _native_check(eng.lib.ds_set_stream(eng.ctx, cur.cuda_stream), "ds_set_stream")
     if backend == "nccl":
         return pivot, (lambda t, src: dist.broadcast(t, src=src)), True
     staging = {}
@@ -381,6 +394,7 @@ def _group_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool
     dev = torch.cuda.current_device()
     backend = dist.get_backend()
     eng = DeviceElimination(n, p, A.kind, dev, rank, world)
+    caller_stream = torch.cuda.current_stream()
     try:
         soa = A.to_soa()
         eng.load(soa)
@@ -398,6 +412,7 @@ def _group_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool
         eng.lib.ds_use_pivot_buffer(eng.ctx, None, 0)
     finally:
         eng.close()
+        torch.cuda.set_stream(caller_stream)
 
     def allreduce(arr):
         t = torch.from_numpy(np.ascontiguousarray(arr))

@@ -93,7 +93,9 @@ eng.load(A)
 _, pbytes = eng.pivot_buffer()
 pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{{local}}")
 eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
-eng.lib.ds_set_stream(eng.ctx, torch.cuda.current_stream().cuda_stream)
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+eng.lib.ds_set_stream(eng.ctx, stream.cuda_stream)
 failed = dist_run(eng, n, True, True, pivot, lambda t, src: dist.broadcast(t, src=src))
 res = HostResults.alloc(n, 1, eng.L, True)
 eng.results(n, res)

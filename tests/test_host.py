@@ -132,3 +132,34 @@ def test_topology_and_plan():
     assert [last - first + 1 for _, first, last in block_reassign_plan(0, 10, 3)] == [4, 3, 3]
     with pytest.raises(ValueError):
         WorkerTopology(0, 5)
+
+
+@pytest.mark.parametrize("p", [64, 65, 100, 1024, 1055])
+def test_counter_uniform_is_exactly_2u_minus_1(p):
+    """synth.counter_uniform_soa (host twin of the device builder): every element equals
+    (k - 2^(p-1)) 2^(1-p) for the generator's p-bit integer k (genmat.py:242-246: 2U - 1 at p
+    bits is exact), recomputed here with Python integers."""
+    from fractions import Fraction
+    import numpy as np
+    from paper_1308_1536_b200.synth import counter_uniform_soa
+    n, seed = 5, 11 + p
+    L = (p + 31) // 32
+    s = counter_uniform_soa(n, p, seed)
+    M64 = 2 ** 64 - 1
+
+    def mix(x):
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+        return x ^ (x >> 31)
+
+    key = mix(seed ^ 0x243F6A8885A308D3)
+    npairs = (L + 1) // 2
+    for idx in range(n * n):
+        K = 0
+        for q in range(npairs):
+            K |= mix((key + (idx * npairs + q + 1) * 0x9E3779B97F4A7C15) & M64) << (64 * q)
+        K &= (1 << (32 * L)) - 1
+        K &= ~((1 << (32 * L - p)) - 1)
+        want = Fraction(K - 2 ** (32 * L - 1), 2 ** (32 * L - 1))
+        got = s.get(idx, p)
+        assert got._fraction() == want, idx

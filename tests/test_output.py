@@ -159,3 +159,28 @@ def test_mpmat_roundtrip_random(tmp_path):
         T, n2, p2, kind = load_mpmat(path)
         assert (n2, p2, kind) == (n, p, "real")
         assert [T.canonical(i, p) for i in range(n * n)] == [S.canonical(i, p) for i in range(n * n)]
+
+
+def test_minors_stream_binary_round_trip(tmp_path):
+    """DSMR v1 records written by output.MinorsStream (the consumer of the device's minors
+    stream) read back bit for bit; rows without the emitted flag are skipped."""
+    import numpy as np
+    from paper_1308_1536_b200.output import MinorsStream, read_minors_binary
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    n, p = 6, 100
+    s, t = random_uniform_soa(n, p, 3), random_uniform_soa(n, p, 4)
+    path = tmp_path / "x.dsmr"
+    st = MinorsStream(n, p, path=str(path), keep_upto=n)
+    st(1, 1, 3, s, t, np.array([3, 1, 3], dtype=np.uint8))
+    st(4, 1, 2, s, t, np.array([0, 3], dtype=np.uint8))
+    st.close()
+    rows = list(read_minors_binary(str(path)))
+    assert [(m, fl) for m, fl, _, _ in rows] == [(2, 3), (3, 1), (4, 3), (6, 3)]
+    for m, fl, sg, nm in rows:
+        r = m - 2 if m <= 4 else m - 5
+        sl = slice(r * n, r * n + m)
+        assert np.array_equal(sg.limbs, s.limbs[:, :, sl]) and np.array_equal(sg.exp, s.exp[:, sl])
+        assert (nm is None) == (not fl & 2)
+        if nm is not None:
+            assert np.array_equal(nm.limbs, t.limbs[:, :, sl])
+    assert st.sizes == [2, 3, 4, 6] and len(st.digest) == 64
