@@ -1348,6 +1348,16 @@ static EncodeTiledFn encode_tiled();
 
 // wide-precision plan: product kernel tiles, stages and the row chunk bounded by
 // the product-limb buffer
+// fallback-list entries per launch: every element one update launch can touch
+// (nrows x ncols <= nloc x n), so inputs with many undecidable short products
+// degrade to the exact path instead of overflowing; capped at 2^25 entries
+// (256 MB per list) -- beyond it the overflow is counted in status[5] and
+// reported as an error
+static int fb_capacity(int nloc, int n) {
+  const int64_t want = (int64_t)(nloc > 0 ? nloc : 1) * n;
+  return (int)(want < (1 << 16) ? (1 << 16) : (want > (1 << 25) ? (1 << 25) : want));
+}
+
 static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int maxsm) {
   (void)device;
   const int L = plan->L, D8p = plan->D8p, zb = 32 * L - p;
@@ -1397,7 +1407,7 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   TcWork* w = new TcWork();
   memset(w, 0, sizeof(*w));
   plan->work = w;
-  w->fb_cap = 1 << 16;
+  w->fb_cap = fb_capacity(nloc, n);
   w->sthreads = 64 * 128;
   w->tthreads = 148 * 3 * 256;
   bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1) * nc) == cudaSuccess &&
@@ -1472,7 +1482,7 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   plan->smem = smem;
   TcWork* w = new TcWork();
   memset(w, 0, sizeof(*w));
-  w->fb_cap = 1 << 16;
+  w->fb_cap = fb_capacity(nloc, n);
   w->sthreads = 64 * 128;
   bool ok = cudaMalloc(&w->zbytes, (size_t)plan->D8p * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
             cudaMalloc(&w->bbytes, (size_t)plan->D8p * n) == cudaSuccess &&

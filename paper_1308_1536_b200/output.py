@@ -153,11 +153,11 @@ class MinorsStream:
             if not fl & 1:
                 continue
             sl = slice(r * n, r * n + m)
-            parts = [np.ascontiguousarray(signed.limbs[:, :, sl]), np.ascontiguousarray(signed.exp[:, sl]),
-                     np.ascontiguousarray(signed.cls[:, sl])]
+            # copies: the arguments are views of staging memory the engine reuses after this call
+            parts = [np.array(signed.limbs[:, :, sl]), np.array(signed.exp[:, sl]), np.array(signed.cls[:, sl])]
             if fl & 2:
-                parts += [np.ascontiguousarray(normalized.limbs[:, :, sl]), np.ascontiguousarray(normalized.exp[:, sl]),
-                          np.ascontiguousarray(normalized.cls[:, sl])]
+                parts += [np.array(normalized.limbs[:, :, sl]), np.array(normalized.exp[:, sl]),
+                          np.array(normalized.cls[:, sl])]
             head = struct.pack("<IB", m, fl)
             self._h.update(head)
             for a in parts:
