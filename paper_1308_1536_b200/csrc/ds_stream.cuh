@@ -178,8 +178,12 @@ struct SWin {
       Z[0] = tcarry << fz;
       tc = 0u;
     }
-    addc_n<NL>(T, T, Z, tc);
-    tcarry = tc;
+    // the round increment propagates through t's limbs only while they are all ones:
+    // past the first block this chain is idle for (almost) every lane
+    if (fz >= 0 || tc) {
+      addc_n<NL>(T, T, Z, tc);
+      tcarry = tc;
+    }
     // X = a (slot w+k) or T;  Y stream = T (xa) or a limbs (slot w+k+dq+1)
     const uint32_t ad0 = at(w + (xa ? 0 : dq + 1));
     uint32_t Ld[NL];

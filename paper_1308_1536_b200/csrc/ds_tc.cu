@@ -257,7 +257,6 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
     uint8_t* bank = bank0 + pp * BR * KS;
     uint8_t* zw = zw0 + pp * ZWL;
     const uint32_t bank_sa = smem_u32(bank);
-    const bool issuer = ptid == 0;
     int q = 0;  // row counter of this pipeline
     for (int ri = pp; ri < nrow_cta; ri += NG, q++) {
       if (q >= 1) mbar_wait(&bar_bank_empty[pp], (q - 1) & 1);  // MMAs of row ri-2 completed
@@ -283,7 +282,11 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       }
       asm volatile("fence.proxy.async.shared::cta;");
       bar_pipe(1 + pp, NPIPE);
-      if (issuer) {
+      if (ptid < 32) {
+        // the whole issuer warp runs the loop (warp-uniform descriptors live in
+        // uniform registers, no per-MMA register->uniform moves); lane 0 issues
+        const uint64_t bd_hi = umma_desc(0u, (uint32_t)BR * 16u, 128);  // LBO / SBO / version fields
+        const uint32_t idesc = idesc_i8(TM, TN);
         for (int t = 0; t < ntiles; t++) {
           const int gt = q * ntiles + t;  // tile counter of this group
           const int buf = gt & 1;
@@ -296,18 +299,23 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
           if (s_hi > a.D8p - 1) s_hi = a.D8p - 1;
           const int ks0 = s_lo / KS, ks1 = s_hi / KS;
           const uint32_t dcol = tmem + (uint32_t)((2 * pp + buf) * TN);
+          // B tile of K step ks: bank rows from t*TN + 32 (nks - 1 - ks) (a multiple of 8):
+          // the descriptor's 16-byte address field steps down by 32 per K step
+          uint64_t bd = bd_hi | (uint64_t)(((bank_sa + (uint32_t)((t * TN + KS * (nks - 1 - ks0)) >> 3) * 128u) >> 4) &
+                                           0x3FFFu);
+          uint32_t acol = tmem + ACOL + 8 * ks0;
           for (int ks = ks0; ks <= ks1; ks++) {
-            const int r0 = t * TN + KS * (nks - 1 - ks);  // multiple of 8
-            uint64_t bd = umma_desc(bank_sa + (uint32_t)(r0 >> 3) * 128u, (uint32_t)BR * 16u, 128);
-            uint32_t acc = ks > ks0 ? 1u : 0u;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dcol),
-                "r"(tmem + ACOL + 8 * ks), "l"(bd), "r"(idesc_i8(TM, TN)), "r"(acc));
+            if (lane == 0)
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dcol),
+                  "r"(acol), "l"(bd), "r"(idesc), "r"((uint32_t)(ks - ks0)));
+            bd -= 32;
+            acol += 8;
           }
-          umma_commit(&bar_tfull[pp][buf]);
+          if (lane == 0) umma_commit(&bar_tfull[pp][buf]);
         }
-        umma_commit(&bar_bank_empty[pp]);
+        if (lane == 0) umma_commit(&bar_bank_empty[pp]);
       }
       __syncwarp();
     }
@@ -432,8 +440,11 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       }
       bool ok = true;
       uint32_t carry = 0;
-      const int nsh = norm ? 0 : 1;
-      uint32_t praw = 0u;  // previous unshifted P limb
+      // non-normalised products are doubled (P' = P 2^nsh) inside the column
+      // combination: the digit weights 2^(8j) become 2^(8j + nsh), so P' limbs come
+      // straight out of the carry chain (no funnel shift per limb)
+      const uint32_t nsh = norm ? 0u : 1u;
+      const uint32_t m0 = 1u << nsh, m1 = 256u << nsh, m2 = 65536u << nsh, m3 = 16777216u << nsh;
       for (int t = 0; t < ntiles; t++) {
         const int gt = q * ntiles + t;
         const int buf = gt & 1;
@@ -461,10 +472,10 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
             uint32_t lo[8], hi[8], P[8];
 #pragma unroll
             for (int g = 0; g < 8; g++) {
-              uint64_t w = (uint64_t)v[4 * g + 3] * 16777216u;  // IMAD.WIDE chain, no zero-extension moves
-              w += (uint64_t)v[4 * g + 2] * 65536u;
-              w += (uint64_t)v[4 * g + 1] * 256u;
-              w += (uint64_t)v[4 * g] * 1u;
+              uint64_t w = (uint64_t)v[4 * g + 3] * m3;  // IMAD.WIDE chain, no zero-extension moves
+              w += (uint64_t)v[4 * g + 2] * m2;
+              w += (uint64_t)v[4 * g + 1] * m1;
+              w += (uint64_t)v[4 * g] * m0;  // < 2^51
               lo[g] = (uint32_t)w;
               hi[g] = (uint32_t)(w >> 32);
             }
@@ -479,12 +490,7 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
               "addc.u32 %8, %24, 0;"
                 : "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]), "+r"(carry)
                 : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
-#pragma unroll
-            for (int g = 0; g < 8; g++) {
-              const uint32_t raw = P[g];
-              P[g] = __funnelshift_l(praw, raw, nsh);
-              praw = raw;
-            }
+
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
             ok = em.block<8, true>(g0, P);  // r' - zb = 32 L: aligned limbs
           }
@@ -494,7 +500,7 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
         if (lane == 0) mbar_arrive(&bar_tempty[grp][buf]);
       }
       if (process && ok) {
-        em.finish((carry || (nsh && (praw >> 31))) ? 1.0 : 0.0);  // the bit shifted out of the top limb
+        em.finish(carry ? 1.0 : 0.0);  // anything above the top limb of P
         if (em.excess) ok = false;
       }
       if (process && !ok) fallback = true;
