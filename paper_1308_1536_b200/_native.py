@@ -15,7 +15,7 @@ from .errors import DeviceUnavailable
 from .soa import ds_soa
 
 LIB_NAME = "libdetseries_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("DS_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DS_OK, DS_ZERO_PIVOT, DS_PRECISION_MISMATCH, DS_INVALID = 0, 1, 2, 3
 DS_CUDA, DS_NCCL, DS_OOM, DS_OVERFLOW = 4, 5, 6, 7

@@ -3,6 +3,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef DS_VAR_ADDC8
+#define DS_VAR_ADDC8 1
+#endif
+
 namespace dss {
 
 // s = x + y + cy over N limbs (low -> high) with the PTX carry chain;
@@ -57,8 +61,10 @@ __device__ __forceinline__ void addc8(uint32_t* s, const uint32_t* x, const uint
 template <int N>
 __device__ __forceinline__ void addc_n(uint32_t (&s)[N], const uint32_t (&x)[N], const uint32_t (&y)[N], uint32_t& cy) {
   int k0 = 0;
+#if DS_VAR_ADDC8
 #pragma unroll
   for (; k0 + 8 <= N; k0 += 8) addc8(s + k0, x + k0, y + k0, cy);
+#endif
 #pragma unroll
   for (int k = k0; k + 4 <= N; k += 4) addc4(s + k, x + k, y + k, cy);
   if (N & 2) addc2(s + (N & ~3), x + (N & ~3), y + (N & ~3), cy);

@@ -8,6 +8,10 @@
 #include "../../include/detseries_b200.h"
 #include "ds_carry.cuh"
 
+#ifndef DS_VAR_TSKIP
+#define DS_VAR_TSKIP 1
+#endif
+
 namespace dss {
 
 // ------------------------------------------------------------ S window
@@ -180,10 +184,15 @@ struct SWin {
     }
     // the round increment propagates through t's limbs only while they are all ones:
     // past the first block this chain is idle for (almost) every lane
+#if DS_VAR_TSKIP
     if (fz >= 0 || tc) {
       addc_n<NL>(T, T, Z, tc);
       tcarry = tc;
     }
+#else
+    addc_n<NL>(T, T, Z, tc);
+    tcarry = tc;
+#endif
     // X = a (slot w+k) or T;  Y stream = T (xa) or a limbs (slot w+k+dq+1)
     const uint32_t ad0 = at(w + (xa ? 0 : dq + 1));
     uint32_t Ld[NL];

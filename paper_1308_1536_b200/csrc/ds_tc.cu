@@ -30,6 +30,14 @@
 #include "ds_stream.cuh"
 #include "ds_tc.cuh"
 
+// implementation variants (A/B measured on the B200)
+#ifndef DS_VAR_MMAWARP
+#define DS_VAR_MMAWARP 1
+#endif
+#ifndef DS_VAR_MULSHIFT
+#define DS_VAR_MULSHIFT 0
+#endif
+
 namespace {
 
 using namespace dss;
@@ -282,6 +290,7 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       }
       asm volatile("fence.proxy.async.shared::cta;");
       bar_pipe(1 + pp, NPIPE);
+#if DS_VAR_MMAWARP
       if (ptid < 32) {
         // the whole issuer warp runs the loop (warp-uniform descriptors live in
         // uniform registers, no per-MMA register->uniform moves); lane 0 issues
@@ -317,6 +326,35 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
         }
         if (lane == 0) umma_commit(&bar_bank_empty[pp]);
       }
+#else
+      const bool issuer = ptid == 0;
+      if (issuer) {
+        for (int t = 0; t < ntiles; t++) {
+          const int gt = q * ntiles + t;  // tile counter of this group
+          const int buf = gt & 1;
+          if (gt >= 2) mbar_wait(&bar_tempty[pp][buf], ((gt >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const int c0 = a.c_lo + t * TN;
+          int s_lo = c0 - (a.D8p - 1);
+          if (s_lo < 0) s_lo = 0;
+          int s_hi = c0 + TN - 1;
+          if (s_hi > a.D8p - 1) s_hi = a.D8p - 1;
+          const int ks0 = s_lo / KS, ks1 = s_hi / KS;
+          const uint32_t dcol = tmem + (uint32_t)((2 * pp + buf) * TN);
+          for (int ks = ks0; ks <= ks1; ks++) {
+            const int r0 = t * TN + KS * (nks - 1 - ks);  // multiple of 8
+            uint64_t bd = umma_desc(bank_sa + (uint32_t)(r0 >> 3) * 128u, (uint32_t)BR * 16u, 128);
+            uint32_t acc = ks > ks0 ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dcol),
+                "r"(tmem + ACOL + 8 * ks), "l"(bd), "r"(idesc_i8(TM, TN)), "r"(acc));
+          }
+          umma_commit(&bar_tfull[pp][buf]);
+        }
+        umma_commit(&bar_bank_empty[pp]);
+      }
+#endif
       __syncwarp();
     }
   } else {
@@ -330,12 +368,42 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
     // full 128-column tiles move a's limbs with one TMA load / store per row
     // (box = 128 columns x L planes into slots 1..L); edge tiles per thread
     const bool tile_io = a.tma_ok && kbase + TM <= a.n && (a.n & 3) == 0;  // box start 16-byte aligned
+    // per-column pivot-row scalars are loop invariant; the per-row scalars (a's class
+    // and exponent, z's class, exponent and fp64 top) are loaded one row ahead so
+    // their HBM latency overlaps the previous row's epilogue
+    const uint8_t cb = col_ok ? a.bcls[k] : (uint8_t)DS_CLS_PZERO;
+    const double bfk = col_ok ? a.bf[k] : 0.0;
+    const int32_t bexk = col_ok ? a.bexp[k] : 0;
+    uint8_t nx_ca = 0, nx_cz = 0;
+    int32_t nx_ea = 0, nx_zexp = 0;
+    double nx_zf = 0.0;
+    if (col_ok && grp < nrow_cta) {
+      const int zr = row0 + grp;
+      const int64_t idx = (int64_t)(a.jl0 + zr) * a.n + k;
+      nx_ca = a.a_cls[idx];
+      nx_ea = a.a_exp[idx];
+      nx_cz = a.zcls[zr];
+      nx_zf = a.zf[zr];
+      nx_zexp = a.zexp[zr];
+    }
     int q = 0;
     for (int ri = grp; ri < nrow_cta; ri += NG, q++) {
       const int zr = row0 + ri;  // row index relative to jl0
       const int jl = a.jl0 + zr;
       const int64_t idx = (int64_t)jl * a.n + k;
       const int tx = (int)((int64_t)jl * a.n + kbase);
+      const uint8_t cur_ca = nx_ca, cur_cz = nx_cz;
+      const int32_t cur_ea = nx_ea, cur_zexp = nx_zexp;
+      const double cur_zf = nx_zf;
+      if (col_ok && ri + NG < nrow_cta) {
+        const int zn = zr + NG;
+        const int64_t idn = idx + (int64_t)NG * a.n;
+        nx_ca = a.a_cls[idn];
+        nx_ea = a.a_exp[idn];
+        nx_cz = a.zcls[zn];
+        nx_zf = a.zf[zn];
+        nx_zexp = a.zexp[zn];
+      }
       if (tile_io) {
         if (r == 0) {
           bulk_wait_read0();  // this group's previous tile store has read the window
@@ -351,17 +419,17 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       int64_t E = 0, d = 0;
       bool xa = false, sub = false, za = false;
       if (col_ok) {
-        uint8_t cz = a.zcls[zr], cb = a.bcls[k], ca = a.a_cls[idx];
+        const uint8_t cz = cur_cz, ca = cur_ca;
         za = ca >= DS_CLS_PZERO;
         int sa = ca & 1, st = (cz & 1) ^ (cb & 1);
         if (cz >= DS_CLS_PZERO || cb >= DS_CLS_PZERO) {
           if (za) a.a_cls[idx] = (sa && !st) ? DS_CLS_NZERO : DS_CLS_PZERO;
         } else {
-          int32_t ea = za ? 0 : a.a_exp[idx];
-          double pr = a.zf[zr] * a.bf[k];
+          int32_t ea = za ? 0 : cur_ea;
+          double pr = cur_zf * bfk;
           norm = pr >= 2.0 ? 1 : 0;
           bool confident = fabs(pr - 2.0) > 0x1p-42;
-          int64_t ebase = (int64_t)a.zexp[zr] + a.bexp[k];
+          int64_t ebase = (int64_t)cur_zexp + bexk;
           if (!za && (int64_t)ea - (ebase - 1) >= (int64_t)a.p + 3) {
             // a dominates whatever the normalisation: unchanged
           } else if (!confident) {
@@ -402,7 +470,7 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       if (process && !za && tile_io && !a.no_direct) {
         const uint64_t atop = ((uint64_t)Sw[L * TM] << 32) | Sw[(L - 1) * TM];
         const double am = (double)atop * 0x1p-63;  // [1, 2)
-        const double prv = a.zf[zr] * a.bf[k];
+        const double prv = cur_zf * bfk;
         const double tm = norm ? prv * 0.5 : prv;  // [1, 2)
         const int64_t sh = xa ? d : -d;
         const double yv = sh < 200 ? ldexp(xa ? tm : am, -(int)sh) : 0.0;
@@ -410,8 +478,8 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
         if (sd < 0.0) {  // only xa, d == 0, sub: t - a with the roles swapped
           sd = -sd;
           xa = false;
-          neg = (int)(((a.zcls[zr] & 1) ^ (a.bcls[k] & 1)) ^ 1);
-          E = (int64_t)a.zexp[zr] + a.bexp[k] - (norm ? 0 : 1);
+          neg = (int)(((cur_cz & 1) ^ (cb & 1)) ^ 1);
+          E = (int64_t)cur_zexp + bexk - (norm ? 0 : 1);
         }
         if (sd > 0x1p-20) {
           int e2;
@@ -443,8 +511,14 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       // non-normalised products are doubled (P' = P 2^nsh) inside the column
       // combination: the digit weights 2^(8j) become 2^(8j + nsh), so P' limbs come
       // straight out of the carry chain (no funnel shift per limb)
+#if DS_VAR_MULSHIFT
       const uint32_t nsh = norm ? 0u : 1u;
       const uint32_t m0 = 1u << nsh, m1 = 256u << nsh, m2 = 65536u << nsh, m3 = 16777216u << nsh;
+#else
+      const int nsh = norm ? 0 : 1;
+      uint32_t praw = 0u;  // previous unshifted P limb
+      constexpr uint32_t m0 = 1u, m1 = 256u, m2 = 65536u, m3 = 16777216u;
+#endif
       for (int t = 0; t < ntiles; t++) {
         const int gt = q * ntiles + t;
         const int buf = gt & 1;
@@ -490,6 +564,14 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
               "addc.u32 %8, %24, 0;"
                 : "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]), "+r"(carry)
                 : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
+#if !DS_VAR_MULSHIFT
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+              const uint32_t raw = P[g];
+              P[g] = __funnelshift_l(praw, raw, nsh);
+              praw = raw;
+            }
+#endif
 
             const int g0 = (a.c_lo + t * TN + cb) >> 2;
             ok = em.block<8, true>(g0, P);  // r' - zb = 32 L: aligned limbs
@@ -500,7 +582,11 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
         if (lane == 0) mbar_arrive(&bar_tempty[grp][buf]);
       }
       if (process && ok) {
-        em.finish(carry ? 1.0 : 0.0);  // anything above the top limb of P
+#if DS_VAR_MULSHIFT
+        em.finish(carry ? 1.0 : 0.0);  // anything above the top limb of P'
+#else
+        em.finish((carry || (nsh && (praw >> 31))) ? 1.0 : 0.0);  // the bit shifted out of the top limb
+#endif
         if (em.excess) ok = false;
       }
       if (process && !ok) fallback = true;

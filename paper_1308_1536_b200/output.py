@@ -124,10 +124,14 @@ class MinorsStream:
         normalized minors in the same layout) -- see read_minors_binary;
       * keep rows whose size is <= ``keep_upto`` or in ``keep_sizes`` as SoA rows
         (parity checks on the prefix / Laplace rows);
-      * fold every row into a running sha256 (``digest``) and count rows/bytes."""
+      * fold every row into a checksum (``digest``): by default a fast order-aware
+        sum of 64-bit words (numpy; the callback runs on the thread that issues
+        the elimination, so it must stay cheap), or sha256 with hash="sha256".
+    The callback copies what it keeps: its arguments are views of staging memory
+    the engine reuses after it returns."""
 
     def __init__(self, n: int, prec_bits: int, kind: str = "real", path=None, keep_upto: int = 0,
-                 keep_sizes=()):
+                 keep_sizes=(), hash: str = "sum"):
         import hashlib
         self.n, self.p, self.kind = n, prec_bits, kind
         self.ncomp = 2 if kind == "complex" else 1
@@ -136,7 +140,9 @@ class MinorsStream:
         self.kept: dict = {}
         self.sizes: list = []
         self.bytes = 0
-        self._h = hashlib.sha256()
+        self._hash = hash
+        self._h = hashlib.sha256() if hash == "sha256" else None
+        self._sum = 0
         self._f = None
         if path is not None:
             import struct
@@ -159,9 +165,16 @@ class MinorsStream:
                 parts += [np.array(normalized.limbs[:, :, sl]), np.array(normalized.exp[:, sl]),
                           np.array(normalized.cls[:, sl])]
             head = struct.pack("<IB", m, fl)
-            self._h.update(head)
-            for a in parts:
-                self._h.update(a.data)
+            if self._h is not None:
+                self._h.update(head)
+                for a in parts:
+                    self._h.update(a.data)
+            else:  # Fletcher-style sums of the bytes (all words, and every other one), mod 2^64
+                acc = m * 0x9E3779B97F4A7C15 + fl
+                for j, a in enumerate(parts):
+                    b = a.reshape(-1).view(np.uint8)
+                    acc += (2 * j + 1) * int(b.sum(dtype=np.uint64)) + (2 * j + 2) * int(b[::2].sum(dtype=np.uint64))
+                self._sum = (self._sum * 1000003 + acc) & 0xFFFFFFFFFFFFFFFF
             if self._f is not None:
                 self._f.write(head)
                 for a in parts:
@@ -175,7 +188,7 @@ class MinorsStream:
 
     @property
     def digest(self) -> str:
-        return self._h.hexdigest()
+        return self._h.hexdigest() if self._h is not None else f"sum64:{self._sum:016x}"
 
     def close(self):
         if self._f is not None:

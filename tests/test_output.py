@@ -183,4 +183,4 @@ def test_minors_stream_binary_round_trip(tmp_path):
         assert (nm is None) == (not fl & 2)
         if nm is not None:
             assert np.array_equal(nm.limbs, t.limbs[:, :, sl])
-    assert st.sizes == [2, 3, 4, 6] and len(st.digest) == 64
+    assert st.sizes == [2, 3, 4, 6] and st.digest.startswith("sum64:")
