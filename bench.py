@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg (outside the timed region)")
     ap.add_argument("--parity-m", type=int, default=256, help="leading block size of the prefix parity check")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share a GPU (host-staged pivot broadcast; tests only)")
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed (NCCL) step loop even at world size 1 (testing)")
     ap.add_argument("--gen-budget", type=float, default=420.0,
@@ -124,8 +126,11 @@ def build_input(args, pinned: bool, rank: int = 0, world: int = 1, agree=None):
               f"on this host: using random_uniform (same shape, same work)", file=sys.stderr)
         args.family = "random"
     if args.family == "random":
-        from paper_1308_1536_b200.synth import random_uniform_soa
-        A = random_uniform_soa(args.n, args.prec, 2000, pinned=pinned)
+        from paper_1308_1536_b200.synth import counter_uniform_soa, random_uniform_soa
+        if world > 1:  # this rank's rows only (the counter-based draw is a function of (row, col))
+            A = counter_uniform_soa(args.n, args.prec, 2000, rows=range(rank, args.n, world), pinned=pinned)
+        else:
+            A = random_uniform_soa(args.n, args.prec, 2000, pinned=pinned)
     return A, workload_desc(args), time.perf_counter() - t0
 
 
@@ -349,12 +354,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())  # gloo test runs: ranks may share a GPU
     torch.cuda.set_device(local)
     dist = None
     use_dist = world > 1 or args.dist
     if use_dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:  # ranks sharing one GPU (tests): host-staged broadcasts
+            dist.init_process_group("gloo")
     from paper_1308_1536_b200.engine import DeviceElimination, HostResults
     from paper_1308_1536_b200.soa import SoA
 
@@ -363,7 +372,8 @@ def main():
     agree = None
     if use_dist:
         def agree(x: float) -> float:
-            t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([x], dtype=torch.float64,
+                             device=f"cuda:{local}" if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
     A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world, agree=agree)  # this rank's rows
@@ -373,14 +383,35 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     pivot = None
+    bcast, la_ok = None, True
     if use_dist:
         from paper_1308_1536_b200.parexec import dist_run
         _, pbytes = eng.pivot_buffer()
         pivot = torch.empty(pbytes, dtype=torch.uint8, device=f"cuda:{local}")
         eng.lib.ds_use_pivot_buffer(eng.ctx, pivot.data_ptr(), pbytes)
+        if args.dist_backend == "nccl":
+            bcast = lambda t, src: dist.broadcast(t, src=src)  # noqa: E731
+        else:
+            staging = {}
+            la_ok = False
+
+            def bcast(t, src):
+                host = staging.get(t.numel())
+                if host is None:
+                    host = staging[t.numel()] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+                if rank == src:
+                    host.copy_(t)
+                dist.broadcast(host, src=src)
+                if rank != src:
+                    t.copy_(host)
     eng.lib.ds_set_stream(eng.ctx, stream.cuda_stream)
+    # host buffers of this rank only: owned rows (count nloc * n) when sharded
+    nloc = (n - rank + world - 1) // world
     res = HostResults.alloc(n, 1, L, True, pinned=True)
-    final = SoA(1, L, n * n, pinned=True)
+    if world > 1:
+        res = HostResults(SoA(1, L, n, pinned=True), SoA(1, L, n, pinned=True), SoA(1, L, nloc * n, pinned=True),
+                          SoA(1, L, nloc * n, pinned=True), res.row_flags)
+    final = SoA(1, L, nloc * n, pinned=True)
 
     def one_pass(resident: bool):
         if resident:
@@ -394,7 +425,7 @@ def main():
                 eng.run(True, True, 0, n, res)
                 eng.fetch(final)  # the in-place L\\U state is part of the result (elim.py:19-22)
         else:
-            dist_run(eng, n, True, True, pivot, lambda t, src: dist.broadcast(t, src=src))
+            dist_run(eng, n, True, True, pivot, bcast, lookahead=la_ok)
             if not resident:
                 eng.results(n, res)
                 eng.fetch(final)
@@ -408,8 +439,15 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t)
         return float(t.item())
 
     eng.load(A)
@@ -448,9 +486,11 @@ def main():
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
         c1 = eng.counters()
+        h2d = sum_over_ranks(c1["h2d_bytes"] - c0["h2d_bytes"])  # whole job: every rank copies its own rows
+        d2h = sum_over_ranks(c1["d2h_bytes"] - c0["d2h_bytes"])
         e2e = {"value": total_work / e2e_s, "unit": "limb-MAC/s",
-               "h2d_bytes_per_step": int((c1["h2d_bytes"] - c0["h2d_bytes"]) / args.steps),
-               "d2h_bytes_per_step": int((c1["d2h_bytes"] - c0["d2h_bytes"]) / args.steps),
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps),
                "bytes_counted_by": "ds_counters (every ABI host<->device copy of this context)",
                "seconds_to_all_minors": e2e_s,
                "includes": "H2D matrix, elimination, D2H pivots/dets/signed+normalized minors/final L\\U matrix"}

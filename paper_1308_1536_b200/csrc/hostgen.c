@@ -269,7 +269,9 @@ int dsh_beta_matrix_cols(int N, long p, const char **zeros, int guard_bits, int 
       mpc_div(term, pAg, den, RNN);
       mpfr_mul_si(val, mpc_realref(term), -2, RN);     /* -2 * term.real */
       mpfr_set(outp, val, RN);                         /* mpfr(val) at prec */
-      put_soa(out, (int64_t)(n - 1) * N + j, outp, L);
+      /* full N x N output, or only rows row0, row0 + rstep, ... (count nloc * N) */
+      const int64_t ridx = out->count == (int64_t)N * N ? (int64_t)(n - 1) : (int64_t)((n - 1 - row0) / rstep);
+      put_soa(out, ridx * N + j, outp, L);
     }
     mpfr_clears(tp, tt, pi, lp, A, lnn, val, ztmp, outp, (mpfr_ptr)0);
     mpc_clear(I); mpc_clear(z); mpc_clear(g); mpc_clear(v); mpc_clear(w2); mpc_clear(pref); mpc_clear(pAg);

@@ -102,7 +102,10 @@ class BetaBuilder:
         self.N, self.p, self.guard, self.nthreads = N, prec_bits, guard_bits, nthreads
         toks = read_zero_tokens(zeros_path, N)
         self._arr = (ctypes.c_char_p * N)(*[t.encode() for t in toks])
-        self.out = SoA(1, (prec_bits + 31) // 32, N * N, pinned=pinned)
+        # a rank of a sharded run (rstep > 1) holds only its rows: count nloc * N, the
+        # layout ds_load accepts for owned rows
+        nloc = (N - row0 + rstep - 1) // rstep if rstep > 1 else N
+        self.out = SoA(1, (prec_bits + 31) // 32, nloc * N, pinned=pinned)
         self._c = self.out.c()
         self._g = gammas
         self._gc = gammas.c() if gammas is not None else None

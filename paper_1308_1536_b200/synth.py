@@ -95,16 +95,19 @@ def counter_uniform_soa(n: int, p: int, seed: int, rows=None, pinned: bool = Fal
     clz = np.where(zero, 0, 32 - e2).astype(np.int64)
     lz = 32 * (L - 1 - np.maximum(top, 0)) + clz
     lq, lr = lz // 32, lz % 32
-    Ms = np.concatenate([np.zeros((1, cnt), dtype=np.uint32), M], axis=0)  # Ms[l+1] = M_l, Ms[0] = 0
     out = s.limbs[0]
-    cols = np.arange(cnt)
+    # common case (top limb of M nonzero, lz < 32): one funnel shift per limb plane
+    lr64 = lr.astype(np.uint64)
+    sh_lo = (np.uint64(32) - lr64)
+    prev = np.zeros(cnt, dtype=np.uint64)
     for l in range(L):
-        hi_i = np.clip(l - lq + 1, 0, L)  # index into Ms of M_{l-lq}
-        lo_i = np.clip(l - lq, 0, L)
-        hi = np.where(l - lq >= 0, Ms[hi_i, cols], 0).astype(np.uint64)
-        lo = np.where(l - lq - 1 >= 0, Ms[lo_i, cols], 0).astype(np.uint64)
-        w = ((hi << lr.astype(np.uint64)) | np.where(lr > 0, lo >> (32 - lr).astype(np.uint64), 0)) & np.uint64(0xFFFFFFFF)
-        out[l] = w.astype(np.uint32)
+        hi = M[l].astype(np.uint64)
+        out[l] = (((hi << lr64) | (prev >> sh_lo)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+        prev = hi
+    # rare: M's top limb is zero (lz >= 32): shift exactly with Python integers
+    for e in np.nonzero((lq > 0) & ~zero)[0]:
+        Mi = int.from_bytes(np.ascontiguousarray(M[:, e]).tobytes(), "little") << int(lz[e])
+        out[:, e] = np.frombuffer(Mi.to_bytes(4 * L, "little"), dtype=np.uint32)
     exp[:] = 1 - lz
     # K = 0 (not pos, no nonzero limb): x = -1;  M = 0 (pos, K = 2^(32L-1)): x = +0
     m1 = (~pos) & (f == L)

@@ -138,3 +138,18 @@ def test_torchrun_lookahead_matches_single_process(tmp_path):
         sl = slice((m - 1) * n, (m - 1) * n + m)
         assert np.array_equal(z["sl"][:, :, sl], res.signed.limbs[:, :, sl])
         assert np.array_equal(z["se"][:, sl], res.signed.exp[:, sl])
+
+
+def test_bench_two_ranks_one_gpu_gloo():
+    """bench.py's multi-rank loop (row-cyclic shards, per-step pivot broadcast, max-over-ranks
+    timing) with 2 ranks on this box's one GPU: gloo with host staging stands in for NCCL (two
+    ranks may not share a device under NCCL).  The rank-0 JSON line reports n_gpus = 2 and the
+    parity leg is skipped (it needs the whole matrix on one rank)."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+                        "--steps", "1", "--warmup", "1", "--dim", "160", "--bits", "1024", "--family", "random",
+                        "--no-cpu", "--dist-backend", "gloo"], timeout=900, cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
