@@ -360,3 +360,57 @@ int dsh_soa_to_mpfr(__mpfr_struct *out, const ds_soa *s, int c, int64_t start, i
   }
   return 0;
 }
+
+void mpfr_set_zero(mpfr_ptr, int);
+
+/* Pooled variant: the mpfr_t structs point into one caller-owned limb pool
+ * (n64 = ceil(p/64) words per scalar, element-major) instead of a malloc per
+ * scalar -- the same representation mpfr_custom_init_set builds (regular
+ * numbers: precision, sign, exponent, significand pointer; zeros through
+ * mpfr_set_zero).  The Python wrappers keep the pool alive and never call
+ * mpfr_clear on these structs. */
+int dsh_soa_to_mpfr_pool(__mpfr_struct *out, uint64_t *pool, const ds_soa *s, int c, int64_t start, int64_t count,
+                         int L, long p) {
+  const int n64 = (int)((p + 63) / 64), pad = 2 * n64 - L;
+  const uint32_t *base = s->limbs + (int64_t)c * L * s->count;
+  for (int64_t k = 0; k < count; k++) {
+    const int64_t idx = start + k;
+    __mpfr_struct *x = &out[k];
+    uint64_t *d = pool + k * n64;
+    x->_mpfr_prec = p;
+    x->_mpfr_d = (mp_limb_t *)d;
+    const uint8_t cl = s->cls[(int64_t)c * s->count + idx];
+    if (cl >= DS_CLS_PZERO) {
+      for (int q = 0; q < n64; q++) d[q] = 0;
+      mpfr_set_zero(x, cl == DS_CLS_NZERO ? -1 : 1);
+      continue;
+    }
+    for (int q = 0; q < n64; q++) {
+      const int l0 = 2 * q - pad, l1 = 2 * q + 1 - pad;
+      const uint64_t lo = l0 >= 0 ? base[(int64_t)l0 * s->count + idx] : 0u;
+      const uint64_t hi = l1 >= 0 ? base[(int64_t)l1 * s->count + idx] : 0u;
+      d[q] = lo | (hi << 32);
+    }
+    x->_mpfr_exp = s->exp[(int64_t)c * s->count + idx];
+    x->_mpfr_sign = cl == DS_CLS_NEG ? -1 : 1;
+  }
+  return 0;
+}
+
+/* Fastest form: the limb pool is already element-major (n64 words per scalar,
+ * built by one numpy transpose of the SoA row); only the struct fields are set. */
+int dsh_mpfr_structs(__mpfr_struct *out, uint64_t *pool, const int32_t *ex, const uint8_t *cl, int64_t count,
+                     int n64, long p) {
+  for (int64_t k = 0; k < count; k++) {
+    __mpfr_struct *x = &out[k];
+    x->_mpfr_prec = p;
+    x->_mpfr_d = (mp_limb_t *)(pool + k * n64);
+    if (cl[k] >= DS_CLS_PZERO) {
+      mpfr_set_zero(x, cl[k] == DS_CLS_NZERO ? -1 : 1);
+      continue;
+    }
+    x->_mpfr_exp = ex[k];
+    x->_mpfr_sign = cl[k] == DS_CLS_NEG ? -1 : 1;
+  }
+  return 0;
+}

@@ -35,6 +35,12 @@ def _load():
         L.dsh_beta_gammas.restype = ctypes.c_int
         L.dsh_beta_gammas.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(ds_soa)]
+        L.dsh_mpfr_structs.restype = ctypes.c_int
+        L.dsh_mpfr_structs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_int64, ctypes.c_int, ctypes.c_long]
+        L.dsh_soa_to_mpfr_pool.restype = ctypes.c_int
+        L.dsh_soa_to_mpfr_pool.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ds_soa), ctypes.c_int,
+                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_long]
         L.dsh_soa_to_mpfr.restype = ctypes.c_int
         L.dsh_soa_to_mpfr.argtypes = [ctypes.c_void_p, ctypes.POINTER(ds_soa), ctypes.c_int, ctypes.c_int64,
                                       ctypes.c_int64, ctypes.c_int, ctypes.c_long]

@@ -650,6 +650,27 @@ def from_limbs(raw: bytes, exp: int, cls: int, prec: int) -> "mpfr":
     return r
 
 
+class _pooled_mpfr(mpfr):
+    """mpfr over a struct whose significand lives in a shared limb pool
+    (SoA.scalars): the pool is kept alive by the object, and nothing is freed per
+    scalar.  Behaves as mpfr everywhere (isinstance, arithmetic, formatting)."""
+    __slots__ = ("_pool",)
+
+    def __del__(self):
+        pass
+
+
+def wrap_pooled(arr, pool, count: int) -> list:
+    new = object.__new__
+    out = []
+    for k in range(count):
+        o = new(_pooled_mpfr)
+        o._s = arr[k]
+        o._pool = pool
+        out.append(o)
+    return out
+
+
 def wrap_structs(arr, count: int) -> list:
     """mpfr objects over the already-initialised structs of a ctypes array
     (each keeps the array alive; __del__ clears its own limbs)."""

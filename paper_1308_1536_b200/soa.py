@@ -86,12 +86,18 @@ class SoA:
             return []
         from .hostgen import _load
         lib = _load()
-        c_soa = self.c()
+        n64 = (prec + 63) // 64
+        pad = 2 * n64 - self.L
         parts = []
         for c in range(self.ncomp):
+            # element-major limb pool (one transpose), read in place by the mpfr structs
+            pool = np.zeros((count, 2 * n64), dtype=np.uint32)
+            pool[:, pad:] = self.limbs[c, :, start:start + count].T
+            ex = np.ascontiguousarray(self.exp[c, start:start + count])
+            cl = np.ascontiguousarray(self.cls[c, start:start + count])
             arr = (mp._MPFR_T * count)()
-            lib.dsh_soa_to_mpfr(arr, ctypes.byref(c_soa), c, start, count, self.L, prec)
-            parts.append(mp.wrap_structs(arr, count))
+            lib.dsh_mpfr_structs(arr, pool.ctypes.data, ex.ctypes.data, cl.ctypes.data, count, n64, prec)
+            parts.append(mp.wrap_pooled(arr, (arr, pool), count))
         if self.ncomp == 1:
             return parts[0]
         return [mp.mpc_from_parts(a, b) for a, b in zip(parts[0], parts[1])]
