@@ -1546,7 +1546,13 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   plan->c_lo = clo;
   // TMEM: 2 NG accumulator buffers of tn columns + 8 nks columns of A <= 512;
   // two epilogue groups if their windows fit in shared memory, else one
-  if (p < 256) return DS_OK;  // not applicable: other engines
+  // measured crossover (profiles/r02_smallp_engines.log, N=1000, all minors): the
+  // FP64-digit engine wins at 256 and 512 bits (0.117 vs 0.139 s, 0.134 vs 0.149 s),
+  // the tensor cores from 1024 bits on (0.180 vs 0.246 s); DS_TC_MIN_BITS overrides
+  int min_bits = 768;
+  if (const char* e = getenv("DS_TC_MIN_BITS")) min_bits = atoi(e);
+  if (min_bits < 256) min_bits = 256;
+  if (p < min_bits) return DS_OK;  // not applicable: other engines
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   size_t smem = 0;

@@ -15,7 +15,7 @@ from paper_1308_1536_b200.engine import HostResults
 from paper_1308_1536_b200.synth import random_uniform_soa
 
 pytestmark = pytest.mark.gpu
-WIDE = {"DS_TC_WIDE": "1"}
+WIDE = {"DS_TC_WIDE": "1", "DS_TC_MIN_BITS": "256"}
 
 
 def _oracle(A, n, p, steps, minors=True):
@@ -120,6 +120,7 @@ def test_wide_complex_real_valued_and_imaginary():
             m = i % 3
             vals.append(mp.mpc(x, 0) if m == 0 else (mp.mpc(0, x) if m == 1 else mp.mpc(x, -x)))
     A = SoA.from_scalars(vals, p, "complex")
+    from paper_1308_1536_b200.engine import DeviceElimination
     rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
     rc_d, done_d, res_d, fin_d = device_eliminate(A, n, p, "complex")
     assert done_o == done_d
@@ -167,3 +168,32 @@ def test_wide_complex_matches_general_engine(budget_mb):
     assert np.array_equal(fin_t.exp, fin_g.exp)
     assert np.array_equal(fin_t.limbs, fin_g.limbs)
     assert results_digest(res_t, fin_t, n, p, steps) == results_digest(res_g, fin_g, n, p, steps)
+
+
+@pytest.mark.parametrize("n,p,bad", [(12, 256, 2), (20, 1024, 5), (10, 4096, 3)])
+def test_complex_zero_pivot_after_first_step(n, p, bad):
+    """A complex matrix whose leading (bad+1)-minor is exactly singular (row `bad` duplicates row 0,
+    so it is eliminated to exact zeros by step 0): the device stops at step `bad` with every earlier minors row
+    emitted -- the side-stream emission of size bad+1 must not be cancelled by the later zero
+    pivot (the reference emits it before raising, elim.py:209-226)."""
+    import random
+    from paper_1308_1536_b200 import mp
+    from paper_1308_1536_b200.soa import SoA
+    rnd = random.Random(n * p + bad)
+    with mp.context(precision=p):
+        rows = [[mp.mpc(rnd.randint(-9, 9), rnd.randint(-9, 9)) for _ in range(n)] for _ in range(n)]
+        rows[bad] = list(rows[0])
+        vals = [x for r in rows for x in r]
+    A = SoA.from_scalars(vals, p, "complex")
+    from paper_1308_1536_b200.engine import DeviceElimination
+    rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
+    assert done_o == bad
+    with DeviceElimination(n, p, "complex") as eng:
+        eng.load(A)
+        res_d = HostResults.alloc(n, 2, eng.L, True)
+        rc, done_d = eng.run(True, True, 0, n, res_d)
+        fin_d = A.copy()
+        eng.fetch(fin_d)
+    assert done_d == bad
+    assert results_digest(res_o, fin_o, n, p, done_o) == results_digest(res_d, fin_d, n, p, done_d)
+    assert res_d.row_flags[bad] & 1  # size bad+1 emitted

@@ -3,6 +3,8 @@ against the oracle: with a_00 = 1 the first step uses z_j = a_j0 exactly, so
 a_jk can be crafted relative to RN(z_j * b_k) -- exact cancellation, +-1 ulp
 residues, exponent gaps around p+2, exact (integer / power-of-two) products
 that force the full-product fallback, all-ones mantissas, signed zeros."""
+import os
+
 import pytest
 
 import oracle
@@ -88,12 +90,26 @@ def test_fused_update_adversarial(p, steps):
     ref.run(True, True, 0, steps, res_o)
     fin_o = A.copy()
     ref.fetch(fin_o)
-    with DeviceElimination(n, p, "real") as eng:
-        eng.load(A)
-        res_d = HostResults.alloc(n, 1, eng.L, True)
-        eng.run(True, True, 0, steps, res_d)
-        fin_d = A.copy()
-        eng.fetch(fin_d)
-    mism = first_mismatch(fin_o, fin_d, p)
-    assert not mism, mism
-    assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)
+    # below the engine crossover (768 bits) run the tensor-core engine too (DS_TC_MIN_BITS)
+    for env in ([None, "256"] if 256 <= p < 768 else [None]):
+        old = os.environ.get("DS_TC_MIN_BITS")
+        if env:
+            os.environ["DS_TC_MIN_BITS"] = env
+        try:
+            with DeviceElimination(n, p, "real") as eng:
+                eng.load(A)
+                res_d = HostResults.alloc(n, 1, eng.L, True)
+                eng.run(True, True, 0, steps, res_d)
+                fin_d = A.copy()
+                eng.fetch(fin_d)
+                if env:
+                    assert eng.counters()["tc_engine"]
+        finally:
+            if env:
+                if old is None:
+                    os.environ.pop("DS_TC_MIN_BITS", None)
+                else:
+                    os.environ["DS_TC_MIN_BITS"] = old
+        mism = first_mismatch(fin_o, fin_d, p)
+        assert not mism, mism
+        assert results_digest(res_o, fin_o, n, p, steps) == results_digest(res_d, fin_d, n, p, steps)

@@ -24,7 +24,7 @@ for r in rows:
 MARKERS = {"ds_tc.cu": [("tc helpers", None), ("tc setup", "k_update_tc(TcArgs"),
                          ("pipelines", "pipelines: banks + MMAs"), ("epi setup+prefetch", "epilogue\n"),
                          ("epi tiles", "for (int t = 0; t < ntiles; t++) {\n        const int gt"),
-                         ("epi tail", "if (process && ok) {\n        em.finish")],
+                         ("epi tail", "if (process && ok) {\n#if DS_VAR_MULSHIFT")],
            "ds_stream.cuh": [("stream helpers", None), ("swin access", "struct SWin {"),
                              ("swin init/push/finish", "void init("), ("swin fast_block", "void fast_block("),
                              ("emit", "struct Emit {"), ("round_out", "void round_out(")]}
