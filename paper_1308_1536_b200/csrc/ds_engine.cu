@@ -229,6 +229,7 @@ struct KArgs {
   int32_t* status;
   uint32_t* scratch; int64_t scratch_threads; int64_t scratch_words;
   int64_t m_count; int m_rows;  // minors storage: plane stride, ring rows (local row jl -> slot jl % m_rows)
+  int sm_threads;  // > 0: the thread-level kernel keeps its scratch in shared memory (blockDim threads)
 };
 
 static KArgs kargs(ds_ctx* c) {
@@ -245,7 +246,36 @@ static KArgs kargs(ds_ctx* c) {
   k.sig_cls = c->sig_cls; k.nrm_cls = c->nrm_cls; k.row_flags = c->row_flags; k.status = c->status;
   k.scratch = c->scratch; k.scratch_threads = c->scratch_threads; k.scratch_words = c->scratch_words;
   k.m_count = c->m_count; k.m_rows = c->m_rows;
+  k.sm_threads = 0;
   return k;
+}
+
+// per-thread scratch of the thread-level (complex) kernels: shared memory when
+// the launch gave each thread its words there (latency ~30 cycles instead of an
+// L2 round trip per limb in the O(L^2) exact products and divisions), else global
+__device__ __forceinline__ Ptr kscratch(const KArgs& k, int64_t tid) {
+  if (k.sm_threads) {
+    extern __shared__ uint32_t ksm[];
+    return Ptr{ksm + threadIdx.x, (int64_t)blockDim.x};
+  }
+  return Ptr{k.scratch + tid, k.scratch_threads};
+}
+
+// operand q (0..3) of this thread copied into shared memory after its scratch
+// (the O(L^2) product loops re-read every operand limb L times: from global
+// memory each limb is a separate line, and the large shared-memory carve-out
+// leaves little L1 to hold them)
+__device__ __forceinline__ Val kstage(const KArgs& k, const Val& v, int q) {
+  if (!k.sm_threads) return v;
+  extern __shared__ uint32_t ksm[];
+  const int64_t T = blockDim.x;
+  uint32_t* dst = ksm + (k.scratch_words + (int64_t)q * k.L) * T + threadIdx.x;
+  for (int l = 0; l < k.L; l++) dst[(int64_t)l * T] = v.m[l];
+  Val o;
+  o.m = CPtr{dst, T};
+  o.e = v.e;
+  o.c = v.c;
+  return o;
 }
 
 // first element of local row jl's minors slot (ring of m_rows rows)
@@ -410,7 +440,11 @@ __global__ void k_det_step(KArgs k, int i, int from_cur) {
   Val p1 = val_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, k.ncomp - 1, k.L, i);
   Out d0 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
   Out d1 = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
-  if (!g_mul(d0, d1, q0, q1, p0, p1, k.kind, k.L, k.p, thread_scratch(k, 0))) atomicAdd(&k.status[2], 1);
+  q0 = kstage(k, q0, 0);
+  q1 = kstage(k, q1, 1);
+  p0 = kstage(k, p0, 2);
+  p1 = kstage(k, p1, 3);
+  if (!g_mul(d0, d1, q0, q1, p0, p1, k.kind, k.L, k.p, kscratch(k, 0))) atomicAdd(&k.status[2], 1);
 }
 
 // first local row index with global row > i
@@ -463,10 +497,10 @@ __global__ void k_mult_c2(KArgs k, int i, int jl0) {
     const int c = (int)(t & 1);
     int64_t jl = jl0 + (t >> 1);
     int64_t idx = jl * k.n + i;
-    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx);
-    Val a1 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx);
+    Val a0 = kstage(k, val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx), 0);
+    Val a1 = kstage(k, val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx), 1);
     Out z = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, c, k.L, jl);
-    if (!cdiv_part(z.m, z.e, z.c, a0, a1, b0, b1, c == 1, k.L, k.p, thread_scratch(k, tid),
+    if (!cdiv_part(z.m, z.e, z.c, a0, a1, kstage(k, b0, 2), kstage(k, b1, 3), c == 1, k.L, k.p, kscratch(k, tid),
                    (unsigned int*)&k.status[3]))
       atomicAdd(&k.status[2], 1);
   }
@@ -504,10 +538,11 @@ __global__ void k_emit_signed_c2(KArgs k, int i) {
       set_val(so, c == 0 ? d0 : d1, k.L);
       continue;
     }
-    Val a0 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, oidx);
-    Val a1 = val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, oidx);
-    bool ok = c == 0 ? cmul_part(so.m, so.e, so.c, d0, a0, d1, a1, true, k.L, k.p, thread_scratch(k, tid))
-                     : cmul_part(so.m, so.e, so.c, d0, a1, d1, a0, false, k.L, k.p, thread_scratch(k, tid));
+    const Val a0 = kstage(k, val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, oidx), 0);
+    const Val a1 = kstage(k, val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, oidx), 1);
+    const Val e0 = kstage(k, d0, 2), e1 = kstage(k, d1, 3);
+    bool ok = c == 0 ? cmul_part(so.m, so.e, so.c, e0, a0, e1, a1, true, k.L, k.p, kscratch(k, tid))
+                     : cmul_part(so.m, so.e, so.c, e0, a1, e1, a0, false, k.L, k.p, kscratch(k, tid));
     if (!ok) atomicAdd(&k.status[2], 1);
   }
 }
@@ -526,10 +561,10 @@ __global__ void k_emit_norm_c2(KArgs k, int i) {
   for (int64_t t = tid; t < 2 * (int64_t)m; t += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(t & 1);
     int64_t idx = r0 + (t >> 1);
-    Val s0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx);
-    Val s1 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, idx);
+    const Val s0 = kstage(k, val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx), 0);
+    const Val s1 = kstage(k, val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, idx), 1);
     Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, c, k.L, idx);
-    if (!cdiv_part(o.m, o.e, o.c, s0, s1, l0, l1, c == 1, k.L, k.p, thread_scratch(k, tid),
+    if (!cdiv_part(o.m, o.e, o.c, s0, s1, kstage(k, l0, 2), kstage(k, l1, 3), c == 1, k.L, k.p, kscratch(k, tid),
                    (unsigned int*)&k.status[3]))
       atomicAdd(&k.status[2], 1);
   }
@@ -1405,6 +1440,32 @@ static void set_wdiv_attrs(int maxsm) {
 #undef SA
 }
 
+// shared-memory scratch for the thread-level complex kernels: threads per block
+// = how many per-thread scratch areas fit (<= 8, and no more than the work
+// items); 0 when one does not fit (very wide precisions: global scratch)
+static size_t cx_smem_launch(ds_ctx* ctx, KArgs* k, int64_t work) {
+  static int maxsm = 0;
+  static bool attrs = false;
+  if (!maxsm) cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  const size_t per = sizeof(uint32_t) * ((size_t)ctx->scratch_words + 4 * (size_t)ctx->L);  // scratch + 4 operands
+  int t = per ? (int)((size_t)maxsm / per) : 0;
+  if (t > 8) t = 8;
+  if (work < t) t = (int)(work > 0 ? work : 1);
+  if (t < 1 || getenv("DS_CX_GLOBAL_SCRATCH")) {
+    k->sm_threads = 0;
+    return 0;
+  }
+  if (!attrs) {
+    cudaFuncSetAttribute(k_det_step, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_mult_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_emit_signed_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_emit_norm_c2, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    attrs = true;
+  }
+  k->sm_threads = t;
+  return per * (size_t)t;
+}
+
 int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   if (i < 0 || i >= ctx->n) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
@@ -1440,7 +1501,11 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     if (!first) {
       CK(cudaEventRecord(ctx->ev_piv, s));
       CK(cudaStreamWaitEvent(ctx->side, ctx->ev_piv, 0));
-      k_det_step<<<1, 32, 0, ctx->side>>>(ks, i, ctx->det_from_cur);
+      {
+        KArgs kd = ks;
+        const size_t sm = cx_smem_launch(ctx, &kd, 1);
+        k_det_step<<<1, kd.sm_threads ? 1 : 32, sm, ctx->side>>>(kd, i, ctx->det_from_cur);
+      }
       ctx->launches++;
     }
   } else if (fast) {
@@ -1490,7 +1555,15 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
       size_t smem = (size_t)wpb * wwords * 4;
       WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0, nullptr);
     } else if (cxf) {
-      k_mult_c2<<<grid_for(ctx, 2 * (int64_t)nrows, 64), 64, 0, s>>>(k, i, jl0);
+      {
+        KArgs km = k;
+        const size_t sm = cx_smem_launch(ctx, &km, 2 * (int64_t)nrows);
+        if (km.sm_threads)
+          k_mult_c2<<<(unsigned)((2 * (int64_t)nrows + km.sm_threads - 1) / km.sm_threads), km.sm_threads, sm, s>>>(
+              km, i, jl0);
+        else
+          k_mult_c2<<<grid_for(ctx, 2 * (int64_t)nrows, 64), 64, 0, s>>>(k, i, jl0);
+      }
       k_neg_z<<<grid_for(ctx, 2 * (int64_t)nrows, 64), 64, 0, s>>>(k, i, jl0);
       ctx->launches++;
     } else {
@@ -1593,8 +1666,16 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         cudaStream_t ss = ctx->side;
         CK(cudaEventRecord(ctx->ev_upd, s));
         CK(cudaStreamWaitEvent(ss, ctx->ev_upd, 0));
-        k_emit_signed_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
-        k_emit_norm_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
+        KArgs ke = ks;
+        const size_t sm = cx_smem_launch(ctx, &ke, 2 * (int64_t)m);
+        if (ke.sm_threads) {
+          const unsigned nb = (unsigned)((2 * (int64_t)m + ke.sm_threads - 1) / ke.sm_threads);
+          k_emit_signed_c2<<<nb, ke.sm_threads, sm, ss>>>(ke, i);
+          k_emit_norm_c2<<<nb, ke.sm_threads, sm, ss>>>(ke, i);
+        } else {
+          k_emit_signed_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
+          k_emit_norm_c2<<<grid_for(ctx, 2 * (int64_t)m, 64), 64, 0, ss>>>(ks, i);
+        }
         ctx->launches += 2;
       } else {
         k_emit_signed<<<grid_for(ctx, m, 64), 64, 0, s>>>(k, i);
