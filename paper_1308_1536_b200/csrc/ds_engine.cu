@@ -25,6 +25,7 @@
 #include "ds_update.cuh"
 #include "ds_tc.cuh"
 #include "ds_warpdiv.cuh"
+#include "ds_cwarp.cuh"
 
 using namespace ds;
 
@@ -568,6 +569,120 @@ __global__ void k_emit_norm_c2(KArgs k, int i) {
                    (unsigned int*)&k.status[3]))
       atomicAdd(&k.status[2], 1);
   }
+}
+
+// ---- complex step on warps (ds_cwarp.cuh): one warp per (item, component),
+// each warp with its own shared-memory region of cw_words words
+__device__ __forceinline__ dscw::Region cw_region(const KArgs& k, int cw_words) {
+  extern __shared__ uint32_t cwsm[];
+  return dscw::Region(cwsm + (int64_t)(threadIdx.x >> 5) * cw_words, k.L, k.p);
+}
+
+// z_j = RN(a_ji / piv) per component (elim.py:47); a_ji <- -z_j by k_neg_z
+__global__ void k_cw_mult(KArgs k, int i, int jl0, int cw_words) {
+  if (k.status[0] >= 0) return;
+  const int wpb = blockDim.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  const int nrows = k.nloc - jl0;
+  if (t >= 2 * (int64_t)nrows) return;
+  dscw::Region R = cw_region(k, cw_words);
+  const int c = (int)(t & 1);
+  const int64_t jl = jl0 + (t >> 1);
+  const int64_t idx = jl * k.n + i;
+  PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
+  const Val a0 = dscw::stage(val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, idx), R.op, k.L);
+  const Val a1 = dscw::stage(val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, idx), R.op + k.L, k.L);
+  const Val b0 = dscw::stage(val_at(pb.limbs, pb.exp, pb.cls, k.n, 0, k.L, i), R.op + 2 * k.L, k.L);
+  const Val b1 = dscw::stage(val_at(pb.limbs, pb.exp, pb.cls, k.n, 1, k.L, i), R.op + 3 * k.L, k.L);
+  __syncwarp();
+  Out z = out_at(k.z_limbs, k.z_exp, k.z_cls, k.nloc, c, k.L, jl);
+  if (!dscw::wcdiv_part(z.m, z.e, z.c, a0, a1, b0, b1, c == 1, k.L, k.p, R, (unsigned int*)&k.status[3]) &&
+      (threadIdx.x & 31) == 0)
+    atomicAdd(&k.status[2], 1);
+}
+
+// det_i = RN(det_{i-1} * piv_i) per component (elim.py:213-215); 2 warps
+__global__ void k_cw_det(KArgs k, int i, int from_cur, int cw_words) {
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
+  const int c = threadIdx.x >> 5;
+  if (c > 1) return;
+  dscw::Region R = cw_region(k, cw_words);
+  const Val q0 = dscw::stage(from_cur ? val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 0, k.L, 0)
+                                      : val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i - 1),
+                             R.op, k.L);
+  const Val q1 = dscw::stage(from_cur ? val_at(k.cur_limbs, k.cur_exp, k.cur_cls, 1, 1, k.L, 0)
+                                      : val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 1, k.L, i - 1),
+                             R.op + k.L, k.L);
+  const Val p0 = dscw::stage(val_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, 0, k.L, i), R.op + 2 * k.L, k.L);
+  const Val p1 = dscw::stage(val_at(k.piv_limbs, k.piv_exp, k.piv_cls, k.n, 1, k.L, i), R.op + 3 * k.L, k.L);
+  __syncwarp();
+  Out d = out_at(k.det_limbs, k.det_exp, k.det_cls, k.n, c, k.L, i);
+  // re = q0 p0 - q1 p1, im = q0 p1 + q1 p0 (g_mul / cmul_part order)
+  const bool ok = c == 0 ? dscw::wcmul_part(d.m, d.e, d.c, q0, p0, q1, p1, true, k.L, k.p, R)
+                         : dscw::wcmul_part(d.m, d.e, d.c, q0, p1, q1, p0, false, k.L, k.p, R);
+  if (!ok && (threadIdx.x & 31) == 0) atomicAdd(&k.status[2], 1);
+}
+
+// signed minors of size m = i+2 per component (elim.py:56-61)
+__global__ void k_cw_emit_signed(KArgs k, int i, int cw_words) {
+  if (k.status[0] >= 0 && k.status[0] <= i) return;  // see k_emit_signed_c2
+  const int m = i + 2;
+  const int64_t jl = (i + 1) / k.world;
+  const int wpb = blockDim.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  if (t >= 2 * (int64_t)m) return;
+  const int c = (int)(t & 1);
+  const int64_t kk = t >> 1;
+  Out so = out_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, c, k.L, mrow(k, jl) + kk);
+  const Val d0r = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
+  const Val d1r = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 1, k.L, i);
+  if (kk == m - 1) {
+    const Val& dv = c == 0 ? d0r : d1r;
+    for (int l = threadIdx.x & 31; l < k.L; l += 32) so.m[l] = dv.m[l];
+    if ((threadIdx.x & 31) == 0) {
+      *so.e = (int32_t)dv.e;
+      *so.c = dv.c;
+    }
+    return;
+  }
+  dscw::Region R = cw_region(k, cw_words);
+  const int64_t oidx = jl * k.n + kk;
+  const Val a0 = dscw::stage(val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 0, k.L, oidx), R.op, k.L);
+  const Val a1 = dscw::stage(val_at(k.a_limbs, k.a_exp, k.a_cls, k.a_count, 1, k.L, oidx), R.op + k.L, k.L);
+  const Val d0 = dscw::stage(d0r, R.op + 2 * k.L, k.L);
+  const Val d1 = dscw::stage(d1r, R.op + 3 * k.L, k.L);
+  __syncwarp();
+  const bool ok = c == 0 ? dscw::wcmul_part(so.m, so.e, so.c, d0, a0, d1, a1, true, k.L, k.p, R)
+                         : dscw::wcmul_part(so.m, so.e, so.c, d0, a1, d1, a0, false, k.L, k.p, R);
+  if (!ok && (threadIdx.x & 31) == 0) atomicAdd(&k.status[2], 1);
+}
+
+// normalized minors RN(s_k / s_0) per component (elim.py:138-155)
+__global__ void k_cw_emit_norm(KArgs k, int i, int cw_words) {
+  if (k.status[0] >= 0 && k.status[0] <= i) return;
+  const int m = i + 2;
+  const int64_t jl = (i + 1) / k.world;
+  const int64_t r0 = mrow(k, jl);
+  const Val l0r = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
+  const Val l1r = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, r0);
+  const bool lead_zero = is_zero_cls(l0r.c) && is_zero_cls(l1r.c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) k.row_flags[m - 1] = lead_zero ? 1 : 3;
+  if (lead_zero) return;
+  const int wpb = blockDim.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  if (t >= 2 * (int64_t)m) return;
+  const int c = (int)(t & 1);
+  const int64_t idx = r0 + (t >> 1);
+  dscw::Region R = cw_region(k, cw_words);
+  const Val s0 = dscw::stage(val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, idx), R.op, k.L);
+  const Val s1 = dscw::stage(val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, idx), R.op + k.L, k.L);
+  const Val l0 = dscw::stage(l0r, R.op + 2 * k.L, k.L);
+  const Val l1 = dscw::stage(l1r, R.op + 3 * k.L, k.L);
+  __syncwarp();
+  Out o = out_at(k.nrm_limbs, k.nrm_exp, k.nrm_cls, k.m_count, c, k.L, idx);
+  if (!dscw::wcdiv_part(o.m, o.e, o.c, s0, s1, l0, l1, c == 1, k.L, k.p, R, (unsigned int*)&k.status[3]) &&
+      (threadIdx.x & 31) == 0)
+    atomicAdd(&k.status[2], 1);
 }
 
 // general-engine update: a_jk <- RN(a_jk - RN(z_j * b_k)); used for complex
@@ -1466,6 +1581,40 @@ static size_t cx_smem_launch(ds_ctx* ctx, KArgs* k, int64_t work) {
   return per * (size_t)t;
 }
 
+// warps per block of the warp-level complex kernels (0: their region does not fit
+// in shared memory -- wide precisions keep the thread-level kernels)
+static int cw_plan(ds_ctx* ctx, int* words) {
+  static int maxsm = 0;
+  static bool attrs = false;
+  static int dyn_max = 0;  // opt-in maximum minus the kernels' static shared memory
+  if (!maxsm) {
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    dyn_max = maxsm - 4096;
+  }
+  const int64_t w = dscw::warp_words(ctx->L, ctx->p);
+  *words = (int)w;
+  if (getenv("DS_CX_THREAD")) return 0;
+  int64_t wpb = (int64_t)dyn_max / (4 * w);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1 || ctx->L > 512) return 0;
+  if (!attrs) {
+    bool ok = cudaFuncSetAttribute(k_cw_det, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) == cudaSuccess &&
+              cudaFuncSetAttribute(k_cw_mult, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) == cudaSuccess &&
+              cudaFuncSetAttribute(k_cw_emit_signed, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) ==
+                  cudaSuccess &&
+              cudaFuncSetAttribute(k_cw_emit_norm, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max) ==
+                  cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      dyn_max = 48 * 1024;  // the default limit: fewer warps per block
+      wpb = (int64_t)dyn_max / (4 * w);
+      if (wpb < 1) return 0;
+    }
+    attrs = true;
+  }
+  return (int)wpb;
+}
+
 int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   if (i < 0 || i >= ctx->n) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
@@ -1501,7 +1650,11 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     if (!first) {
       CK(cudaEventRecord(ctx->ev_piv, s));
       CK(cudaStreamWaitEvent(ctx->side, ctx->ev_piv, 0));
-      {
+      int cw_words = 0;
+      const int cw_wpb = cw_plan(ctx, &cw_words);
+      if (cw_wpb >= 2) {  // one warp per component
+        k_cw_det<<<1, 64, (size_t)2 * cw_words * 4, ctx->side>>>(ks, i, ctx->det_from_cur, cw_words);
+      } else {
         KArgs kd = ks;
         const size_t sm = cx_smem_launch(ctx, &kd, 1);
         k_det_step<<<1, kd.sm_threads ? 1 : 32, sm, ctx->side>>>(kd, i, ctx->det_from_cur);
@@ -1555,7 +1708,12 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
       size_t smem = (size_t)wpb * wwords * 4;
       WDIV_DISPATCH(K, k_mult_w, blocks, 32 * wpb, smem, s, k, i, jl0, wwords, 0, nullptr);
     } else if (cxf) {
-      {
+      int cw_words = 0;
+      const int cw_wpb = cw_plan(ctx, &cw_words);
+      if (cw_wpb >= 1) {  // one warp per (row, component)
+        const unsigned nb = (unsigned)((2 * (int64_t)nrows + cw_wpb - 1) / cw_wpb);
+        k_cw_mult<<<nb, 32 * cw_wpb, (size_t)cw_wpb * cw_words * 4, s>>>(k, i, jl0, cw_words);
+      } else {
         KArgs km = k;
         const size_t sm = cx_smem_launch(ctx, &km, 2 * (int64_t)nrows);
         if (km.sm_threads)
@@ -1591,7 +1749,11 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
                    : update_launch(&ctx->plan, s, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->pbuf,
                                    ctx->z_limbs, ctx->z_exp, ctx->z_cls, ctx->nloc, n, i, jl0, collect_minors,
                                    ctx->status, &ctx->launches);
-      if (rc != DS_OK) { ctx->err = g_last_error; return rc; }
+      if (rc != DS_OK) {
+        ctx->err = g_last_error.empty() ? std::string("update launch: ") + cudaGetErrorString(cudaGetLastError())
+                                        : g_last_error;
+        return rc;
+      }
       if (ctx->la_ext) {
         // caller-driven lookahead: it stages / broadcasts a_{i+1,i+1} and launches
         // the multipliers (ds_lookahead_pivot, ds_lookahead_mult) on the lookahead
@@ -1666,9 +1828,16 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
         cudaStream_t ss = ctx->side;
         CK(cudaEventRecord(ctx->ev_upd, s));
         CK(cudaStreamWaitEvent(ss, ctx->ev_upd, 0));
+        int cw_words = 0;
+        const int cw_wpb = cw_plan(ctx, &cw_words);
         KArgs ke = ks;
-        const size_t sm = cx_smem_launch(ctx, &ke, 2 * (int64_t)m);
-        if (ke.sm_threads) {
+        const size_t sm = cw_wpb >= 1 ? 0 : cx_smem_launch(ctx, &ke, 2 * (int64_t)m);
+        if (cw_wpb >= 1) {  // one warp per (entry, component)
+          const unsigned nb = (unsigned)((2 * (int64_t)m + cw_wpb - 1) / cw_wpb);
+          const size_t smw = (size_t)cw_wpb * cw_words * 4;
+          k_cw_emit_signed<<<nb, 32 * cw_wpb, smw, ss>>>(ks, i, cw_words);
+          k_cw_emit_norm<<<nb, 32 * cw_wpb, smw, ss>>>(ks, i, cw_words);
+        } else if (ke.sm_threads) {
           const unsigned nb = (unsigned)((2 * (int64_t)m + ke.sm_threads - 1) / ke.sm_threads);
           k_emit_signed_c2<<<nb, ke.sm_threads, sm, ss>>>(ke, i);
           k_emit_norm_c2<<<nb, ke.sm_threads, sm, ss>>>(ke, i);
