@@ -79,8 +79,10 @@ def parse():
                     help="use the torch.distributed (NCCL) step loop even at world size 1 (testing)")
     ap.add_argument("--gen-budget", type=float, default=420.0,
                     help="max seconds of host time to build the Artless input before falling back to random")
-    ap.add_argument("--family", default="beta", choices=["beta", "random"],
-                    help="beta: Artless-method beta matrix (genmat.beta_matrix, Eq. 9); random: random_uniform")
+    ap.add_argument("--family", default="beta", choices=["beta", "random", "power"],
+                    help="beta: Artless-method beta matrix (genmat.beta_matrix, Eq. 9); random: random_uniform; "
+                         "power: the complex Artless zero-power matrix (genmat.power_matrix, M = ceil((N-1)/2), "
+                         "leading N x N block as the reference CLI's --limit-n)")
     return ap.parse_args()
 
 
@@ -125,6 +127,23 @@ def build_input(args, pinned: bool, rank: int = 0, world: int = 1, agree=None):
         print(f"[bench] beta matrix generation would take ~{est:.0f}s > --gen-budget {args.gen_budget:.0f}s "
               f"on this host: using random_uniform (same shape, same work)", file=sys.stderr)
         args.family = "random"
+    if args.family == "power":
+        from paper_1308_1536_b200 import hostgen
+        from paper_1308_1536_b200.soa import SoA
+        M = args.n // 2  # 2M + 1 >= n rows: the leading n x n block (prefix property, cli.py:296-302)
+        N = 2 * M + 1
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        threads = max(1, len(os.sched_getaffinity(0)) // local_world)
+        full = hostgen.power_matrix_soa(ZEROS, M, args.prec, nthreads=threads, row0=rank, rstep=world)
+        n, L = args.n, (args.prec + 31) // 32
+        rows_here = len(range(rank, n, world))
+        nrow_full = full.count // N
+        lim = full.limbs.reshape(2, L, nrow_full, N)[:, :, :rows_here, :n]
+        A = SoA(2, L, rows_here * n, pinned=pinned)
+        A.limbs[...] = lim.reshape(2, L, -1)
+        A.exp[...] = full.exp.reshape(2, nrow_full, N)[:, :rows_here, :n].reshape(2, -1)
+        A.cls[...] = full.cls.reshape(2, nrow_full, N)[:, :rows_here, :n].reshape(2, -1)
+        return A, workload_desc(args), time.perf_counter() - t0
     if args.family == "random":
         from paper_1308_1536_b200.synth import counter_uniform_soa, random_uniform_soa
         if world > 1:  # this rank's rows only (the counter-based draw is a function of (row, col))
@@ -138,7 +157,14 @@ def workload_desc(args) -> str:
     if args.family == "beta":
         return (f"Artless beta matrix a[n][j] = beta_n(gamma_j) (genmat.beta_matrix, Eq. 9), N={args.n} "
                 f"@{args.prec}b, zeros data/zeta_zeros_4096.txt")
+    if args.family == "power":
+        return (f"Artless zero-power matrix (genmat.power_matrix, complex, M={args.n // 2}, t=25), leading "
+                f"N={args.n} block @{args.prec}b, zeros data/zeta_zeros_4096.txt (SURVEY 8d config 3)")
     return f"N={args.n} random_uniform real matrix @{args.prec}b (SURVEY 8d config 3')"
+
+
+def kind_of(args) -> str:
+    return "complex" if args.family == "power" else "real"
 
 
 def work_limb_macs(n: int, L: int, complex_: bool = False) -> float:
@@ -149,7 +175,7 @@ def workload(args, desc: str = "") -> dict:
     return {"workload": f"{desc}: all leading minors + last-column signed/normalized minors for every size "
                         f"(BASELINE config 3)",
             "family": args.family,
-            "n": args.n, "prec_bits": args.prec, "limbs": (args.prec + 31) // 32, "kind": "real",
+            "n": args.n, "prec_bits": args.prec, "limbs": (args.prec + 31) // 32, "kind": kind_of(args),
             "collect_minors": True, "series": True,
             "l2": "inputs larger than L2 (matrix %.1f GB)" % (args.n * args.n * (4 * ((args.prec + 31) // 32) + 5) / 1e9)}
 
@@ -209,7 +235,7 @@ class _Soa:
         self.limbs, self.exp, self.cls, self.count = limbs, exp, cls, limbs.shape[2]
 
 
-def cpu_sample(n: int, p: int, rows: int, seed: int = 2000):
+def cpu_sample(n: int, p: int, rows: int, seed: int = 2000, ncomp: int = 1):
     """Pivot row + `rows` full-width rows at p bits in the ds SoA layout, drawn with
     numpy from the random_uniform family's distribution (genmat.py:242-246: sign
     uniform, |x| = U with a full p-bit mantissa).  MPFR's mul/sub cost at fixed p
@@ -220,19 +246,19 @@ def cpu_sample(n: int, p: int, rows: int, seed: int = 2000):
     rng = np.random.default_rng(seed)
     out = []
     for count in (n, rows * n):
-        limbs = rng.integers(0, 2 ** 32, size=(1, L, count), dtype=np.uint32)
+        limbs = rng.integers(0, 2 ** 32, size=(ncomp, L, count), dtype=np.uint32)
         zb = 32 * L - p
         if zb:
-            limbs[0, zb // 32] &= np.uint32((0xFFFFFFFF << (zb % 32)) & 0xFFFFFFFF)
-            limbs[0, :zb // 32] = 0
-        limbs[0, L - 1] |= np.uint32(0x80000000)
-        exp = (1 - rng.geometric(0.5, size=(1, count))).astype(np.int32)
-        cls = rng.integers(0, 2, size=(1, count)).astype(np.uint8)
+            limbs[:, zb // 32] &= np.uint32((0xFFFFFFFF << (zb % 32)) & 0xFFFFFFFF)
+            limbs[:, :zb // 32] = 0
+        limbs[:, L - 1] |= np.uint32(0x80000000)
+        exp = (1 - rng.geometric(0.5, size=(ncomp, count))).astype(np.int32)
+        cls = rng.integers(0, 2, size=(ncomp, count)).astype(np.uint8)
         out.append(_Soa(np.ascontiguousarray(limbs), np.ascontiguousarray(exp), np.ascontiguousarray(cls)))
     return out
 
 
-def cpu_reference(n: int, p: int, seconds: float):
+def cpu_reference(n: int, p: int, seconds: float, kind: str = "real"):
     """Time the reference hot loop (oracle = elim.py:37-53 restated over MPFR) on a
     bounded sample of the workload: pivot step i applied to `rows` full-width rows,
     i = 0, 1, ... until ~`seconds` of timed MPFR work; all host threads."""
@@ -241,21 +267,22 @@ def cpu_reference(n: int, p: int, seconds: float):
     L = (p + 31) // 32
     threads = len(os.sched_getaffinity(0))
     rows_per_call = min(max(threads * 4, 64), n - 1)
-    prow, rows = cpu_sample(n, p, rows_per_call)
+    cx = kind == "complex"
+    prow, rows = cpu_sample(n, p, rows_per_call, ncomp=2 if cx else 1)
     total_t, total_macs, calls, i = 0.0, 0.0, 0, 0
     while total_t < seconds and i < n - 1:
         # step i touches all n-1 columns of every sampled row (L and U slots)
-        dt = oracle.time_apply_pivot_rows(n, p, "real", i, prow, rows, rows_per_call, threads, True)
+        dt = oracle.time_apply_pivot_rows(n, p, kind, i, prow, rows, rows_per_call, threads, True)
         total_t += dt
         total_macs += rows_per_call * (n - 1)
         calls += 1
         i += 1
-    rate = total_macs * L * L / total_t
+    rate = total_macs * L * L * (4 if cx else 1) / total_t
     return {"value": rate, "unit": "limb-MAC/s", "cores": threads, "kind": "port",
-            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}, p={p}, random_uniform "
-                      f"distribution, numpy seed 2000), elim.py:37-53 restated over MPFR 4.2.1 "
+            "sample": f"{calls} pivot steps x {rows_per_call} full-width rows (n={n}, p={p}, {kind}, random_uniform "
+                      f"distribution, numpy seed 2000), elim.py:37-53 restated over MPFR 4.2.1 / MPC 1.3.1 "
                       f"(oracle/ds_oracle.c), {total_macs:.3g} element MACs in {total_t:.2f}s on {threads} threads",
-            "seconds_to_all_minors_extrapolated": work_limb_macs(n, L) / rate}
+            "seconds_to_all_minors_extrapolated": work_limb_macs(n, L, cx) / rate}
 
 
 def run_reference(args):
@@ -269,11 +296,11 @@ def run_reference(args):
     per = max(2.0, min(args.cpu_seconds, 24.0 / max(1, args.steps + args.warmup)))
     desc = workload_desc(args)
     for _ in range(args.warmup):
-        cpu_reference(args.n, args.prec, per / 4)
+        cpu_reference(args.n, args.prec, per / 4, kind_of(args))
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference(args.n, args.prec, per))
+        vals.append(cpu_reference(args.n, args.prec, per, kind_of(args)))
     wall = time.perf_counter() - t0
     rate = sum(v["value"] for v in vals) / len(vals)
     base = vals[-1]
@@ -285,7 +312,7 @@ def run_reference(args):
            "data": "synthetic (random_uniform sample rows; MPFR cost is value-independent at fixed p)",
            "impl": "reference",
            "config": workload(args, desc),
-           "seconds_to_all_minors": work_limb_macs(args.n, L) / rate,
+           "seconds_to_all_minors": work_limb_macs(args.n, L, kind_of(args) == "complex") / rate,
            "cpu_baseline": {"value": rate, "unit": "limb-MAC/s", "cores": base["cores"], "kind": "port",
                             "sample": base["sample"]},
            "e2e": {"value": rate, "unit": "limb-MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -330,12 +357,13 @@ def parity_leg(args, A, res, final, eng_factory):
     head = 4 if p > 8192 else 8
     with eng_factory() as e2:
         e2.load(A)
-        rh = HostResults.alloc(n, 1, e2.L, False)
+        rh = HostResults.alloc(n, e2.ncomp, e2.L, False)
         e2.run(True, True, 0, head, rh)
         fh = A.copy()
         e2.fetch(fh)
-    out["leading_steps"] = pc.leading_steps(A, n, p, "real", head, fh, rh)
-    out["prefix"] = pc.prefix(A, n, p, "real", min(args.parity_m, n), res, final)
+    kind = kind_of(args)
+    out["leading_steps"] = pc.leading_steps(A, n, p, kind, head, fh, rh)
+    out["prefix"] = pc.prefix(A, n, p, kind, min(args.parity_m, n), res, final)
     sizes = sorted({n, n - 1, max(2, n // 2)})
     out["laplace"] = pc.laplace(A, n, p, res, sizes)
     out["ok"] = bool(out["leading_steps"]["ok"] and out["prefix"]["ok"])
@@ -377,7 +405,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
     A, desc, gen_s = build_input(args, pinned=True, rank=rank, world=world, agree=agree)  # this rank's rows
-    eng = DeviceElimination(n, p, "real", local, rank, world)
+    kind = kind_of(args)
+    nc = 2 if kind == "complex" else 1
+    eng = DeviceElimination(n, p, kind, local, rank, world)
     # a dedicated stream (the legacy default stream's handle 0 would mean "own stream" to
     # ds_set_stream): kernels, NCCL broadcasts and the timing events share its order
     stream = torch.cuda.Stream()
@@ -407,11 +437,11 @@ def main():
     eng.lib.ds_set_stream(eng.ctx, stream.cuda_stream)
     # host buffers of this rank only: owned rows (count nloc * n) when sharded
     nloc = (n - rank + world - 1) // world
-    res = HostResults.alloc(n, 1, L, True, pinned=True)
+    res = HostResults.alloc(n, nc, L, True, pinned=True)
     if world > 1:
-        res = HostResults(SoA(1, L, n, pinned=True), SoA(1, L, n, pinned=True), SoA(1, L, nloc * n, pinned=True),
-                          SoA(1, L, nloc * n, pinned=True), res.row_flags)
-    final = SoA(1, L, nloc * n, pinned=True)
+        res = HostResults(SoA(nc, L, n, pinned=True), SoA(nc, L, n, pinned=True), SoA(nc, L, nloc * n, pinned=True),
+                          SoA(nc, L, nloc * n, pinned=True), res.row_flags)
+    final = SoA(nc, L, nloc * n, pinned=True)
 
     def one_pass(resident: bool):
         if resident:
@@ -471,7 +501,7 @@ def main():
     upd_ms, upd_launches, upd_work = eng.profile_read()
     eng.profile(False)
     gpu_launches = eng.launches() - launches0
-    total_work = work_limb_macs(n, L)
+    total_work = work_limb_macs(n, L, kind == "complex")
     value = total_work / (ms / 1e3)
     # ---- timed: end to end through the C ABI with host buffers (pinned): H2D of the
     # matrix, the elimination, D2H of trace + minors (progressive) + final matrix
@@ -496,20 +526,23 @@ def main():
                "includes": "H2D matrix, elimination, D2H pivots/dets/signed+normalized minors/final L\\U matrix"}
     # ---- roofline of the dominant kernel: the update (tensor-core engine)
     # algorithmic bytes per updated element: read + write a_jk (L limbs + exp + cls)
-    elems = upd_work / (L * L) if L else 0.0
+    cxw = 4 if kind == "complex" else 1  # component products per element
+    elems = upd_work / (L * L * cxw) if L else 0.0
     upd_s = upd_ms / 1e3
-    bytes_alg = elems * 2 * (4 * L + 5)
+    bytes_alg = elems * 2 * nc * (4 * L + 5)
     hbm_peak, peak_src = measured_hbm_peak()
     achieved_gbs = bytes_alg / upd_s / 1e9 if upd_s > 0 else 0.0
     counters = eng.counters()
-    engine_name = ("k_update_tc (ds_tc.cu): tcgen05.mma kind::i8 digit products in TMEM + rounding epilogue"
+    engine_name = ("k_prod_tcw x4 + k_tcw_finish_c (ds_tc.cu): complex component products on tcgen05 kind::i8 + "
+                   "exact two-product sums and rounding" if kind == "complex" else
+                   "k_update_tc (ds_tc.cu): tcgen05.mma kind::i8 digit products in TMEM + rounding epilogue"
                    if counters.get("tc_engine") else "k_fused (ds_update.cu): FP64 digit products + rounding epilogue")
-    prof = committed_profile(n, p)
+    prof = committed_profile(n, p) if kind == "real" else None
     roof = {"kernel": engine_name, "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved_gbs / hbm_peak if hbm_peak else None,
             "traffic": (prof["dram_bytes_per_element"] * elems / upd_launches) if prof and upd_launches else None,
             "traffic_per_element": prof.get("dram_bytes_per_element") if prof else None,
-            "algorithmic_bytes_per_element": 2 * (4 * L + 5),
+            "algorithmic_bytes_per_element": 2 * nc * (4 * L + 5),
             "elements_per_step": elems / args.steps if args.steps else None,
             "share_of_step": (upd_ms / args.steps) / ms if ms > 0 else None,
             "launches_per_step": upd_launches / args.steps,
@@ -526,7 +559,7 @@ def main():
     parity = None
     if world == 1 and not args.no_parity and not args.no_e2e:
         try:
-            parity = parity_leg(args, A, res, final, lambda: DeviceElimination(n, p, "real", local))
+            parity = parity_leg(args, A, res, final, lambda: DeviceElimination(n, p, kind, local))
         except Exception as exc:  # reported, never hidden
             parity = {"ok": False, "error": repr(exc)}
     out = None
@@ -534,14 +567,15 @@ def main():
         cpu = None
         if not args.no_cpu and world == 1:  # rank 0 at N=1 only
             try:
-                cpu = cpu_reference(n, p, args.cpu_seconds)
+                cpu = cpu_reference(n, p, args.cpu_seconds, kind)
             except Exception as exc:  # never fail the GPU line on the baseline
                 cpu = {"error": repr(exc)}
         out = {"metric": f"limb-MAC/s (schoolbook 32x32 limb products) of the all-minors elimination, N={n} @{p}b",
                "value": value, "unit": "limb-MAC/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "u8 digit products (tcgen05 kind::i8, s32 accumulate) + u32 limbs",
-               "data": "synthetic" if args.family == "random" else "Artless beta matrix from data/ zeta zeros",
+               "data": {"random": "synthetic", "beta": "Artless beta matrix from data/ zeta zeros",
+                        "power": "Artless zero-power matrix (complex) from data/ zeta zeros"}[args.family],
                "config": workload(args, desc), "seconds_to_all_minors": ms / 1e3,
                "input_generation_s": gen_s,
                "e2e": e2e, "roofline": roof, "parity": parity, "cpu_baseline": cpu, "gpu_launches": gpu_launches,

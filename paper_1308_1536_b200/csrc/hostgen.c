@@ -280,3 +280,83 @@ int dsh_beta_matrix_cols(int N, long p, const char **zeros, int guard_bits, int 
   }
   return failed ? -1 : 0;
 }
+
+
+/* ---- the Artless zero-power matrix (reference genmat.py:193-223) ----------
+ * (2M+1) x (2M+1) complex; row 1 = 1; row n >= 2 holds, at the work precision
+ * w = p + guard (genmat power_matrix):
+ *     ln_n = log(mpfr(n)),  r = exp(-ln_n / 2),
+ *     for m < M: theta = gamma_m * ln_n, c = r*cos(theta), s = r*sin(theta),
+ *                entries (c, s), (c, -s);
+ *     last: theta_t = mpfr(t) * ln_n, entry (r*cos(theta_t), -r*sin(theta_t)),
+ * each op correctly rounded at w (cos and sin from mpfr_sin_cos, which rounds
+ * both exactly as mpfr_cos / mpfr_sin do), then every component rounded to p
+ * (mpc(x) in the p context).  gamma_m are the zeros file's tokens rounded at
+ * zero_prec (load_zeros' precision) and t the token t_str at t_prec, as the
+ * reference's callers pass them.  Rows row0, row0 + rstep, ... only, into a full
+ * (count N*N) or owned-rows (count nloc*N) complex SoA. */
+int dsh_power_matrix(int M, long p, const char **zeros, long zero_prec, const char *t_str, long t_prec,
+                     int guard_bits, int nthreads, ds_soa *out, int row0, int rstep) {
+  const int N = 2 * M + 1;
+  const long work = p + guard_bits;
+  const int L = (int)((p + 31) / 32);
+  const int full = out->count == (int64_t)N * N;
+  mpfr_t *g = (mpfr_t *)malloc(sizeof(mpfr_t) * (M > 0 ? M : 1));
+  mpfr_t t;
+  for (int m = 0; m < M; m++) {
+    mpfr_init2(g[m], zero_prec);
+    mpfr_set_str(g[m], zeros[m], 10, RN);
+  }
+  mpfr_init2(t, t_prec);
+  mpfr_set_str(t, t_str, 10, RN);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : omp_get_max_threads())
+  for (int n = 1 + row0; n <= N; n += rstep) {
+    const int64_t ridx = full ? (int64_t)(n - 1) : (int64_t)((n - 1 - row0) / rstep);
+    mpfr_t lnn, r, th, c, sn, cc, ss, tw, o;
+    mpfr_inits2(work, lnn, r, th, c, sn, cc, ss, tw, (mpfr_ptr)0);
+    mpfr_init2(o, p);
+    if (n == 1) {
+      for (int j = 0; j < N; j++) {
+        mpfr_set_ui(o, 1, RN);
+        dsh_put_soa(out, 0, ridx * N + j, o, L);
+        mpfr_set_ui(o, 0, RN);
+        dsh_put_soa(out, 1, ridx * N + j, o, L);
+      }
+    } else {
+      mpfr_set_ui(lnn, (unsigned long)n, RN);
+      mpfr_log(lnn, lnn, RN);                      /* ln_n = log(mpfr(n)) */
+      mpfr_neg(r, lnn, RN);
+      mpfr_div_2ui(r, r, 1, RN);                   /* -ln_n / 2 (exact) */
+      mpfr_exp(r, r, RN);                          /* r */
+      for (int m = 0; m < M; m++) {
+        mpfr_mul(th, g[m], lnn, RN);               /* theta = gamma_m * ln_n */
+        mpfr_sin_cos(sn, cc, th, RN);
+        mpfr_mul(c, r, cc, RN);                    /* r * cos(theta) */
+        mpfr_mul(ss, r, sn, RN);                   /* r * sin(theta) */
+        const int64_t e0 = ridx * N + 2 * m;
+        mpfr_set(o, c, RN);
+        dsh_put_soa(out, 0, e0, o, L);
+        dsh_put_soa(out, 0, e0 + 1, o, L);
+        mpfr_set(o, ss, RN);
+        dsh_put_soa(out, 1, e0, o, L);
+        mpfr_neg(o, o, RN);                        /* mpc(c, -s): -RN(s) = RN(-s) */
+        dsh_put_soa(out, 1, e0 + 1, o, L);
+      }
+      mpfr_set(tw, t, RN);                         /* mpfr(t) at work */
+      mpfr_mul(th, tw, lnn, RN);                   /* theta_t */
+      mpfr_sin_cos(sn, cc, th, RN);
+      mpfr_mul(c, r, cc, RN);
+      mpfr_mul(ss, r, sn, RN);
+      mpfr_neg(ss, ss, RN);                        /* -r * sin(theta_t) */
+      mpfr_set(o, c, RN);
+      dsh_put_soa(out, 0, ridx * N + 2 * M, o, L);
+      mpfr_set(o, ss, RN);
+      dsh_put_soa(out, 1, ridx * N + 2 * M, o, L);
+    }
+    mpfr_clears(lnn, r, th, c, sn, cc, ss, tw, o, (mpfr_ptr)0);
+  }
+  for (int m = 0; m < M; m++) mpfr_clear(g[m]);
+  free(g);
+  mpfr_clear(t);
+  return 0;
+}

@@ -42,6 +42,8 @@ int mpfr_neg(mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_sqrt(mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_exp(mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_log(mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
+int mpfr_sin_cos(mpfr_ptr, mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
+int mpfr_div_2ui(mpfr_ptr, mpfr_srcptr, unsigned long, mpfr_rnd_t);
 int mpfr_log2(mpfr_ptr, mpfr_srcptr, mpfr_rnd_t);
 int mpfr_const_pi(mpfr_ptr, mpfr_rnd_t);
 int mpfr_fac_ui(mpfr_ptr, unsigned long, mpfr_rnd_t);

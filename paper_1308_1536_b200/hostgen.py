@@ -35,6 +35,10 @@ def _load():
         L.dsh_beta_gammas.restype = ctypes.c_int
         L.dsh_beta_gammas.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(ds_soa)]
+        L.dsh_power_matrix.restype = ctypes.c_int
+        L.dsh_power_matrix.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.POINTER(ctypes.c_char_p), ctypes.c_long,
+                                       ctypes.c_char_p, ctypes.c_long, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(ds_soa), ctypes.c_int, ctypes.c_int]
         L.dsh_mpfr_structs.restype = ctypes.c_int
         L.dsh_mpfr_structs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int64, ctypes.c_int, ctypes.c_long]
@@ -129,3 +133,24 @@ class BetaBuilder:
             from .errors import GammaEvaluationFailed
             raise GammaEvaluationFailed("Spouge Gamma did not stabilise")
         self.done = j1
+
+
+def power_matrix_soa(zeros_path: str, M: int, prec_bits: int, t: str = "25", zero_prec: int = 2048,
+                     t_prec: int = 2048, guard_bits: int = 32, nthreads: int = 0, pinned: bool = False,
+                     row0: int = 0, rstep: int = 1) -> SoA:
+    """genmat.power_matrix(load_zeros(zeros_path, Precision(zero_prec), M), M, mpfr(t) at t_prec,
+    Precision(prec_bits), guard_bits) -- the (2M+1) x (2M+1) complex Artless zero-power matrix
+    (reference genmat.py:193-223) -- bit for bit, in multi-threaded C (csrc/hostgen.c
+    dsh_power_matrix).  rstep > 1: only rows row0, row0 + rstep, ... (owned-rows layout)."""
+    lib = _load()
+    toks = read_zero_tokens(zeros_path, M)
+    arr = (ctypes.c_char_p * max(M, 1))(*[t_.encode() for t_ in toks])
+    N = 2 * M + 1
+    nloc = (N - row0 + rstep - 1) // rstep if rstep > 1 else N
+    out = SoA(2, (prec_bits + 31) // 32, nloc * N, pinned=pinned)
+    c = out.c()
+    rc = lib.dsh_power_matrix(M, prec_bits, arr, zero_prec, str(t).encode(), t_prec, guard_bits, nthreads,
+                              ctypes.byref(c), row0, rstep)
+    if rc != 0:
+        raise RuntimeError("power matrix builder failed")
+    return out

@@ -153,3 +153,14 @@ def test_bench_two_ranks_one_gpu_gloo():
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def test_bench_power_family_small():
+    """bench.py on the complex Artless power family (leading N x N block of genmat.power_matrix), with
+    the parity leg checking the run against the oracle."""
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "1", "--dim", "64", "--bits", "1024",
+                        "--family", "power", "--cpu-seconds", "1", "--parity-m", "32"], timeout=900, cwd=ROOT,
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["config"]["kind"] == "complex" and d["parity"]["ok"], d["parity"]

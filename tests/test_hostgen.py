@@ -45,3 +45,28 @@ def test_gamma_cache_columns():
     a = hostgen.beta_matrix_soa(ZEROS, 3, 4096)
     b = hostgen.beta_matrix_soa(ZEROS, 3, 4096, gammas=cache)
     assert np.array_equal(a.limbs, b.limbs) and np.array_equal(a.exp, b.exp) and np.array_equal(a.cls, b.cls)
+
+
+@pytest.mark.parametrize("M,p", [(8, 256), (5, 1000), (3, 4096)])
+def test_power_matrix_c_builder_bit_identical(M, p):
+    """hostgen.power_matrix_soa (multi-threaded C) reproduces genmat.power_matrix (the reference's
+    genmat.py:193-223 op sequence) bit for bit, at the zeros/t precision the goldens use."""
+    from paper_1308_1536_b200 import genmat, mp
+    from paper_1308_1536_b200.hostgen import power_matrix_soa
+    from paper_1308_1536_b200.scalars import Precision, canonical_bits
+    z = genmat.load_zeros(REF_ZEROS, Precision(2048), M)
+    with mp.context(precision=2048):
+        t = mp.mpfr(25)
+    A = genmat.power_matrix(z, M, t, Precision(p))
+    S = power_matrix_soa(REF_ZEROS, M, p)
+    N = 2 * M + 1
+    for i in range(N):
+        for j in range(N):
+            assert canonical_bits(S.get(i * N + j, p)) == canonical_bits(A.rows[i][j]), (i, j)
+    # owned rows of a 3-rank split
+    for r in range(3):
+        part = power_matrix_soa(REF_ZEROS, M, p, row0=r, rstep=3)
+        rows = list(range(r, N, 3))
+        for jl, i in enumerate(rows):
+            for j in range(0, N, 3):
+                assert canonical_bits(part.get(jl * N + j, p)) == canonical_bits(A.rows[i][j])
