@@ -28,7 +28,7 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // largest divisor block (limbs per lane) of the warp division; wider exact
 // denominators (huge exponent gaps, or p > ~8000 bits) take the lane-0 path
-constexpr int KMAX = 16;
+constexpr int KMAX = 40;
 
 // U of the warp division: nU <= nD + L + 4 limbs, zero-filled up to nU + 32 K
 __host__ __device__ inline int64_t u_words(int L, int p) {
@@ -237,6 +237,8 @@ __device__ bool wcdiv_part(Ptr rm, int32_t* re, uint8_t* rc, const Val& ar, cons
   if (K <= 4) return wdiv_body<4>(rm, re, rc, xn, xd, nD, L, p, R, warn);
   if (K <= 8) return wdiv_body<8>(rm, re, rc, xn, xd, nD, L, p, R, warn);
   if (K <= 12) return wdiv_body<12>(rm, re, rc, xn, xd, nD, L, p, R, warn);
+  if (K <= 16) return wdiv_body<16>(rm, re, rc, xn, xd, nD, L, p, R, warn);
+  if (K <= 24) return wdiv_body<24>(rm, re, rc, xn, xd, nD, L, p, R, warn);
   if (K <= KMAX) return wdiv_body<KMAX>(rm, re, rc, xn, xd, nD, L, p, R, warn);
   // very wide denominator (exponent gap near the window): the thread-level division
   bool ok = true;

@@ -1250,9 +1250,13 @@ __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int ro
   const int L = a.L, p = a.p;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)w.nrows * a.ncols;
-  const int RW = (8 * L + 32 + 7) & ~7;
-  uint32_t* row = scratch + tid * (int64_t)RW;
-  const ds::Ptr Ssum{row, 1}, Tre{row + 4 * L + 16, 1}, Tim{row + 5 * L + 16, 1}, tmp{row + 6 * L + 16, 1};
+  // per-thread scratch interleaved across the grid (word k of thread t at k * T + t):
+  // the generic limb loops below touch the same word index in every lane, so each
+  // warp access is one coalesced line instead of 32 (and the rows stay in L2)
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  uint32_t* row = scratch + tid;
+  const ds::Ptr Ssum{row, T}, Tre{row + (4 * (int64_t)L + 16) * T, T}, Tim{row + (5 * (int64_t)L + 16) * T, T},
+      tmp{row + (6 * (int64_t)L + 16) * T, T};
   const int64_t region = w.pstride * (int64_t)w.W;  // words per product region (c1, c2)
   for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
@@ -1288,7 +1292,7 @@ __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int ro
       if (x.zero) {
         ok = X.zero && Y.zero;  // a truncated nonzero sum that cancels: undecided
       } else {
-        const int64_t H = x.base + ds::top_bit(ds::CPtr{Ssum.p, 1}, x.n);
+        const int64_t H = x.base + ds::top_bit(ds::CPtr{Ssum.p, Ssum.s}, x.n);
         const int64_t R = H - p + 1;  // weight of the result's LSB
         int64_t bnd = INT64_MIN;
         int64_t tmin = INT64_MAX;
@@ -1306,7 +1310,7 @@ __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int ro
           ok = false;
         } else {
           bool ones, zeros;
-          bit_range(ds::CPtr{Ssum.p, 1}, x.n, max((int64_t)0, bnd - x.base), R - 1 - x.base, &ones, &zeros);
+          bit_range(ds::CPtr{Ssum.p, Ssum.s}, x.n, max((int64_t)0, bnd - x.base), R - 1 - x.base, &ones, &zeros);
           ok = !ones && !zeros;
         }
       }
@@ -1325,7 +1329,7 @@ __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int ro
       const int64_t off = (int64_t)c * L * a.a_count + idx;
       const int64_t mo = (int64_t)c * a.a_count + idx;
       ds::Val av{ds::CPtr{a.a_limbs + off, a.a_count}, a.a_exp[mo], a.a_cls[mo]};
-      ds::Val tv{ds::CPtr{(c == 0 ? Tre : Tim).p, 1}, te[c], tcl[c]};
+      ds::Val tv{ds::CPtr{(c == 0 ? Tre : Tim).p, T}, te[c], tcl[c]};
       int32_t re;
       uint8_t rc;
       if (!ds::add_rn(ds::Ptr{a.a_limbs + off, a.a_count}, &re, &rc, av, tv, true, L, p, tmp))

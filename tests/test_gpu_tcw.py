@@ -99,7 +99,7 @@ from paper_1308_1536_b200.soa import SoA  # noqa: E402
 
 
 @pytest.mark.parametrize("n,p,special", [(24, 256, True), (30, 1024, False), (20, 2000, True), (14, 4096, True),
-                                          (12, 300, False)])
+                                          (12, 300, False), (10, 8192, True), (8, 16384, False)])
 def test_wide_complex_full_elimination_matches_oracle(n, p, special):
     A = _random_matrix(n, p, 77 * n + p, "complex", special)
     rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
@@ -197,3 +197,20 @@ def test_complex_zero_pivot_after_first_step(n, p, bad):
     assert done_d == bad
     assert results_digest(res_o, fin_o, n, p, done_o) == results_digest(res_d, fin_d, n, p, done_d)
     assert res_d.row_flags[bad] & 1  # size bad+1 emitted
+
+
+@pytest.mark.parametrize("p", [1024, 4096])
+def test_complex_warp_and_thread_engines_agree(p):
+    """The warp-cooperative complex kernels (ds_cwarp.cuh) and the thread-level ones (DS_CX_THREAD=1)
+    give the same bits on an exponent-spread complex matrix (wide exact sums, perturbations)."""
+    import os
+    n = 40
+    A = _random_matrix(n, p, 5 * n + p, "complex", True)
+    rc_w, done_w, res_w, fin_w = device_eliminate(A, n, p, "complex")
+    os.environ["DS_CX_THREAD"] = "1"
+    try:
+        rc_t, done_t, res_t, fin_t = device_eliminate(A, n, p, "complex")
+    finally:
+        os.environ.pop("DS_CX_THREAD", None)
+    assert done_w == done_t
+    assert results_digest(res_w, fin_w, n, p, done_w) == results_digest(res_t, fin_t, n, p, done_t)
