@@ -96,6 +96,19 @@ int ds_create(ds_ctx **out, int n, long prec_bits, int kind, int device, int ran
               int world);
 void ds_destroy(ds_ctx *ctx);
 
+/* Row-block context for the panel-paged executor (out-of-core, SURVEY 8(f)
+ * rank 4; the reference's blockpager.py:224-241 / 505-529 role): it holds the
+ * consecutive rows [row0, row0 + nrows) of an n x n matrix at full width.
+ * Steps i < row0 take their (final) pivot row from the host (ds_pivot_load);
+ * steps row0 <= i < row0 + nrows stage it from the block (ds_pivot_stage).
+ * Every element sees the in-core op sequence, so results are bit-identical
+ * (the prefix / left-looking order of elim.py:203-218).  ds_load / ds_fetch /
+ * ds_results_fetch take the block's rows (count nrows*n) or the full matrix. */
+int ds_create_block(ds_ctx **out, int n, long prec_bits, int kind, int device, int row0, int nrows);
+/* Copy a final pivot row (host SoA of count n) into the pivot buffer for step
+ * `step` (elim.py:216-218 with prow = rows[step]), instead of ds_pivot_stage. */
+int ds_pivot_load(ds_ctx *ctx, int step, const ds_soa *row);
+
 /* Copy the rows this rank owns into HBM.  The host matrix is either the full
  * n x n matrix (count = n*n; global row r at idx r*n + col) or only this
  * rank's rows (count = nloc*n with nloc = #{r < n : r % world == rank}; local

@@ -28,7 +28,7 @@ EXPORTS = ("ds_version", "ds_create", "ds_destroy", "ds_load", "ds_fetch", "ds_r
            "ds_pivot_copy", "ds_snapshot", "ds_profile", "ds_profile_read", "ds_counters", "ds_lookahead_enable", "ds_lookahead_stream",
            "ds_lookahead_pivot", "ds_lookahead_mult", "ds_set_pivot_mode", "ds_swaps_fetch",
            "ds_results_fetch_range", "ds_generate", "ds_stream_minors", "ds_stream_flush",
-           "ds_update_rows")
+           "ds_update_rows", "ds_create_block", "ds_pivot_load")
 
 
 class ds_results(ctypes.Structure):
@@ -65,6 +65,8 @@ def load_library(path: str = LIB_PATH):
         "ds_stream_minors": (I, [VP, I, VP, VP]),
         "ds_stream_flush": (I, [VP, I, I]),
         "ds_update_rows": (I, [VP, P(ds_soa)]),
+        "ds_create_block": (I, [P(VP), I, ctypes.c_long, I, I, I, I]),
+        "ds_pivot_load": (I, [VP, I, P(ds_soa)]),
         "ds_set_det": (I, [VP, S]),
         "ds_stream": (VP, [VP]),
         "ds_launch_count": (ctypes.c_int64, [VP]),

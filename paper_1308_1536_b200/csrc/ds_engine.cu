@@ -33,6 +33,10 @@ using namespace ds;
 
 struct ds_ctx {
   int n, L, p, kind, ncomp, device, rank, world, nloc;
+  // this context holds the rows row_base + rank + jl*world, jl < nloc: the
+  // row-cyclic shard of a rank (row_base 0), or a block of consecutive rows
+  // (world 1) of the panel-paged executor (ds_create_block)
+  int row_base;
   cudaStream_t stream, own_stream;
   cudaStream_t side;           // det chain + minors emission (outputs only, may lag)
   cudaEvent_t ev, ev_piv, ev_upd;
@@ -216,7 +220,7 @@ __device__ bool g_add(Out o0, Out o1, Val a0, Val a1, Val b0, Val b1, int kind, 
 
 // ---------------------------------------------------------------- kernels
 struct KArgs {
-  int n, L, p, kind, ncomp, rank, world, nloc;
+  int n, L, p, kind, ncomp, rank, world, nloc, row_base;
   uint32_t* a_limbs; int32_t* a_exp; uint8_t* a_cls; int64_t a_count;
   uint8_t* pbuf;
   uint32_t* z_limbs; int32_t* z_exp; uint8_t* z_cls;
@@ -236,7 +240,7 @@ struct KArgs {
 static KArgs kargs(ds_ctx* c) {
   KArgs k;
   k.n = c->n; k.L = c->L; k.p = c->p; k.kind = c->kind; k.ncomp = c->ncomp; k.rank = c->rank;
-  k.world = c->world; k.nloc = c->nloc;
+  k.world = c->world; k.nloc = c->nloc; k.row_base = c->row_base;
   k.a_limbs = c->a_limbs; k.a_exp = c->a_exp; k.a_cls = c->a_cls; k.a_count = c->a_count;
   k.pbuf = c->pbuf;
   k.z_limbs = c->z_limbs; k.z_exp = c->z_exp; k.z_cls = c->z_cls;
@@ -290,7 +294,7 @@ __device__ __forceinline__ Ptr thread_scratch(const KArgs& k, int64_t tid) {
 // limb plane, column), coalesced along the row
 __global__ void k_stage(KArgs k, int i) {
   if (k.status[0] >= 0) return;
-  int64_t jl = i / k.world;
+  int64_t jl = (i - k.row_base) / k.world;
   PB pb = pb_view(k.pbuf, k.n, k.L, k.ncomp);
   int64_t planes = (int64_t)k.ncomp * (k.L + 2);  // L limb planes + exp + cls per component
   int64_t tot = planes * k.n;
@@ -448,11 +452,17 @@ __global__ void k_det_step(KArgs k, int i, int from_cur) {
   if (!g_mul(d0, d1, q0, q1, p0, p1, k.kind, k.L, k.p, kscratch(k, 0))) atomicAdd(&k.status[2], 1);
 }
 
-// first local row index with global row > i
-__host__ __device__ static inline int first_local_after(int i, int rank, int world) {
-  int first = i + 1;
-  int k0 = (first - rank + world - 1) / world;
-  return k0 < 0 ? 0 : k0;
+// first local row index with global row > i (global = row_base + rank + jl*world)
+__host__ __device__ static inline int first_local_after(int i, int rank, int world, int row_base = 0) {
+  int first = i + 1 - row_base;
+  if (first <= rank) return 0;
+  return (first - rank + world - 1) / world;
+}
+
+// does this context hold global row g
+static inline bool owns_row(const ds_ctx* c, int g) {
+  const int r = g - c->row_base;
+  return r >= 0 && r % c->world == c->rank && r / c->world < c->nloc;
 }
 
 // z_j = RN(a_ji / piv), a_ji <- -z_j  (elim.py:47, 53)
@@ -526,7 +536,7 @@ __global__ void k_emit_signed_c2(KArgs k, int i) {
   // emits size i+2 before step i+1 raises)
   if (k.status[0] >= 0 && k.status[0] <= i) return;
   int m = i + 2;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   Val d0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);
   Val d1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 1, k.L, i);
@@ -551,7 +561,7 @@ __global__ void k_emit_signed_c2(KArgs k, int i) {
 __global__ void k_emit_norm_c2(KArgs k, int i) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;  // see k_emit_signed_c2
   int m = i + 2;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r0 = mrow(k, jl);
   Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
@@ -627,7 +637,7 @@ __global__ void k_cw_det(KArgs k, int i, int from_cur, int cw_words) {
 __global__ void k_cw_emit_signed(KArgs k, int i, int cw_words) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;  // see k_emit_signed_c2
   const int m = i + 2;
-  const int64_t jl = (i + 1) / k.world;
+  const int64_t jl = (i + 1 - k.row_base) / k.world;
   const int wpb = blockDim.x >> 5;
   const int64_t t = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
   if (t >= 2 * (int64_t)m) return;
@@ -661,7 +671,7 @@ __global__ void k_cw_emit_signed(KArgs k, int i, int cw_words) {
 __global__ void k_cw_emit_norm(KArgs k, int i, int cw_words) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;
   const int m = i + 2;
-  const int64_t jl = (i + 1) / k.world;
+  const int64_t jl = (i + 1 - k.row_base) / k.world;
   const int64_t r0 = mrow(k, jl);
   const Val l0r = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
   const Val l1r = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 1, k.L, r0);
@@ -745,7 +755,7 @@ __global__ void k_update_general(KArgs k, int i, int jl0, int collect_minors) {
 __global__ void k_emit_signed(KArgs k, int i) {
   if (k.status[0] >= 0) return;
   int m = i + 2;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   Val d0 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, 0, k.L, i);  // det_i (k_pivot / k_det_step)
   Val d1 = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, k.ncomp - 1, k.L, i);
@@ -770,7 +780,7 @@ __global__ void k_emit_signed(KArgs k, int i) {
 __global__ void k_emit_norm(KArgs k, int i) {
   if (k.status[0] >= 0) return;
   int m = i + 2;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r0 = mrow(k, jl);
   Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
@@ -910,7 +920,7 @@ __global__ void k_emit_norm_w(KArgs k, int i, int wwords) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;
   const int warp = threadIdx.x >> 5;
   int m = i + 2;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   const int64_t kk = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   const int64_t r0 = mrow(k, jl);
   Val l0 = val_at(k.sig_limbs, k.sig_exp, k.sig_cls, k.m_count, 0, k.L, r0);
@@ -957,7 +967,7 @@ __global__ void k_pivot_lite(KArgs k, int i, int first) {
 // sig_{m-1} = det_i (elim.py:60)
 __global__ void k_emit_last(KArgs k, int i) {
   if (k.status[0] >= 0 && k.status[0] <= i) return;
-  int64_t jl = (i + 1) / k.world;
+  int64_t jl = (i + 1 - k.row_base) / k.world;
   int64_t idx = mrow(k, jl) + (i + 1);
   for (int c = 0; c < k.ncomp; c++) {
     Val d = val_at(k.det_limbs, k.det_exp, k.det_cls, k.n, c, k.L, i);
@@ -1078,6 +1088,33 @@ int ds_pivot_copy(ds_ctx* dst, ds_ctx* src) {
 
 int64_t ds_launch_count(ds_ctx* ctx) { return ctx->launches; }
 
+static int ds_create_sized(ds_ctx** out, int n, long prec_bits, int kind, int device, int rank, int world,
+                           int nloc_override);
+
+int ds_create_block(ds_ctx** out, int n, long prec_bits, int kind, int device, int row0, int nrows) {
+  *out = nullptr;
+  if (row0 < 0 || nrows < 1 || row0 + nrows > n) return DS_INVALID;
+  // a one-rank context sized for the block, then re-based onto rows [row0, row0 + nrows)
+  int rc = ds_create_sized(out, n, prec_bits, kind, device, 0, 1, nrows);
+  if (rc != DS_OK) return rc;
+  (*out)->row_base = row0;
+  return DS_OK;
+}
+
+int ds_pivot_load(ds_ctx* ctx, int step, const ds_soa* row) {
+  if (step < 0 || step >= ctx->n || row->count != ctx->n) return DS_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  const int n = ctx->n, L = ctx->L, nc = ctx->ncomp;
+  PB pb = pb_view(ctx->pbuf, n, L, nc);
+  // the host row is a count-n SoA: exactly the pivot buffer's planes
+  CK(cudaMemcpyAsync(pb.limbs, row->limbs, sizeof(uint32_t) * nc * L * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(pb.exp, row->exp, sizeof(int32_t) * nc * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(pb.cls, row->cls, (size_t)nc * n, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->h2d_bytes += (int64_t)nc * (4 * L + 5) * n;
+  (void)step;
+  return DS_OK;
+}
+
 void ds_destroy(ds_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -1118,6 +1155,11 @@ void ds_destroy(ds_ctx* ctx) {
 }
 
 int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int rank, int world) {
+  return ds_create_sized(out, n, prec_bits, kind, device, rank, world, -1);
+}
+
+static int ds_create_sized(ds_ctx** out, int n, long prec_bits, int kind, int device, int rank, int world,
+                           int nloc_override) {
   *out = nullptr;
   if (n < 1 || prec_bits < 64 || prec_bits > (1L << 24) || (kind != DS_KIND_REAL && kind != DS_KIND_COMPLEX) ||
       world < 1 || rank < 0 || rank >= world) {
@@ -1127,7 +1169,8 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
   ds_ctx* ctx = new ds_ctx();
   ctx->n = n; ctx->p = (int)prec_bits; ctx->L = nlimbs(prec_bits); ctx->kind = kind;
   ctx->ncomp = kind == DS_KIND_COMPLEX ? 2 : 1; ctx->device = device; ctx->rank = rank; ctx->world = world;
-  ctx->nloc = (n - rank + world - 1) / world;
+  ctx->nloc = nloc_override >= 0 ? nloc_override : (n - rank + world - 1) / world;
+  ctx->row_base = 0;
   ctx->launches = 0;
   memset(&ctx->plan, 0, sizeof(ctx->plan));
   CK(cudaSetDevice(device));
@@ -1237,7 +1280,7 @@ int ds_create(ds_ctx** out, int n, long prec_bits, int kind, int device, int ran
 static bool host_rows(const ds_ctx* ctx, int64_t count, int64_t* r0, int64_t* rs) {
   const int64_t n = ctx->n;
   if (count == n * n) {
-    *r0 = ctx->rank;
+    *r0 = ctx->row_base + ctx->rank;
     *rs = ctx->world;
     return true;
   }
@@ -1270,6 +1313,10 @@ static int copy_row_range_to(ds_ctx* ctx, ds_soa* dst, const uint32_t* limbs, co
 
 // ---- streaming of minors rows (ds_stream_minors / ds_stream_flush)
 int ds_stream_minors(ds_ctx* ctx, int batch_steps, ds_rows_cb cb, void* user) {
+  if (ctx->row_base != 0 && batch_steps > 0) {
+    ctx->err = "minors streaming is not available on a row-block (paged) context";
+    return DS_INVALID;
+  }
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaStreamSynchronize(ctx->side));
@@ -1443,7 +1490,7 @@ int ds_generate(ds_ctx* ctx, int family, uint64_t seed) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
   if (gen_uniform_launch(ctx->stream, ctx->a_limbs, ctx->a_exp, ctx->a_cls, ctx->a_count, ctx->n, ctx->L, ctx->p,
-                         ctx->rank, ctx->world, ctx->nloc, seed) != 0) {
+                         ctx->row_base + ctx->rank, ctx->world, ctx->nloc, seed) != 0) {
     ctx->err = "k_gen_uniform launch failed";
     return DS_CUDA;
   }
@@ -1489,7 +1536,7 @@ static int grid_for(ds_ctx* ctx, int64_t work, int block) {
 }
 
 int ds_pivot_stage(ds_ctx* ctx, int i) {
-  if (i < 0 || i >= ctx->n || i % ctx->world != ctx->rank) return DS_INVALID;
+  if (i < 0 || i >= ctx->n || !owns_row(ctx, i)) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
   KArgs k = kargs(ctx);
   int64_t tot = (int64_t)ctx->ncomp * (ctx->L + 2) * ctx->n;
@@ -1684,7 +1731,7 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   }
   ctx->host_have_det = 1;
   ctx->det_from_cur = 0;
-  int jl0 = first_local_after(i, ctx->rank, ctx->world);
+  int jl0 = first_local_after(i, ctx->rank, ctx->world, ctx->row_base);
   int nrows = ctx->nloc - jl0;
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (ctx->prof_on && nrows > 0) {
@@ -1737,7 +1784,8 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
     }
     if (fast) {
       // lookahead for step i + 1 (one rank, inside the current ds_run range, rows left)
-      const int la_col = (ctx->tc.enabled && (ctx->world == 1 || ctx->la_ext) && i + 1 < ctx->la_limit &&
+      const int la_col = (ctx->tc.enabled && ((ctx->world == 1 && ctx->row_base == 0) || ctx->la_ext) &&
+                          i + 1 < ctx->la_limit &&
                           i + 2 < n && !getenv("DS_NO_LOOKAHEAD"))
                              ? i + 1
                              : -1;
@@ -1797,13 +1845,13 @@ int ds_step(ds_ctx* ctx, int i, int collect_minors, int series) {
   // ---- minors of leading size m = i+2 (elim.py:220-226)
   if (collect_minors && i + 1 < n) {
     int m = i + 2;
-    if ((series || m == n) && (i + 1) % ctx->world == ctx->rank) {
+    if ((series || m == n) && owns_row(ctx, i + 1)) {
       int mrc = ensure_minors(ctx);
       if (mrc != DS_OK) return mrc;
       k = kargs(ctx);  // minors pointers
       ks = k;
       ks.scratch = ctx->scratch_side;
-      int64_t jl = (i + 1) / ctx->world;
+      int64_t jl = (i + 1 - ctx->row_base) / ctx->world;
       if (fast) {
         // outputs only: run on the side stream after this step's update
         cudaStream_t ss = ctx->side;
@@ -1915,6 +1963,7 @@ int ds_profile_read(ds_ctx* ctx, double* ms, int64_t* launches, double* work) {
 }
 
 int ds_lookahead_enable(ds_ctx* ctx, int limit) {
+  if (ctx->row_base != 0 && limit > 0) return DS_INVALID;
   if (limit > 0 && (!fast_real(ctx) || !wdiv_ok(ctx))) return DS_INVALID;  // needs the warp division
   ctx->la_limit = limit;
   ctx->la_ext = limit > 0 ? 1 : 0;
@@ -2126,7 +2175,10 @@ static int results_fetch_from(ds_ctx* ctx, int upto, ds_results* r, int minors_f
     CK(cudaMemcpyAsync(tmp, ctx->row_flags, ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->d2h_bytes += ctx->n;
     CK(cudaStreamSynchronize(ctx->stream));
-    for (int m1 = ctx->rank; m1 < ctx->n; m1 += ctx->world) r->row_flags[m1] = tmp[m1];
+    for (int jl = 0; jl < ctx->nloc; jl++) {
+      const int m1 = ctx->row_base + ctx->rank + jl * ctx->world;
+      if (m1 < ctx->n) r->row_flags[m1] = tmp[m1];
+    }
     free(tmp);
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -2139,7 +2191,7 @@ int ds_results_fetch(ds_ctx* ctx, int upto, ds_results* r) { return results_fetc
 // its first m entries) with their flags: the incremental fetch the drop-in
 // eliminate() streams rows to its sink with (world 1)
 int ds_results_fetch_range(ds_ctx* ctx, int t0, int t1, int m0, int m1, ds_results* r) {
-  if (ctx->world != 1) return DS_INVALID;
+  if (ctx->world != 1 || ctx->row_base != 0) return DS_INVALID;
   if (t0 < 0 || t1 > ctx->n || m0 < 2 || m1 > ctx->n + 1) return DS_INVALID;
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->side));
@@ -2186,7 +2238,7 @@ int ds_results_fetch_range(ds_ctx* ctx, int t0, int t1, int m0, int m1, ds_resul
 
 int ds_set_pivot_mode(ds_ctx* ctx, int mode) {
   if (mode != 0 && mode != 1) return DS_INVALID;
-  if (mode == 1 && (ctx->world != 1 || ctx->kind != DS_KIND_REAL)) {
+  if (mode == 1 && (ctx->world != 1 || ctx->row_base != 0 || ctx->kind != DS_KIND_REAL)) {
     ctx->err = "pivot_mode='partial' runs on the serial real engine only (world 1, kind real)";
     return DS_INVALID;
   }
@@ -2216,7 +2268,7 @@ int ds_swaps_fetch(ds_ctx* ctx, int upto_step, uint8_t* swapped) {
 
 int ds_run(ds_ctx* ctx, int collect_minors, int series, int start_step, int stop_step, ds_results* res,
            int* steps_done) {
-  if (ctx->world != 1) return DS_INVALID;
+  if (ctx->world != 1 || ctx->row_base != 0) return DS_INVALID;
   if (start_step < 0 || stop_step > ctx->n || start_step > stop_step) return DS_INVALID;
   if (ctx->pivot_partial && collect_minors) {  // elim.py:186-187
     ctx->err = "partial pivoting cannot be combined with minors collection";

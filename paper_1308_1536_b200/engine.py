@@ -64,19 +64,30 @@ def _check(rc: int, ctx, what: str, rank: int = 0):
 class DeviceElimination:
     """One rank's device context (ds_create .. ds_destroy)."""
 
-    def __init__(self, n: int, prec_bits: int, kind: str, device: int = 0, rank: int = 0, world: int = 1):
+    def __init__(self, n: int, prec_bits: int, kind: str, device: int = 0, rank: int = 0, world: int = 1,
+                 block: tuple | None = None):
+        """block=(row0, nrows): a row-block context of the panel-paged executor (ds_create_block)."""
         self.lib = _native.lib()
         self.n, self.prec_bits, self.kind = n, prec_bits, kind
         self.ncomp = 2 if kind == "complex" else 1
         self.L = (prec_bits + 31) // 32
         self.device, self.rank, self.world = device, rank, world
+        self.block = block
         ctx = ctypes.c_void_p()
-        rc = self.lib.ds_create(ctypes.byref(ctx), n, prec_bits,
-                                _native.DS_KIND_COMPLEX if kind == "complex" else _native.DS_KIND_REAL,
-                                device, rank, world)
+        kcode = _native.DS_KIND_COMPLEX if kind == "complex" else _native.DS_KIND_REAL
+        if block is None:
+            rc = self.lib.ds_create(ctypes.byref(ctx), n, prec_bits, kcode, device, rank, world)
+        else:
+            rc = self.lib.ds_create_block(ctypes.byref(ctx), n, prec_bits, kcode, device, int(block[0]),
+                                          int(block[1]))
         if rc != DS_OK:
             _check(rc, None, "ds_create", rank)
         self.ctx = ctx
+
+    def pivot_load(self, step: int, row: SoA):
+        """Final pivot row `step` (host SoA, count n) into the pivot buffer (ds_pivot_load)."""
+        s = row.c()
+        _check(self.lib.ds_pivot_load(self.ctx, int(step), ctypes.byref(s)), self.ctx, "ds_pivot_load", self.rank)
 
     def close(self):
         if getattr(self, "ctx", None):
