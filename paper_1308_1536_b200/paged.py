@@ -57,13 +57,15 @@ def paged_eliminate_soa(A: SoA, n: int, prec_bits: int, kind: str, panel_rows: i
     nc = 2 if kind == "complex" else 1
     L = (prec_bits + 31) // 32
     res = HostResults.alloc(n, nc, L, collect_minors and sink is None)
-    done = n
+    done = n  # steps completed: the zero-pivot step when one is found
     for r0 in range(0, n, panel_rows):
         r1 = min(n, r0 + panel_rows)
         with DeviceElimination(n, prec_bits, kind, device, block=(r0, r1 - r0)) as e:
             e.load(_rows(A, n, r0, r1))
             failed = -1
-            for i in range(r1):
+            # after a zero pivot at step `done`, later panels still receive steps < done:
+            # the reference leaves every row updated through the completed steps
+            for i in range(min(r1, done)):
                 if i < r0:
                     e.pivot_load(i, _rows(A, n, i, i + 1))
                 else:
@@ -80,10 +82,10 @@ def paged_eliminate_soa(A: SoA, n: int, prec_bits: int, kind: str, panel_rows: i
             _store_rows(A, n, r0, fin)
             part = HostResults(SoA(nc, L, n), SoA(nc, L, n), SoA(nc, L, (r1 - r0) * n) if collect_minors else None,
                                SoA(nc, L, (r1 - r0) * n) if collect_minors else None, np.zeros(n, np.uint8))
-            upto = failed if failed >= 0 else r1
+            upto = failed if failed >= 0 else min(r1, done)
             e.results(upto, part)
         # trace entries of this panel's steps
-        lo, hi = r0, upto
+        lo, hi = r0, max(r0, upto)
         if hi > lo:
             for dst, srcv in ((res.pivots, part.pivots), (res.dets, part.dets)):
                 dst.limbs[:, :, lo:hi] = srcv.limbs[:, :, lo:hi]
@@ -117,7 +119,6 @@ def paged_eliminate_soa(A: SoA, n: int, prec_bits: int, kind: str, panel_rows: i
                         res.normalized.cls[:, g * n:g * n + m] = nm.cls
         if failed >= 0:
             done = failed
-            break
     return res, done
 
 
