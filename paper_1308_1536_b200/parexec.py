@@ -536,6 +536,17 @@ def _spawn_run(A: MatrixBuffer, workers: int, collect_minors: bool, series: bool
                  for r in range(workers)]
         for pr in procs:
             pr.start()
+        # a rank that dies leaves the others blocked in a collective: stop them all
+        import time as _time
+        while any(pr.exitcode is None for pr in procs):
+            if any(pr.exitcode not in (None, 0) for pr in procs):
+                for pr in procs:
+                    if pr.exitcode is None:
+                        pr.terminate()
+                for pr in procs:
+                    pr.join(timeout=30)
+                break
+            _time.sleep(0.05)
         for pr in procs:
             pr.join()
         for r, pr in enumerate(procs):

@@ -109,3 +109,26 @@ def test_spawned_process_transport_matches_reference(name, world):
     dig = digest_parts([canonical_bits(x) for x in trace.pivots], [canonical_bits(x) for x in trace.det_series],
                        rows, [canonical_bits(x) for row in A.rows for x in row])
     assert dig == meta["digest"]
+
+
+def _dying_engine(n, p, kind, rank, world):
+    """Engine factory whose rank 1 fails at creation (tests the coordinator's failure path)."""
+    if rank == 1:
+        raise RuntimeError("injected worker failure")
+    import oracle
+    return oracle.OracleRank(n, p, kind, rank, world, 1)
+
+
+def test_spawned_process_transport_worker_failure():
+    """A rank that dies raises WorkerFailure in the caller and the surviving ranks are stopped
+    instead of waiting in a collective forever (ref parexec.py:395-405 raises WorkerFailure)."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _util import build_input, load_golden
+    from paper_1308_1536_b200 import MatrixBuffer, Precision, par_eliminate
+    from paper_1308_1536_b200.errors import WorkerFailure
+    from test_dist_gloo import _dying_engine
+    meta, arrays = load_golden("uniform13_s5_p192")
+    A = MatrixBuffer.from_soa(meta["n"], meta["kind"], Precision(meta["prec"]), build_input(meta, arrays))
+    with pytest.raises(WorkerFailure):
+        par_eliminate(A, 2, transport="process", _engine_factory=_dying_engine)
