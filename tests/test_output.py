@@ -184,3 +184,24 @@ def test_minors_stream_binary_round_trip(tmp_path):
         if nm is not None:
             assert np.array_equal(nm.limbs, t.limbs[:, :, sl])
     assert st.sizes == [2, 3, 4, 6] and st.digest.startswith("sum64:")
+
+
+def test_write_results_applies_partial_pivot_swap_signs(tmp_path):
+    """write_results(..., swaps=) writes the signed det_series of a pivot_mode="partial" run: the
+    device keeps the unsigned pivot product and every row swap flips the sign of all later
+    determinants (elim.py:207, 216) -- an exact sign flip of the class byte."""
+    from paper_1308_1536_b200 import mp
+    from paper_1308_1536_b200.engine import HostResults
+    from paper_1308_1536_b200.output import write_results
+    from paper_1308_1536_b200.scalars import format_scalar
+    n, p = 4, 128
+    res = HostResults.alloc(n, 1, (p + 31) // 32, False)
+    with mp.context(precision=p):
+        vals = [mp.mpfr(3), mp.mpfr(-5), mp.mpfr(7), mp.mpfr(0)]
+    for i, v in enumerate(vals):
+        res.dets.set(i, v, p)
+    write_results(res, n, p, "real", tmp_path, n, digits=10, minors=False, swaps=[False, True, False, True])
+    got = (tmp_path / "dets.txt").read_text().splitlines()
+    with mp.context(precision=p):
+        want = [vals[0], -vals[1], -vals[2], vals[3]]  # sign flips from step 1 on, back at step 3
+    assert got == [f"{i + 1} {format_scalar(w, 10)}" for i, w in enumerate(want)]
