@@ -1505,7 +1505,14 @@ static int tcw_plan_init(TcPlan* plan, int n, int nloc, int p, int device, int m
   plan->work = w;
   w->fb_cap = fb_capacity(nloc, n);
   w->sthreads = 64 * 128;
-  w->tthreads = 148 * 3 * 256;
+  {  // finish-kernel threads: 6 blocks of 256 per SM (measured: -4 % update at 16384 bits vs 3, equal at
+     // 33220 bits and for complex; DS_TCW_FINISH_BLOCKS overrides, A/B)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int bps = 6;
+    if (const char* e = getenv("DS_TCW_FINISH_BLOCKS")) bps = atoi(e) > 0 ? atoi(e) : 6;
+    w->tthreads = (int64_t)sms * bps * 256;
+  }
   bool ok = cudaMalloc(&w->zbytes, (size_t)D8p * (nloc > 0 ? nloc : 1) * nc) == cudaSuccess &&
             cudaMalloc(&w->bbytes, (size_t)D8p * ncp * nc) == cudaSuccess &&  // k_tcw_pack image(s)
             cudaMalloc(&w->zf, sizeof(double) * (nloc > 0 ? nloc : 1)) == cudaSuccess &&
