@@ -1558,10 +1558,13 @@ static bool force_general() {
   return g_force_general == 1;
 }
 
+// limbs per lane of the warp division: the smallest instantiated K with 32 K >= L
+// (33,220 bits = 1039 limbs takes K = 36, not 64: half the lane work, no spills)
 static int warp_k(int L) {
-  int K = 1;
-  while (32 * K < L) K *= 2;
-  return K;
+  static const int ks[] = {1, 2, 4, 8, 16, 24, 32, 36, 48, 64};
+  for (int K : ks)
+    if (32 * K >= L) return K;
+  return 64;
 }
 
 #define WDIV_DISPATCH(K_, KERNEL, grid, block, smem, s, ...)                 \
@@ -1571,7 +1574,10 @@ static int warp_k(int L) {
     case 4: KERNEL<4><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
     case 8: KERNEL<8><<<grid, block, smem, s>>>(__VA_ARGS__); break;         \
     case 16: KERNEL<16><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    case 24: KERNEL<24><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
     case 32: KERNEL<32><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    case 36: KERNEL<36><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
+    case 48: KERNEL<48><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
     default: KERNEL<64><<<grid, block, smem, s>>>(__VA_ARGS__); break;       \
   }
 
@@ -1595,7 +1601,10 @@ static void set_wdiv_attrs(int maxsm) {
   cudaFuncSetAttribute(KERNEL<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<36>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
+  cudaFuncSetAttribute(KERNEL<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm); \
   cudaFuncSetAttribute(KERNEL<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
   SA(k_mult_w)
   SA(k_emit_norm_w)
