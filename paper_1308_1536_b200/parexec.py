@@ -188,13 +188,15 @@ def block_reassign_plan(step: int, n: int, workers: int) -> list:
 def _assemble(A: MatrixBuffer, trace: EliminationTrace, res: HostResults, done: int, collect_minors: bool,
               sink, out: MinorSeries | None):
     p = A.prec.bits
-    for i in range(done):
-        trace.pivots.append(res.pivots.get(i, p))
-        trace.det_series.append(res.dets.get(i, p))
+    from .soa import paused_gc
+    with paused_gc():
+        trace.pivots.extend(res.pivots.scalars(0, done, p))
+        trace.det_series.extend(res.dets.scalars(0, done, p))
+        rows = minor_rows_from_results(res, A.n, p) if collect_minors else []
     trace.step = done
     if collect_minors:
         emit = sink if sink is not None else out.add
-        for row in minor_rows_from_results(res, A.n, p):
+        for row in rows:
             emit(row)
 
 

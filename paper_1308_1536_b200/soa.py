@@ -21,6 +21,24 @@ from .mp import mpc, mpfr
 CLS_POS, CLS_NEG, CLS_PZERO, CLS_NZERO = 0, 1, 2, 3
 
 
+class paused_gc:
+    """Cyclic garbage collection paused while millions of scalar objects are created
+    (the boundary conversion of minors rows / the in-place buffer): the objects hold
+    no reference cycles, and repeated full collections over a growing heap made the
+    conversion ~4x slower.  Restores the previous state; nests."""
+
+    def __enter__(self):
+        import gc
+        self._was = gc.isenabled()
+        gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+
+
 class ds_soa(ctypes.Structure):
     _fields_ = [("limbs", ctypes.c_void_p), ("exp", ctypes.c_void_p), ("cls", ctypes.c_void_p),
                 ("count", ctypes.c_int64)]
