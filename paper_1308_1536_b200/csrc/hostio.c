@@ -414,3 +414,27 @@ int dsh_mpfr_structs(__mpfr_struct *out, uint64_t *pool, const int32_t *ex, cons
   }
   return 0;
 }
+
+/* Same, from the plane-major SoA limbs directly: the transpose into the
+ * element-major pool (2*n64 words per scalar, the L limbs right-aligned) is done
+ * here in 32-element blocks so each block's pool rows stay in L1. */
+int dsh_mpfr_structs_planes(__mpfr_struct *out, uint32_t *pool, const uint32_t *limbs, int64_t plane_stride, int L,
+                            const int32_t *ex, const uint8_t *cl, int64_t count, int n64, long p) {
+  const int W = 2 * n64, pad = W - L;
+  if (pad < 0) return -1;
+  const int64_t nblk = (count + 31) / 32;
+#pragma omp parallel for schedule(static) if (count >= 1024)
+  for (int64_t b = 0; b < nblk; b++) {
+    const int64_t k0 = b * 32;
+    const int64_t nb = count - k0 < 32 ? count - k0 : 32;
+    uint32_t *dst = pool + k0 * W;
+    for (int64_t kk = 0; kk < nb; kk++)
+      for (int j = 0; j < pad; j++) dst[kk * W + j] = 0;
+    for (int j = 0; j < L; j++) {
+      const uint32_t *src = limbs + (int64_t)j * plane_stride + k0;
+      for (int64_t kk = 0; kk < nb; kk++) dst[kk * W + pad + j] = src[kk];
+    }
+  }
+  return dsh_mpfr_structs(out, (uint64_t *)pool, ex, cl, count, n64, p);
+}
+

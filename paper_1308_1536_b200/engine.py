@@ -218,6 +218,14 @@ class DeviceElimination:
         _check(self.lib.ds_stream_minors(self.ctx, int(batch_steps), self._stream_cb, None), self.ctx,
                "ds_stream_minors", self.rank)
 
+    def stream_minors_native(self, batch_steps: int, cb_ptr: int, user_ptr: int):
+        """Stream the minors rows to a native ds_rows_cb (e.g. hostgen.RowQueue, which
+        builds the scalar structs off the interpreter)."""
+        self._stream_cb = None
+        self._stream_exc = None
+        _check(self.lib.ds_stream_minors(self.ctx, int(batch_steps), ctypes.c_void_p(cb_ptr),
+                                         ctypes.c_void_p(user_ptr)), self.ctx, "ds_stream_minors", self.rank)
+
     def stream_flush(self, upto_step: int, final: bool = False):
         _check(self.lib.ds_stream_flush(self.ctx, int(upto_step), int(final)), self.ctx, "ds_stream_flush",
                self.rank)

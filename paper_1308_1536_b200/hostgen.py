@@ -42,6 +42,20 @@ def _load():
         L.dsh_mpfr_structs.restype = ctypes.c_int
         L.dsh_mpfr_structs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int64, ctypes.c_int, ctypes.c_long]
+        L.dsh_mpfr_structs_planes.restype = ctypes.c_int
+        L.dsh_mpfr_structs_planes.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int, ctypes.c_long]
+        L.dsh_rowq_create.restype = ctypes.c_void_p
+        L.dsh_rowq_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, ctypes.c_int]
+        L.dsh_rowq_close.restype = None
+        L.dsh_rowq_close.argtypes = [ctypes.c_void_p]
+        L.dsh_rowq_destroy.restype = None
+        L.dsh_rowq_destroy.argtypes = [ctypes.c_void_p]
+        L.dsh_rowq_pop.restype = ctypes.POINTER(_RowBatch)
+        L.dsh_rowq_pop.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+        L.dsh_rowbatch_free.restype = None
+        L.dsh_rowbatch_free.argtypes = [ctypes.POINTER(_RowBatch)]
         L.dsh_soa_to_mpfr_pool.restype = ctypes.c_int
         L.dsh_soa_to_mpfr_pool.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ds_soa), ctypes.c_int,
                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_long]
@@ -154,3 +168,78 @@ def power_matrix_soa(zeros_path: str, M: int, prec_bits: int, t: str = "25", zer
     if rc != 0:
         raise RuntimeError("power matrix builder failed")
     return out
+
+
+# -- native consumer of the minors stream (csrc/hoststream.c) ---------------------------
+class _RowBatch(ctypes.Structure):
+    _fields_ = [("g0", ctypes.c_int32), ("stride", ctypes.c_int32), ("nrows", ctypes.c_int32),
+                ("ncomp", ctypes.c_int32), ("m", ctypes.POINTER(ctypes.c_int32)),
+                ("flags", ctypes.POINTER(ctypes.c_uint8)), ("off", ctypes.POINTER(ctypes.c_int64)),
+                ("sg", ctypes.c_void_p * 2), ("nm", ctypes.c_void_p * 2), ("nel", ctypes.c_int64)]
+
+
+class _BatchOwner:
+    """Keeps one native batch (structs + limb pool) alive while any scalar wraps it."""
+    __slots__ = ("ptr", "free")
+
+    def __init__(self, ptr, free):
+        self.ptr, self.free = ptr, free
+
+    def __del__(self):
+        self.free(self.ptr)
+
+
+class RowQueue:
+    """Minors-stream consumer whose callback (dsh_rowq_cb) runs natively on the thread
+    that drives ds_run: each delivered batch becomes ready mpfr structs there, and
+    pop_rows() on the caller's thread (GIL released while it waits) only wraps them
+    in scalar objects.  Rows come back as (m, signed, normalized | None) in delivery
+    (= increasing size) order."""
+
+    def __init__(self, n: int, ncomp: int, L: int, prec: int, nthreads: int = 0):
+        self.lib = _load()
+        self.prec = prec
+        self.q = self.lib.dsh_rowq_create(n, ncomp, L, prec, nthreads)
+        if not self.q:
+            raise ValueError("dsh_rowq_create: invalid shape")
+        self.cb_ptr = ctypes.cast(self.lib.dsh_rowq_cb, ctypes.c_void_p).value
+
+    def close(self):
+        """Producer side done: pop_rows() returns None once drained."""
+        self.lib.dsh_rowq_close(self.q)
+
+    def pop_rows(self):
+        """The next batch's rows, or None when the queue is closed and drained."""
+        from . import mp
+        failed = ctypes.c_int(0)
+        bp = self.lib.dsh_rowq_pop(self.q, ctypes.byref(failed))
+        if not bp:
+            if failed.value:
+                raise MemoryError("host memory for a streamed minors batch could not be allocated")
+            return None
+        b = bp.contents
+        owner = _BatchOwner(bp, self.lib.dsh_rowbatch_free)
+        T = mp._MPFR_T
+        sz = ctypes.sizeof(T)
+        out = []
+        for r in range(b.nrows):
+            m = b.m[r]
+            if not m:
+                continue
+            off = b.off[r] * sz
+            sg = [mp.wrap_pooled((T * m).from_address(b.sg[c] + off), owner, m) for c in range(b.ncomp)]
+            nm = ([mp.wrap_pooled((T * m).from_address(b.nm[c] + off), owner, m) for c in range(b.ncomp)]
+                  if b.flags[r] & 2 else None)
+            if b.ncomp == 2:
+                sg = [mp.mpc_from_parts(x, y) for x, y in zip(*sg)]
+                nm = [mp.mpc_from_parts(x, y) for x, y in zip(*nm)] if nm is not None else None
+            else:
+                sg = sg[0]
+                nm = nm[0] if nm is not None else None
+            out.append((m, sg, nm))
+        return out
+
+    def __del__(self):
+        q, self.q = getattr(self, "q", None), None
+        if q:
+            self.lib.dsh_rowq_destroy(q)

@@ -108,13 +108,19 @@ class SoA:
         pad = 2 * n64 - self.L
         parts = []
         for c in range(self.ncomp):
-            # element-major limb pool (one transpose), read in place by the mpfr structs
-            pool = np.zeros((count, 2 * n64), dtype=np.uint32)
-            pool[:, pad:] = self.limbs[c, :, start:start + count].T
+            # element-major limb pool, transposed from the planes natively and read in
+            # place by the mpfr structs
+            pool = np.empty((count, 2 * n64), dtype=np.uint32)
+            planes = self.limbs[c]
+            if planes.strides[1] != 4:
+                planes = np.ascontiguousarray(planes)
             ex = np.ascontiguousarray(self.exp[c, start:start + count])
             cl = np.ascontiguousarray(self.cls[c, start:start + count])
             arr = (mp._MPFR_T * count)()
-            lib.dsh_mpfr_structs(arr, pool.ctypes.data, ex.ctypes.data, cl.ctypes.data, count, n64, prec)
+            if pad < 0 or lib.dsh_mpfr_structs_planes(arr, pool.ctypes.data, planes.ctypes.data + 4 * start,
+                                                      planes.strides[0] // 4, self.L, ex.ctypes.data,
+                                                      cl.ctypes.data, count, n64, prec) != 0:
+                raise ValueError("SoA.scalars: precision %d does not hold %d limbs" % (prec, self.L))
             parts.append(mp.wrap_pooled(arr, (arr, pool), count))
         if self.ncomp == 1:
             return parts[0]
