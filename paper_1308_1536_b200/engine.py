@@ -10,6 +10,7 @@ semantics) -- see parexec.py of this package.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +62,19 @@ def _check(rc: int, ctx, what: str, rank: int = 0):
     raise WorkerFailure(rank, f"{what} failed with code {rc}: {msg}")
 
 
+_closing: list = []  # threads releasing contexts in the background (DeviceElimination.close_async)
+_closing_lock = threading.Lock()
+
+
+def wait_released():
+    """Join every background context release (its HBM is free afterwards)."""
+    with _closing_lock:
+        threads = list(_closing)
+        _closing.clear()
+    for t in threads:
+        t.join()
+
+
 class DeviceElimination:
     """One rank's device context (ds_create .. ds_destroy)."""
 
@@ -68,6 +82,7 @@ class DeviceElimination:
                  block: tuple | None = None):
         """block=(row0, nrows): a row-block context of the panel-paged executor (ds_create_block)."""
         self.lib = _native.lib()
+        wait_released()  # a context still being released holds its HBM
         self.n, self.prec_bits, self.kind = n, prec_bits, kind
         self.ncomp = 2 if kind == "complex" else 1
         self.L = (prec_bits + 31) // 32
@@ -93,6 +108,20 @@ class DeviceElimination:
         if getattr(self, "ctx", None):
             self.lib.ds_destroy(self.ctx)
             self.ctx = None
+
+    def close_async(self):
+        """Release the context on a background thread: ds_destroy frees gigabytes of
+        device and pinned memory (10-800 ms) that the caller need not wait for.  The
+        next context creation (and interpreter exit: the thread is not a daemon) waits
+        for it, so peak memory is as with close()."""
+        ctx = getattr(self, "ctx", None)
+        if not ctx:
+            return
+        self.ctx = None
+        t = threading.Thread(target=self.lib.ds_destroy, args=(ctx,), name="ds_destroy")
+        with _closing_lock:
+            _closing.append(t)
+        t.start()
 
     def __del__(self):
         try:

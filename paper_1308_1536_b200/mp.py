@@ -651,22 +651,31 @@ def from_limbs(raw: bytes, exp: int, cls: int, prec: int) -> "mpfr":
 
 
 class _pooled_mpfr(mpfr):
-    """mpfr over a struct whose significand lives in a shared limb pool
-    (SoA.scalars): the pool is kept alive by the object, and nothing is freed per
-    scalar.  Behaves as mpfr everywhere (isinstance, arithmetic, formatting)."""
-    __slots__ = ("_pool",)
+    """mpfr over struct k of a ctypes array of initialised structs whose significands
+    live in a shared limb pool (SoA.scalars, hostgen.RowQueue).  The object holds the
+    array (which holds the pool's owner); the struct view is made on access, so
+    creating one costs two slot stores and nothing is freed per scalar.  Behaves as
+    mpfr everywhere (isinstance, arithmetic, formatting)."""
+    __slots__ = ("_arr", "_k")
+
+    @property
+    def _s(self):
+        return self._arr[self._k]
 
     def __del__(self):
         pass
 
 
-def wrap_pooled(arr, pool, count: int) -> list:
+def wrap_pooled(arr, owner, count: int) -> list:
+    """Scalars over arr[0..count); `owner` (the limb pool / native batch) lives as long
+    as any of them."""
+    arr._owner = owner
     new = object.__new__
     out = []
     for k in range(count):
         o = new(_pooled_mpfr)
-        o._s = arr[k]
-        o._pool = pool
+        o._arr = arr
+        o._k = k
         out.append(o)
     return out
 

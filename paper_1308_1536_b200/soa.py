@@ -121,7 +121,7 @@ class SoA:
                                                       planes.strides[0] // 4, self.L, ex.ctypes.data,
                                                       cl.ctypes.data, count, n64, prec) != 0:
                 raise ValueError("SoA.scalars: precision %d does not hold %d limbs" % (prec, self.L))
-            parts.append(mp.wrap_pooled(arr, (arr, pool), count))
+            parts.append(mp.wrap_pooled(arr, pool, count))
         if self.ncomp == 1:
             return parts[0]
         return [mp.mpc_from_parts(a, b) for a, b in zip(parts[0], parts[1])]
