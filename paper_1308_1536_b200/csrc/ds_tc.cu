@@ -1236,7 +1236,93 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
 }
 
 // ---------------------------------------------------------------- complex
-// a <- RN(a - RN(z b)) per component on the wide engine (elim.py:49-52 on mpc):
+// a <- RN(a - RN(z b)) per component on the wide engine (elim.py:49-52 on mpc).
+//
+// One element (row ri of the chunk, column index cidx) of the complex finish; a's
+// limbs of component c are read and written through am[c] (global planes, or a
+// shared-memory staging copy).  Returns false when the element went to the
+// fallback list (a unchanged).
+__device__ bool finish_c_elem(const TcArgs& a, const TwArgs& w, int ri, int cidx, int row_first, ds::Ptr Ssum,
+                              ds::Ptr Tre, ds::Ptr Tim, ds::Ptr tmp, const ds::Ptr* am) {
+  const int L = a.L, p = a.p;
+  const int k = a.kstart + cidx;
+  const int zr = row_first + ri;  // relative to jl0
+  const int jl = a.jl0 + zr;
+  const int64_t idx = (int64_t)jl * a.n + k;
+  const int64_t region = w.pstride * (int64_t)w.W;  // words per product region (c1, c2)
+  int64_t ze[2], be[2];
+  uint8_t zc[2], bc[2];
+  for (int c = 0; c < 2; c++) {
+    ze[c] = a.zexp[(int64_t)c * a.zstride + zr];
+    zc[c] = a.zcls[(int64_t)c * a.zstride + zr];
+    be[c] = a.bexp[(int64_t)c * a.n + k];
+    bc[c] = a.bcls[(int64_t)c * a.n + k];
+  }
+  auto term = [&](int c1, int c2) -> ds::XTerm {
+    ds::XTerm t;
+    t.m = ds::CPtr{w.tprod + (2 * c1 + c2) * region + (int64_t)ri * w.ncp + cidx, w.pstride};
+    t.n = w.W;
+    t.base = ze[c1] + be[c2] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
+    t.neg = (zc[c1] & 1) ^ (bc[c2] & 1);
+    t.zero = zc[c1] >= DS_CLS_PZERO || bc[c2] >= DS_CLS_PZERO;
+    return t;
+  };
+  bool ok = true;
+  int32_t te[2];
+  uint8_t tcl[2];
+  for (int c = 0; c < 2 && ok; c++) {
+    const ds::XTerm X = c == 0 ? term(0, 0) : term(0, 1);
+    const ds::XTerm Y = c == 0 ? term(1, 1) : term(1, 0);
+    const ds::XSum x = ds::exact_sum(Ssum, X, Y, c == 0, 2 * (int64_t)p + 64);
+    if (x.zero) {
+      ok = X.zero && Y.zero;  // a truncated nonzero sum that cancels: undecided
+    } else {
+      const int64_t H = x.base + ds::top_bit(ds::CPtr{Ssum.p, Ssum.s}, x.n);
+      const int64_t R = H - p + 1;  // weight of the result's LSB
+      int64_t bnd = INT64_MIN;
+      int64_t tmin = INT64_MAX;
+      if (!X.zero) {
+        bnd = max(bnd, X.base + w.eps);
+        tmin = min(tmin, X.base + ds::top_bit(X.m, X.n));
+      }
+      if (!Y.zero) {
+        bnd = max(bnd, Y.base + w.eps);
+        tmin = min(tmin, Y.base + ds::top_bit(Y.m, Y.n));
+      }
+      bnd += 1;                                // both errors together < 2^bnd
+      if (x.pert) bnd = max(bnd, tmin + 2);    // the far term only perturbs
+      if (R - 1 <= bnd) {
+        ok = false;
+      } else {
+        bool ones, zeros;
+        bit_range(ds::CPtr{Ssum.p, Ssum.s}, x.n, max((int64_t)0, bnd - x.base), R - 1 - x.base, &ones, &zeros);
+        ok = !ones && !zeros;
+      }
+    }
+    if (ok) {
+      const ds::Ptr T = c == 0 ? Tre : Tim;
+      if (!ds::round_xsum(T, &te[c], &tcl[c], Ssum, x, L, p)) atomicAdd(&a.status[2], 1);
+    }
+  }
+  if (!ok) {
+    int slot = atomicAdd(a.fb_count, 1);
+    if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
+    else atomicAdd(&a.status[5], 1);
+    return false;
+  }
+  for (int c = 0; c < 2; c++) {
+    const int64_t mo = (int64_t)c * a.a_count + idx;
+    ds::Val av{ds::CPtr{am[c].p, am[c].s}, a.a_exp[mo], a.a_cls[mo]};
+    ds::Val tv{ds::CPtr{(c == 0 ? Tre : Tim).p, (c == 0 ? Tre : Tim).s}, te[c], tcl[c]};
+    int32_t re;
+    uint8_t rc;
+    if (!ds::add_rn(am[c], &re, &rc, av, tv, true, L, p, tmp)) atomicAdd(&a.status[2], 1);
+    a.a_exp[mo] = re;
+    a.a_cls[mo] = rc;
+  }
+  return true;
+}
+
 // Re = RN(zr br - zi bi), Im = RN(zr bi + zi br), each the exact formula rounded
 // once (mpc_mul), then a_c <- RN(a_c - t_c) (mpc_sub).  The four products come
 // from k_prod_tcw as truncated limbs (each short by < 2^eps units of its limb
@@ -1244,10 +1330,11 @@ __global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int r
 // between the combined error bound and the round bit are neither all zeros nor
 // all ones, so no rounding boundary lies within the error; else the element
 // takes the exact complex fallback.  Scratch row per thread: sum | T_re | T_im |
-// add_rn.
+// add_rn.  Thread per element (DS_CX_FINISH_THREAD=1; the default is the
+// warp-cooperative k_cfw_finish below).
 __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int row_first, uint32_t* scratch) {
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
-  const int L = a.L, p = a.p;
+  const int L = a.L;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)w.nrows * a.ncols;
   // per-thread scratch interleaved across the grid (word k of thread t at k * T + t):
@@ -1257,88 +1344,18 @@ __global__ void __launch_bounds__(256) k_tcw_finish_c(TcArgs a, TwArgs w, int ro
   uint32_t* row = scratch + tid;
   const ds::Ptr Ssum{row, T}, Tre{row + (4 * (int64_t)L + 16) * T, T}, Tim{row + (5 * (int64_t)L + 16) * T, T},
       tmp{row + (6 * (int64_t)L + 16) * T, T};
-  const int64_t region = w.pstride * (int64_t)w.W;  // words per product region (c1, c2)
   for (int64_t e = tid; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int ri = (int)(e / a.ncols), cidx = (int)(e % a.ncols);
     const int k = a.kstart + cidx;
     if (k < a.kmin || k == a.skip_col || k >= a.n) continue;
-    const int zr = row_first + ri;  // relative to jl0
-    const int jl = a.jl0 + zr;
-    const int64_t idx = (int64_t)jl * a.n + k;
-    int64_t ze[2], be[2];
-    uint8_t zc[2], bc[2];
-    for (int c = 0; c < 2; c++) {
-      ze[c] = a.zexp[(int64_t)c * a.zstride + zr];
-      zc[c] = a.zcls[(int64_t)c * a.zstride + zr];
-      be[c] = a.bexp[(int64_t)c * a.n + k];
-      bc[c] = a.bcls[(int64_t)c * a.n + k];
-    }
-    auto term = [&](int c1, int c2) -> ds::XTerm {
-      ds::XTerm t;
-      t.m = ds::CPtr{w.tprod + (2 * c1 + c2) * region + (int64_t)ri * w.ncp + cidx, w.pstride};
-      t.n = w.W;
-      t.base = ze[c1] + be[c2] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
-      t.neg = (zc[c1] & 1) ^ (bc[c2] & 1);
-      t.zero = zc[c1] >= DS_CLS_PZERO || bc[c2] >= DS_CLS_PZERO;
-      return t;
-    };
-    bool ok = true;
-    int32_t te[2];
-    uint8_t tcl[2];
-    for (int c = 0; c < 2 && ok; c++) {
-      const ds::XTerm X = c == 0 ? term(0, 0) : term(0, 1);
-      const ds::XTerm Y = c == 0 ? term(1, 1) : term(1, 0);
-      const ds::XSum x = ds::exact_sum(Ssum, X, Y, c == 0, 2 * (int64_t)p + 64);
-      if (x.zero) {
-        ok = X.zero && Y.zero;  // a truncated nonzero sum that cancels: undecided
-      } else {
-        const int64_t H = x.base + ds::top_bit(ds::CPtr{Ssum.p, Ssum.s}, x.n);
-        const int64_t R = H - p + 1;  // weight of the result's LSB
-        int64_t bnd = INT64_MIN;
-        int64_t tmin = INT64_MAX;
-        if (!X.zero) {
-          bnd = max(bnd, X.base + w.eps);
-          tmin = min(tmin, X.base + ds::top_bit(X.m, X.n));
-        }
-        if (!Y.zero) {
-          bnd = max(bnd, Y.base + w.eps);
-          tmin = min(tmin, Y.base + ds::top_bit(Y.m, Y.n));
-        }
-        bnd += 1;                                // both errors together < 2^bnd
-        if (x.pert) bnd = max(bnd, tmin + 2);    // the far term only perturbs
-        if (R - 1 <= bnd) {
-          ok = false;
-        } else {
-          bool ones, zeros;
-          bit_range(ds::CPtr{Ssum.p, Ssum.s}, x.n, max((int64_t)0, bnd - x.base), R - 1 - x.base, &ones, &zeros);
-          ok = !ones && !zeros;
-        }
-      }
-      if (ok) {
-        const ds::Ptr T = c == 0 ? Tre : Tim;
-        if (!ds::round_xsum(T, &te[c], &tcl[c], Ssum, x, L, p)) atomicAdd(&a.status[2], 1);
-      }
-    }
-    if (!ok) {
-      int slot = atomicAdd(a.fb_count, 1);
-      if (slot < a.fb_cap) a.fb_list[slot] = make_int2(jl, k);
-      else atomicAdd(&a.status[5], 1);
-      continue;
-    }
-    for (int c = 0; c < 2; c++) {
-      const int64_t off = (int64_t)c * L * a.a_count + idx;
-      const int64_t mo = (int64_t)c * a.a_count + idx;
-      ds::Val av{ds::CPtr{a.a_limbs + off, a.a_count}, a.a_exp[mo], a.a_cls[mo]};
-      ds::Val tv{ds::CPtr{(c == 0 ? Tre : Tim).p, T}, te[c], tcl[c]};
-      int32_t re;
-      uint8_t rc;
-      if (!ds::add_rn(ds::Ptr{a.a_limbs + off, a.a_count}, &re, &rc, av, tv, true, L, p, tmp))
-        atomicAdd(&a.status[2], 1);
-      a.a_exp[mo] = re;
-      a.a_cls[mo] = rc;
-    }
+    const int64_t idx = (int64_t)(a.jl0 + row_first + ri) * a.n + k;
+    const ds::Ptr am[2] = {ds::Ptr{a.a_limbs + idx, a.a_count}, ds::Ptr{a.a_limbs + (int64_t)L * a.a_count + idx,
+                                                                       a.a_count}};
+    finish_c_elem(a, w, ri, cidx, row_first, Ssum, Tre, Tim, tmp, am);
   }
 }
+
+#include "ds_cfinish.cuh"
 
 // exact complex update of the listed elements: cmul_part x 2 then add_rn x 2
 __global__ void k_tc_fallback_c(TcArgs a, const uint32_t* z_limbs, int64_t z_count, const uint32_t* b_limbs,
@@ -1620,7 +1637,28 @@ int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device) {
   plan->ncomp = 2;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  return tcw_plan_init(plan, n, nloc, p, device, maxsm);
+  int rc = tcw_plan_init(plan, n, nloc, p, device, maxsm);
+  if (rc != DS_OK || !plan->wide) return rc;
+  // the warp-cooperative finish (ds_cfinish.cuh) unless DS_CX_FINISH_THREAD=1
+  const char* ft = getenv("DS_CX_FINISH_THREAD");
+  const int K = (ft && atoi(ft)) ? 0 : cf_k_for(plan->w_W);
+  if (K) {
+    const size_t sm = cf_smem(K, plan->w_W, plan->L);
+    cudaError_t e = cudaSuccess;
+    switch (K) {
+      case 2: e = cudaFuncSetAttribute(k_cfw_finish<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
+      case 3: e = cudaFuncSetAttribute(k_cfw_finish<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
+      case 5: e = cudaFuncSetAttribute(k_cfw_finish<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
+      default: e = cudaFuncSetAttribute(k_cfw_finish<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
+    }
+    if (e == cudaSuccess && (int)sm <= maxsm) {
+      plan->cf_k = K;
+      plan->cf_smem = sm;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  return DS_OK;
 }
 
 void tc_plan_free(TcPlan* plan) {
@@ -1743,7 +1781,14 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
             tc.tprod = w->tprod + (size_t)(2 * c1 + c2) * tw.pstride * tw.W;
             k_prod_tcw<<<dim3(ntile, (rc + tw.rbr - 1) / tw.rbr), TW_THREADS, plan->smem, s>>>(tc);
           }
-        k_tcw_finish_c<<<(unsigned)(w->tthreads / 256), 256, 0, s>>>(a, tw, r0, w->tscratch);
+        const unsigned fb = (unsigned)(w->tthreads / 256);
+        switch (plan->cf_k) {
+          case 2: k_cfw_finish<2><<<fb, 256, plan->cf_smem, s>>>(a, tw, r0, w->tscratch, w->tthreads); break;
+          case 3: k_cfw_finish<3><<<fb, 256, plan->cf_smem, s>>>(a, tw, r0, w->tscratch, w->tthreads); break;
+          case 5: k_cfw_finish<5><<<fb, 256, plan->cf_smem, s>>>(a, tw, r0, w->tscratch, w->tthreads); break;
+          case 9: k_cfw_finish<9><<<fb, 256, plan->cf_smem, s>>>(a, tw, r0, w->tscratch, w->tthreads); break;
+          default: k_tcw_finish_c<<<fb, 256, 0, s>>>(a, tw, r0, w->tscratch);
+        }
         *launches += 5;
       }
     }

@@ -14,6 +14,8 @@ struct TcPlan {
   int wide;
   int ncomp;           // 2: complex elements (wide engine, four component products)
   int w_kc, w_nst, w_brc, w_qlo, w_W, w_zwb, w_rows, w_rbr;
+  int cf_k;            // complex: words per lane of the warp finish (0: thread-per-element finish)
+  size_t cf_smem;
   void* work;
 };
 

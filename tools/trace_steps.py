@@ -1,6 +1,6 @@
 """Kernel timeline of a window of elimination steps (CUPTI via torch.profiler).
 
-usage: python tools/trace_steps.py N P START STOP [out.json]
+usage: python tools/trace_steps.py N P[c] START STOP [out.json]   (Pc: complex)
 Runs steps [0, START) untraced, traces [START, STOP), prints per-kernel totals,
 per-stream busy time and the idle gaps of the main stream."""
 import collections
@@ -14,12 +14,14 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 from paper_1308_1536_b200.engine import DeviceElimination, HostResults  # noqa: E402
 from paper_1308_1536_b200.synth import random_uniform_soa  # noqa: E402
 
+kind = "complex" if sys.argv[2].endswith("c") else "real"  # P suffix c: complex elements
+sys.argv[2] = sys.argv[2].rstrip("c")
 n, p, start, stop = map(int, sys.argv[1:5])
 out = sys.argv[5] if len(sys.argv) > 5 else "gpurun_out/trace.json"
-A = random_uniform_soa(n, p, 1)
+A = random_uniform_soa(n, p, 1, kind=kind)
 L = (p + 31) // 32
-with DeviceElimination(n, p, "real") as eng:
-    res = HostResults.alloc(n, 1, L, True)
+with DeviceElimination(n, p, kind) as eng:
+    res = HostResults.alloc(n, eng.ncomp, L, True)
     eng.load(A)
     eng.run(True, True, 0, start, res)
     torch.cuda.synchronize()
