@@ -207,6 +207,7 @@ struct CfTerm {
   int64_t base;
   int neg;
   bool zero;
+  bool exact;         // no nonzero digit product below c_lo: the short product is the product
 };
 
 // T = RN(X +/- Y) -- ds::exact_sum, the error-bound test of finish_c_elem and
@@ -217,7 +218,9 @@ struct CfTerm {
 // most W + 2 words whatever the gap between the terms (a term far below the other
 // -- the perturbation case of exact_sum -- is just a borrow here; both formulations
 // decide only when the rounding of the exact value is certain, so the results are
-// the same bits).  Returns 0 (T written; a zero T has a zero class), 1 (undecided:
+// the same bits).  Products whose omitted digit products are all zero (k_lowdig:
+// low(z) + low(b) >= c_lo, e.g. a pivot row of small integers) carry no error: a
+// sum of such terms is rounded directly.  Returns 0 (T written; a zero T has a zero class), 1 (undecided:
 // fallback list).
 template <int K>
 __device__ int cf_xsum_round(const CfTerm& X, const CfTerm& Y, bool subY, int W, int eps, int p, int L,
@@ -230,8 +233,9 @@ __device__ int cf_xsum_round(const CfTerm& X, const CfTerm& Y, bool subY, int W,
     return 0;
   }
   int64_t bnd = INT64_MIN;
-  if (!X.zero) bnd = max(bnd, X.base + eps);
-  if (!Y.zero) bnd = max(bnd, Y.base + eps);
+  if (!X.zero && !X.exact) bnd = max(bnd, X.base + eps);
+  if (!Y.zero && !Y.exact) bnd = max(bnd, Y.base + eps);
+  const bool exact = bnd == INT64_MIN;  // the sum formed below is the exact value
   bnd += 1;  // both truncation errors together < 2^bnd
   const int64_t tx = X.zero ? INT64_MIN : X.base + cf_top_sm(X.m, W, lane);
   const int64_t ty = Y.zero ? INT64_MIN : Y.base + cf_top_sm(Y.m, W, lane);
@@ -272,14 +276,22 @@ __device__ int cf_xsum_round(const CfTerm& X, const CfTerm& Y, bool subY, int W,
     }
   }
   const int64_t hS = cf_top<K>(S);
-  if (hS < 0) return 1;  // the sum is below 2^hi < 2^bnd: undecided
+  if (hS < 0) return 1;  // the sum is below 2^hi: undecided (exact engine)
   const int64_t R = hi + hS - p + 1;  // weight of the result's LSB
-  if (R - 1 <= bnd) return 1;
-  bool ones, zeros;
-  cf_range<K>(S, bnd - hi, R - 1 - hi, lane, &ones, &zeros);
-  if (ones || zeros) return 1;
-  // the bits checked above lie below the round bit and are not all zeros: sticky
-  const int64_t e = hi + cf_round<K>(S, hS, p, L, sb, Tout, lane, true);
+  int64_t e;
+  if (exact) {
+    // exact products: round the exact sum (round bit in the window, sticky from the
+    // window and the low term)
+    if (R - 1 < hi) return 1;
+    e = hi + cf_round<K>(S, hS, p, L, sb, Tout, lane, low_nz);
+  } else {
+    if (R - 1 <= bnd) return 1;
+    bool ones, zeros;
+    cf_range<K>(S, bnd - hi, R - 1 - hi, lane, &ones, &zeros);
+    if (ones || zeros) return 1;
+    // the bits checked above lie below the round bit and are not all zeros: sticky
+    e = hi + cf_round<K>(S, hS, p, L, sb, Tout, lane, true);
+  }
   *te = (int32_t)e;
   *tcl = ds::nz_cls(neg);
   *rng = ds::range_ok(e);
@@ -414,6 +426,7 @@ __device__ bool cf_element(const TcArgs& a, const TwArgs& w, int row_first, int 
     t.base = ze[c1] + be[c2] - 64 * (int64_t)L + 32 * (int64_t)w.qlo;
     t.neg = (zc[c1] & 1) ^ (bc[c2] & 1);
     t.zero = zc[c1] >= DS_CLS_PZERO || bc[c2] >= DS_CLS_PZERO;
+    t.exact = a.zlow[(int64_t)c1 * a.zstride + zr] + a.blow[(int64_t)c2 * a.n + k] >= w.c_lo;
     return t;
   };
   uint32_t* sb = wsb;

@@ -85,6 +85,8 @@ struct TcArgs {
   int* fb_count;           // fallback list
   int2* fb_list;
   int fb_cap;
+  const int* zlow;         // complex warp finish: lowest nonzero digit of z [c][row] and b [c][col]
+  const int* blow;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -170,6 +172,23 @@ __global__ void k_tc_bytes(const uint32_t* src, int64_t count, int num, int L, i
     uint64_t top = ((uint64_t)src[(int64_t)(L - 1) * count + e] << 32) | src[(int64_t)(L - 2) * count + e];
     topf[e] = (double)top * 0x1p-63;
   }
+}
+
+// index of the lowest nonzero digit (byte of the limbs) of each element, 1 << 28 for
+// zero: a short product z b omits no nonzero digit product exactly when
+// low(z) + low(b) >= c_lo (ds_cfinish.cuh treats such products as exact)
+__global__ void k_lowdig(const uint32_t* src, int64_t count, int num, int L, int* out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= num) return;
+  int low = 1 << 28;
+  for (int l = 0; l < L; l++) {
+    const uint32_t v = src[(int64_t)l * count + e];
+    if (v) {
+      low = 4 * l + (__ffs(v) - 1) / 8;
+      break;
+    }
+  }
+  out[e] = low;
 }
 
 // ---------------------------------------------------------------- main
@@ -1452,6 +1471,8 @@ struct TcWork {
   uint32_t* tprod;         // wide: product limbs [W][rows][ncp]
   uint32_t* tscratch;      // wide: finish-kernel scratch [3L + 8][tthreads]
   int64_t tthreads;
+  int* zlow;               // complex warp finish: k_lowdig of z [2][nloc] and of the pivot row [2][n]
+  int* blow;
   const void* amap_base;
   int64_t amap_count;
   int amap_ok;
@@ -1651,7 +1672,10 @@ int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device) {
       case 5: e = cudaFuncSetAttribute(k_cfw_finish<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
       default: e = cudaFuncSetAttribute(k_cfw_finish<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); break;
     }
-    if (e == cudaSuccess && (int)sm <= maxsm) {
+    TcWork* w = (TcWork*)plan->work;
+    if (e == cudaSuccess && (int)sm <= maxsm &&
+        cudaMalloc(&w->zlow, sizeof(int) * 2 * (size_t)(nloc > 0 ? nloc : 1)) == cudaSuccess &&
+        cudaMalloc(&w->blow, sizeof(int) * 2 * (size_t)n) == cudaSuccess) {
       plan->cf_k = K;
       plan->cf_smem = sm;
     } else {
@@ -1664,7 +1688,8 @@ int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device) {
 void tc_plan_free(TcPlan* plan) {
   TcWork* w = (TcWork*)plan->work;
   if (!w) return;
-  void* ptrs[] = {w->zbytes, w->bbytes, w->zf, w->bf, w->fb_count, w->fb_list, w->scratch, w->tprod, w->tscratch};
+  void* ptrs[] = {w->zbytes, w->bbytes, w->zf, w->bf, w->fb_count, w->fb_list, w->scratch, w->tprod, w->tscratch,
+                  w->zlow, w->blow};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete w;
@@ -1755,6 +1780,17 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
     for (int c = 0; c < nc; c++)
       k_tcw_pack<<<(unsigned)((npieces + 255) / 256), 256, 0, s>>>(b_limbs + (int64_t)c * L * n, n, L, plan->nks,
                                                                    kstart, ntile, w->bbytes + c * img);
+    a.zlow = w->zlow;
+    a.blow = w->blow;
+    if (nc == 2 && plan->cf_k) {
+      for (int c = 0; c < 2; c++) {
+        k_lowdig<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(z_limbs + (int64_t)c * L * nloc + jl0, nloc, nrows,
+                                                                  L, w->zlow + (size_t)c * nloc);
+        k_lowdig<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(b_limbs + (int64_t)c * L * n, n, n, L,
+                                                              w->blow + (size_t)c * n);
+      }
+      *launches += 4;
+    }
     for (int r0 = 0; r0 < nrows; r0 += plan->w_rows) {
       const int rc = nrows - r0 < plan->w_rows ? nrows - r0 : plan->w_rows;
       TwArgs tw;

@@ -86,3 +86,30 @@ def test_warp_finish_many_blocks_and_row_chunks():
     assert r_w[1] == r_t[1] == n
     assert not first_mismatch(r_t[3], r_w[3], p)
     assert results_digest(r_w[2], r_w[3], n, p, n) == results_digest(r_t[2], r_t[3], n, p, n)
+
+
+@pytest.mark.parametrize("n,p", [(30, 1024), (16, 4096), (12, 333)])
+def test_warp_finish_exact_products(n, p):
+    """Rows of small Gaussian integers (like the power matrix's first row of ones):
+    their short products omit nothing, and the warp finish rounds those sums directly
+    (k_lowdig) instead of sending them to the exact engine -- same bits as the thread
+    finish and the oracle."""
+    rs = mp.random_state(n + p)
+    with mp.context(precision=p):
+        vals = []
+        for i in range(n * n):
+            r, c = divmod(i, n)
+            if r % 3 == 0 or c % 4 == 1:
+                vals.append(mp.mpc(mp.mpfr(int(7 * mp.mpfr_random(rs)) - 3), mp.mpfr(int(5 * mp.mpfr_random(rs)) - 2)))
+            else:
+                vals.append(mp.mpc(2 * mp.mpfr_random(rs) - 1, 2 * mp.mpfr_random(rs) - 1))
+        vals[0] = mp.mpc(1, 0)
+    A = SoA.from_scalars(vals, p, "complex")
+    rc_o, done_o, res_o, fin_o = oracle.eliminate_soa(A, n, p, "complex")
+    rc_w, done_w, res_w, fin_w = device_eliminate(A, n, p, "complex")
+    rc_t, done_t, res_t, fin_t = _thread_finish(A, n, p)
+    assert done_o == done_w == done_t
+    want = results_digest(res_o, fin_o, n, p, done_o)
+    assert not first_mismatch(fin_o, fin_w, p)
+    assert results_digest(res_w, fin_w, n, p, done_w) == want
+    assert results_digest(res_t, fin_t, n, p, done_t) == want
