@@ -20,7 +20,8 @@
 // a gap that makes one product a mere perturbation, sums or alignments wider than
 // the registers, an a - t alignment past the registers) run finish_c_elem on lane
 // 0, unchanged.  DS_CX_FINISH_THREAD=1 selects the thread-per-element kernel
-// (A/B; tests/test_gpu_cfinish.py compares the two bit for bit).
+// (A/B; tests/test_gpu_cfinish.py compares the two bit for bit); below ~1400 bits
+// the thread kernel is the default (cf_k_for).
 
 constexpr uint32_t CF_FULL = 0xffffffffu;
 constexpr int CF_GE = 8;  // elements (warps) per block
@@ -577,10 +578,15 @@ __global__ void __launch_bounds__(256, 3) k_cfw_finish(TcArgs a, TwArgs w, int r
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// words per lane for the finish of W-word products (0: the thread kernel)
-inline int cf_k_for(int W) {
+// words per lane for the finish of W-word products (0: the thread kernel).  Measured
+// (N=1000 @1024, 800 @2000, 600 @3000, 500 @4096, 300 @8192 complex, update time, warp
+// vs thread finish): 2.21 vs 1.26 s, 1.39 vs 1.43, 0.74 vs 1.09, 0.49 vs 0.97, 0.30 vs
+// 0.70 -- so the K = 2 shapes (p up to ~1400 bits) keep the thread kernel unless
+// force_warp (DS_CX_FINISH_WARP=1, tests).
+inline int cf_k_for(int W, bool force_warp) {
   const int need = W + 17;  // >= 16 words of alignment room
-  return need <= 64 ? 2 : need <= 96 ? 3 : need <= 160 ? 5 : need <= 288 ? 9 : 0;
+  if (need <= 64) return force_warp ? 2 : 0;
+  return need <= 96 ? 3 : need <= 160 ? 5 : need <= 288 ? 9 : 0;
 }
 
 inline size_t cf_smem(int K, int W, int L) {

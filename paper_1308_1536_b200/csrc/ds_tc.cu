@@ -1662,7 +1662,8 @@ int tc_plan_init_c(TcPlan* plan, int n, int nloc, int p, int device) {
   if (rc != DS_OK || !plan->wide) return rc;
   // the warp-cooperative finish (ds_cfinish.cuh) unless DS_CX_FINISH_THREAD=1
   const char* ft = getenv("DS_CX_FINISH_THREAD");
-  const int K = (ft && atoi(ft)) ? 0 : cf_k_for(plan->w_W);
+  const char* fw = getenv("DS_CX_FINISH_WARP");
+  const int K = (ft && atoi(ft)) ? 0 : cf_k_for(plan->w_W, fw && atoi(fw));
   if (K) {
     const size_t sm = cf_smem(K, plan->w_W, plan->L);
     cudaError_t e = cudaSuccess;

@@ -40,6 +40,12 @@ def _matrix(n, p, seed, spread_bits, zeros):
     return SoA.from_scalars(vals, p, "complex")
 
 
+@pytest.fixture(autouse=True)
+def _force_warp(monkeypatch):
+    # the warp finish also where the thread kernel is the faster default (K = 2, p <~ 1400)
+    monkeypatch.setenv("DS_CX_FINISH_WARP", "1")
+
+
 def _thread_finish(A, n, p):
     os.environ["DS_CX_FINISH_THREAD"] = "1"
     try:
