@@ -45,7 +45,7 @@ using namespace dss;
 constexpr int TM = 128;      // columns per CTA (TMEM lanes)
 constexpr int KS = 32;       // digits per MMA K step
 // NG epilogue groups of 4 warps (rows ri = grp mod NG) and NG producer
-// pipelines of 2 warps; NG = 2 up to 4096 bits, 1 where two groups' windows do
+// pipelines of 2 warps; NG = 3 up to ~2048 bits, 2 up to 4096 bits, 1 where two groups' windows do
 // not fit in shared memory (8192 bits)
 constexpr int NPIPE = 64;    // producer threads per pipeline
 template <int NG>
@@ -217,10 +217,10 @@ template <int NG>
 __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update_tc(TcArgs a, const __grid_constant__ CUtensorMap amap) {
   constexpr int NEPI = Cfg<NG>::NEPI;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_bank_empty[2];
-  __shared__ __align__(8) uint64_t bar_tfull[2][2];
-  __shared__ __align__(8) uint64_t bar_tempty[2][2];
-  __shared__ __align__(8) uint64_t bar_tile[2];  // a-tile loads (TMA), one per epilogue group
+  __shared__ __align__(8) uint64_t bar_bank_empty[NG];
+  __shared__ __align__(8) uint64_t bar_tfull[NG][2];
+  __shared__ __align__(8) uint64_t bar_tempty[NG][2];
+  __shared__ __align__(8) uint64_t bar_tile[NG];  // a-tile loads (TMA), one per epilogue group
   __shared__ uint32_t tmem_base_sh;
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
       }
       if (tile_io) {  // all 128 results of the row in the window -> one tile store
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_pipe(3 + grp, TM);
+        bar_pipe(1 + NG + grp, TM);
         if (r == 0) tma_store_2d(&amap, tx, 0, region + TM);
       }
     }
@@ -1446,7 +1446,9 @@ static EncodeTiledFn encode_tiled() {
 }
 
 static void launch_update(int ng, dim3 grid, size_t smem, cudaStream_t s, const TcArgs& a, const CUtensorMap& m) {
-  if (ng == 2)
+  if (ng == 3)
+    k_update_tc<3><<<grid, Cfg<3>::NTHREADS, smem, s>>>(a, m);
+  else if (ng == 2)
     k_update_tc<2><<<grid, Cfg<2>::NTHREADS, smem, s>>>(a, m);
   else
     k_update_tc<1><<<grid, Cfg<1>::NTHREADS, smem, s>>>(a, m);
@@ -1606,7 +1608,12 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   size_t smem = 0;
   int ng = 0;
-  for (int g = 2; g >= 1 && !ng; g--) {
+  // three groups (more rows in flight per SM) where TMEM and shared memory allow, i.e.
+  // up to ~2048 bits: measured -4..-8 % device time at N=1000 @768 / 1024 / 2048 and
+  // N=2000 @1024 (profiles/r02_three_groups_ab.log); DS_TC_THREE_GROUPS=0 turns it off
+  const char* e3 = getenv("DS_TC_THREE_GROUPS");
+  const int g0 = (e3 && !atoi(e3)) ? 2 : 3;
+  for (int g = g0; g >= 1 && !ng; g--) {
     if (g == 2 && getenv("DS_TC_ONE_GROUP")) continue;
     int tn = ((512 - 8 * plan->nks) / (2 * g)) & ~31;  // multiple of the 32-column epilogue chunk
     if (tn > 256) tn = 256;
@@ -1623,8 +1630,9 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   }
   if (!ng || getenv("DS_TC_WIDE")) return tcw_plan_init(plan, n, nloc, p, device, maxsm);
   plan->ng = ng;
-  cudaError_t ea = ng == 2 ? cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                           : cudaFuncSetAttribute(k_update_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t ea = ng == 3 ? cudaFuncSetAttribute(k_update_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                   : ng == 2 ? cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(k_update_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (ea != cudaSuccess) return DS_CUDA;
   plan->smem = smem;
   TcWork* w = new TcWork();
