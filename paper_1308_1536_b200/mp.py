@@ -262,6 +262,20 @@ class mpfr:
     def is_zero(self):
         return bool(_f_zero_p(byref(self._s)))
 
+    # values are immutable (as gmpy2's): copies are the object itself; pickling carries
+    # the exact limbs and the precision
+    def __copy__(self):
+        return self
+
+    def __deepcopy__(self, memo):
+        return self
+
+    def __reduce__(self):
+        if not _f_number_p(byref(self._s)):  # NaN / Inf
+            text = "@NaN@" if _f_nan_p(byref(self._s)) else ("-@Inf@" if _f_signbit(byref(self._s)) else "@Inf@")
+            return (_mpfr_from_str, (text, self.precision))
+        return (from_limbs, limbs_of(self) + (self.precision,))
+
     def as_mantissa_exp(self):
         if self.is_zero():
             return mpz(0), mpz(1)
@@ -479,6 +493,15 @@ class mpc:
     def precision(self):
         return (int(self._s.re.prec), int(self._s.im.prec))
 
+    def __copy__(self):
+        return self
+
+    def __deepcopy__(self, memo):
+        return self
+
+    def __reduce__(self):
+        return (mpc_from_parts, (self.real, self.imag))
+
     def _bin(self, other, op, rev=False):
         o = _exact_mpc(other)
         if o is None:
@@ -632,6 +655,10 @@ def limbs_of(x: "mpfr"):
     if 2 * n64 != L:  # drop the low 32 padding bits
         raw = raw[4:]
     return raw, int(x._s.exp), (1 if _f_signbit(byref(x._s)) else 0)
+
+
+def _mpfr_from_str(text: str, prec: int) -> "mpfr":
+    return mpfr(text, prec)
 
 
 def from_limbs(raw: bytes, exp: int, cls: int, prec: int) -> "mpfr":

@@ -163,3 +163,21 @@ def test_counter_uniform_is_exactly_2u_minus_1(p):
         want = Fraction(K - 2 ** (32 * L - 1), 2 ** (32 * L - 1))
         got = s.get(idx, p)
         assert got._fraction() == want, idx
+
+
+def test_scalars_pickle_and_copy():
+    """Result scalars behave like gmpy2's: immutable (copy returns the object) and
+    picklable bit-exactly -- including the pooled ones the boundary conversion makes."""
+    import copy
+    import pickle
+    from paper_1308_1536_b200 import mp
+    from paper_1308_1536_b200.scalars import canonical_bits
+    from paper_1308_1536_b200.synth import random_uniform_soa
+    s = random_uniform_soa(3, 333, seed=1)
+    xs = s.scalars(0, 9, 333)
+    for x in xs + [mp.mpfr(0), -mp.mpfr(0), mp.mpfr(1.5)]:
+        y = pickle.loads(pickle.dumps(x))
+        assert canonical_bits(y) == canonical_bits(x) and y.precision == x.precision
+    c = mp.mpc_from_parts(xs[0], xs[1])
+    assert canonical_bits(pickle.loads(pickle.dumps(c))) == canonical_bits(c)
+    assert copy.copy(xs[0]) is xs[0] and copy.deepcopy([xs[2]])[0] is xs[2]
