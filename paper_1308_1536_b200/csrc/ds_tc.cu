@@ -38,6 +38,10 @@
 #define DS_VAR_MULSHIFT 0
 #endif
 
+#ifndef DS_TCW_FINISH_MINB
+#define DS_TCW_FINISH_MINB 3  // k_tcw_finish blocks per SM the registers are capped for
+#endif
+
 namespace {
 
 using namespace dss;
@@ -1024,7 +1028,7 @@ struct TGen {
 // a's limbs.  Equal exponents with top limbs within one (the order of |a| and
 // |T| unknown before the carry): T materialised and the general add_rn.
 // Undecidable RN(P), or T rounding up to 2^p: the exact fallback list.
-__global__ void __launch_bounds__(256, 3) k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
+__global__ void __launch_bounds__(256, DS_TCW_FINISH_MINB) k_tcw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
                                                     int64_t sthreads) {
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   const int L = a.L, p = a.p, zb = 32 * L - p;
