@@ -109,12 +109,23 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
 }
 // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
 // the phase completes instead of spinning through issue slots
+#ifndef DS_VAR_WAITHINT
+#define DS_VAR_WAITHINT 1000000  // try_wait suspend-time hint (ns); 0: no hint
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#if DS_VAR_WAITHINT
   asm volatile(
       "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(b)),
-      "r"(parity), "r"(1000000));
+      "r"(parity), "r"(DS_VAR_WAITHINT));
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(b)),
+      "r"(parity));
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(b)));
