@@ -1726,9 +1726,11 @@ void tc_plan_free(TcPlan* plan) {
 // {16,12,8,6,4} minimising waves x (rbr + per-CTA setup).  Measured on B200: it
 // lowers the summed update-kernel time (N=1000 @8192: 0.85 -> 0.79 s) but not the
 // elimination (0.88 -> 0.90 s; N=2000 @4096: 2.10 -> 2.17 s): the lookahead tile
-// on its own stream then finds no free SM.  So the default stays 16.
-// DS_TC_RBR=r fixes r.
-static int pick_rbr(int ntiles, int nrows, int ng) {
+// on its own stream then finds no free SM.  So the default stays 16 for one rank;
+// a row-cyclic shard (nloc < n) adapts: rank 0 of 8 at N=2000 @4096, update time
+// 0.427 -> 0.337 s, of 4: 0.649 -> 0.577 s (tools/shard_projection.py,
+// profiles/r02_shard_projection_rbr.json).  DS_TC_RBR=r fixes r.
+static int pick_rbr(int ntiles, int nrows, int ng, bool sharded) {
   static int sms = 0, fixed = -1, adapt_all = 0;
   if (!sms) {
     int dev = 0;
@@ -1741,7 +1743,7 @@ static int pick_rbr(int ntiles, int nrows, int ng) {
   }
   if (fixed > 0) return fixed < RBR ? fixed : RBR;
   (void)ng;
-  if (!adapt_all) return RBR;
+  if (!adapt_all && !sharded) return RBR;
   if (ntiles < 1) ntiles = 1;
   const int cand[5] = {16, 12, 8, 6, 4};
   int best = RBR;
@@ -1879,7 +1881,7 @@ int tc_update_launch(TcPlan* plan, cudaStream_t s, uint32_t* a_limbs, int32_t* a
   a.tma_ok = w->amap_ok;
   a.no_direct = getenv("DS_TC_NO_DIRECT") ? 1 : 0;
   const int ntile = (ncols + TM - 1) / TM;
-  a.rbr = pick_rbr(ntile - (la_col >= 0 && ntile >= 2 ? 1 : 0), nrows, plan->ng);
+  a.rbr = pick_rbr(ntile - (la_col >= 0 && ntile >= 2 ? 1 : 0), nrows, plan->ng, nloc < n);
   const int nrg = (nrows + a.rbr - 1) / a.rbr;
   const int ts = la_col >= 0 ? (la_col - kstart) / TM : -1;  // tile holding the lookahead column
   if (ts >= 0 && ts < ntile && ntile >= 2 && la) {
