@@ -707,18 +707,6 @@ def wrap_pooled(arr, owner, count: int) -> list:
     return out
 
 
-def wrap_structs(arr, count: int) -> list:
-    """mpfr objects over the already-initialised structs of a ctypes array
-    (each keeps the array alive; __del__ clears its own limbs)."""
-    new = object.__new__
-    out = []
-    for k in range(count):
-        o = new(mpfr)
-        o._s = arr[k]
-        out.append(o)
-    return out
-
-
 def mpc_from_parts(re: "mpfr", im: "mpfr") -> "mpc":
     """Exact complex from two reals of the same precision."""
     r = _new_c(re.precision)
