@@ -49,7 +49,7 @@ using namespace dss;
 constexpr int TM = 128;      // columns per CTA (TMEM lanes)
 constexpr int KS = 32;       // digits per MMA K step
 // NG epilogue groups of 4 warps (rows ri = grp mod NG) and NG producer
-// pipelines of 2 warps; NG = 3 up to ~2048 bits, 2 up to 4096 bits, 1 where two groups' windows do
+// pipelines of 2 warps; NG = 4 up to ~2048 bits, 2 up to 4096 bits, 1 where two groups' windows do
 // not fit in shared memory (8192 bits)
 constexpr int NPIPE = 64;    // producer threads per pipeline
 template <int NG>
@@ -1461,7 +1461,9 @@ static EncodeTiledFn encode_tiled() {
 }
 
 static void launch_update(int ng, dim3 grid, size_t smem, cudaStream_t s, const TcArgs& a, const CUtensorMap& m) {
-  if (ng == 3)
+  if (ng == 4)
+    k_update_tc<4><<<grid, Cfg<4>::NTHREADS, smem, s>>>(a, m);
+  else if (ng == 3)
     k_update_tc<3><<<grid, Cfg<3>::NTHREADS, smem, s>>>(a, m);
   else if (ng == 2)
     k_update_tc<2><<<grid, Cfg<2>::NTHREADS, smem, s>>>(a, m);
@@ -1623,11 +1625,13 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   size_t smem = 0;
   int ng = 0;
-  // three groups (more rows in flight per SM) where TMEM and shared memory allow, i.e.
-  // up to ~2048 bits: measured -4..-8 % device time at N=1000 @768 / 1024 / 2048 and
-  // N=2000 @1024 (profiles/r02_three_groups_ab.log); DS_TC_THREE_GROUPS=0 turns it off
-  const char* e3 = getenv("DS_TC_THREE_GROUPS");
-  const int g0 = (e3 && !atoi(e3)) ? 2 : 3;
+  // more epilogue groups (more rows in flight per SM) where TMEM and shared memory
+  // allow, i.e. up to ~2048 bits: three groups measured -4..-8 % device time at N=1000
+  // @768 / 1024 / 2048 and N=2000 @1024 (profiles/r02_three_groups_ab.log), four a
+  // further -10 % update time at 768 / 1024 bits (profiles/r02_four_groups_ab.log).
+  // DS_TC_GROUPS_MAX caps the count (A/B).
+  int g0 = 4;
+  if (const char* e = getenv("DS_TC_GROUPS_MAX")) g0 = atoi(e) >= 1 && atoi(e) <= 4 ? atoi(e) : 4;
   for (int g = g0; g >= 1 && !ng; g--) {
     if (g == 2 && getenv("DS_TC_ONE_GROUP")) continue;
     int tn = ((512 - 8 * plan->nks) / (2 * g)) & ~31;  // multiple of the 32-column epilogue chunk
@@ -1645,7 +1649,8 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   }
   if (!ng || getenv("DS_TC_WIDE")) return tcw_plan_init(plan, n, nloc, p, device, maxsm);
   plan->ng = ng;
-  cudaError_t ea = ng == 3 ? cudaFuncSetAttribute(k_update_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+  cudaError_t ea = ng == 4 ? cudaFuncSetAttribute(k_update_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                   : ng == 3 ? cudaFuncSetAttribute(k_update_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                    : ng == 2 ? cudaFuncSetAttribute(k_update_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                              : cudaFuncSetAttribute(k_update_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (ea != cudaSuccess) return DS_CUDA;
