@@ -1614,10 +1614,12 @@ int tc_plan_init(TcPlan* plan, int n, int nloc, int p, int device) {
   plan->c_lo = clo;
   // TMEM: 2 NG accumulator buffers of tn columns + 8 nks columns of A <= 512;
   // two epilogue groups if their windows fit in shared memory, else one
-  // measured crossover (profiles/r02_smallp_engines.log, N=1000, all minors): the
-  // FP64-digit engine wins at 256 and 512 bits (0.117 vs 0.139 s, 0.134 vs 0.149 s),
-  // the tensor cores from 1024 bits on (0.180 vs 0.246 s); DS_TC_MIN_BITS overrides
-  int min_bits = 768;
+  // measured crossover (N=1000, all minors, device time): with two epilogue groups the
+  // FP64-digit engine won at 256 and 512 bits (profiles/r02_smallp_engines.log); with
+  // four (profiles/r02_engine_crossover_4groups.log) it still wins at 256 bits (0.103 vs
+  // 0.113 s) and the tensor cores win from 512 bits (0.123 vs 0.129 s; 640: 0.155 vs
+  // 0.183 s); DS_TC_MIN_BITS overrides
+  int min_bits = 512;
   if (const char* e = getenv("DS_TC_MIN_BITS")) min_bits = atoi(e);
   if (min_bits < 256) min_bits = 256;
   if (p < min_bits) return DS_OK;  // not applicable: other engines
