@@ -1748,7 +1748,7 @@ static int pick_rbr(int ntiles, int nrows, int ng, bool sharded) {
     fixed = e ? atoi(e) : 0;
     adapt_all = getenv("DS_TC_RBR_ADAPT") ? 1 : 0;
   }
-  if (fixed > 0) return fixed < RBR ? fixed : RBR;
+  if (fixed > 0) return fixed < 64 ? fixed : 64;  // A/B above the default 16 too
   (void)ng;
   if (!adapt_all && !sharded) return RBR;
   if (ntiles < 1) ntiles = 1;
