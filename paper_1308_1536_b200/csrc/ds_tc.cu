@@ -58,7 +58,10 @@ struct Cfg {
   static constexpr int NTHREADS = NEPI + NG * NPIPE;
 };
 constexpr int RBR = 16;      // rows per CTA (the lookahead tile uses RBR_LA)
-constexpr int RBR_LA = 4;
+#ifndef DS_VAR_RBR_LA
+#define DS_VAR_RBR_LA 8  // lookahead-tile rows per CTA: 8 measured -0.8 % update at N=2000 @4096, -1.5 % at N=1000 (profiles/r02_lookahead_rbr_ab.log)
+#endif
+constexpr int RBR_LA = DS_VAR_RBR_LA;
 
 struct TcArgs {
   int p, L, zb, D8p, nks, ntiles, c_lo, eps;
