@@ -58,6 +58,9 @@ struct Cfg {
   static constexpr int NTHREADS = NEPI + NG * NPIPE;
 };
 constexpr int RBR = 16;      // rows per CTA (the lookahead tile uses RBR_LA)
+#ifndef DS_VAR_PREF
+#define DS_VAR_PREF 1  // rows (of the group) ahead that the a-tile L2 prefetch targets
+#endif
 #ifndef DS_VAR_RBR_LA
 #define DS_VAR_RBR_LA 8  // lookahead-tile rows per CTA: 8 measured -0.8 % update at N=2000 @4096, -1.5 % at N=1000 (profiles/r02_lookahead_rbr_ab.log)
 #endif
@@ -446,8 +449,8 @@ __global__ void __launch_bounds__(NG == 2 ? 448 : Cfg<NG>::NTHREADS, 1) k_update
           bulk_wait_read0();  // this group's previous tile store has read the window
           mbar_expect_tx(&bar_tile[grp], (uint32_t)(TM * L * 4));
           tma_load_2d(region + TM, &amap, tx, 0, &bar_tile[grp]);
-          if (ri + NG < nrow_cta)  // the group's next tile into L2 while this row runs
-            tma_prefetch_2d(&amap, (int)((int64_t)(jl + NG) * a.n + kbase), 0);
+          if (ri + DS_VAR_PREF * NG < nrow_cta)  // the group's next tile into L2 while this row runs
+            tma_prefetch_2d(&amap, (int)((int64_t)(jl + DS_VAR_PREF * NG) * a.n + kbase), 0);
         }
       }
       // ---- element setup (mirrors ds_update.cu fused_element)
