@@ -23,6 +23,12 @@
 // (A/B; tests/test_gpu_cfinish.py compares the two bit for bit); below ~1400 bits
 // the thread kernel is the default (cf_k_for).
 
+#ifndef DS_VAR_CF_STAGES
+#define DS_VAR_CF_STAGES 1  // staging stages of k_cfw_finish: 1 measured faster than 2 (power N=1000 -2 %, 300 @8192 update -18 %; profiles/r02_cfinish_stages_ab.log)
+#endif
+#ifndef DS_VAR_CF_MINB
+#define DS_VAR_CF_MINB 3    // k_cfw_finish blocks per SM the registers are capped for
+#endif
 constexpr uint32_t CF_FULL = 0xffffffffu;
 constexpr int CF_GE = 8;  // elements (warps) per block
 
@@ -496,7 +502,7 @@ __device__ __forceinline__ void cf_cp4(uint32_t* sdst, const uint32_t* gsrc) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(256, 3) k_cfw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
+__global__ void __launch_bounds__(256, DS_VAR_CF_MINB) k_cfw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
                                                        int64_t sstride) {
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   extern __shared__ __align__(16) uint32_t cfs[];
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(256, 3) k_cfw_finish(TcArgs a, TwArgs w, int r
   // two stages of [4][CF_GE][Wp] product words + [2][CF_GE][Lp] a limbs, then per warp
   // staging | T_re | T_im
   const int stage_words = 4 * CF_GE * Wp + 2 * CF_GE * Lp;
-  uint32_t* wsb = cfs + 2 * stage_words + warp * (32 * K + 2 * Lp);
+  uint32_t* wsb = cfs + DS_VAR_CF_STAGES * stage_words + warp * (32 * K + 2 * Lp);
   const int64_t total = (int64_t)w.nrows * a.ncols;
   const int64_t region = w.pstride * (int64_t)W;
   const int64_t gstep = (int64_t)gridDim.x * CF_GE;
@@ -540,14 +546,24 @@ __global__ void __launch_bounds__(256, 3) k_cfw_finish(TcArgs a, TwArgs w, int r
     }
   };
   int64_t g0 = (int64_t)blockIdx.x * CF_GE;
+#if DS_VAR_CF_STAGES == 2
   load(g0, 0);
   asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
   for (int it = 0; g0 < total; g0 += gstep, it++) {
+#if DS_VAR_CF_STAGES == 2
     const int st = it & 1;
     __syncthreads();  // every thread is done with stage st ^ 1 (group it - 1's stores)
     if (g0 + gstep < total) load(g0 + gstep, st ^ 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // this group's copies have landed
+#else
+    const int st = 0;
+    __syncthreads();  // every thread is done with the stage (the previous group's stores)
+    load(g0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#endif
     __syncthreads();
     uint32_t* Ts = cfs + st * stage_words;
     uint32_t* As = Ts + 4 * CF_GE * Wp;
@@ -590,6 +606,6 @@ inline int cf_k_for(int W, bool force_warp) {
 }
 
 inline size_t cf_smem(int K, int W, int L) {
-  return sizeof(uint32_t) * (2 * ((size_t)4 * CF_GE * cf_pad(W) + (size_t)2 * CF_GE * cf_pad(L)) +
+  return sizeof(uint32_t) * (DS_VAR_CF_STAGES * ((size_t)4 * CF_GE * cf_pad(W) + (size_t)2 * CF_GE * cf_pad(L)) +
                              (size_t)CF_GE * (32 * K + 2 * cf_pad(L)));
 }
