@@ -27,7 +27,8 @@
 #define DS_VAR_CF_STAGES 1  // staging stages of k_cfw_finish: 1 measured faster than 2 (power N=1000 -2 %, 300 @8192 update -18 %; profiles/r02_cfinish_stages_ab.log)
 #endif
 #ifndef DS_VAR_CF_MINB
-#define DS_VAR_CF_MINB 3    // k_cfw_finish blocks per SM the registers are capped for
+#define DS_VAR_CF_MINB 3    // k_cfw_finish blocks per SM the registers are capped for (K = 9: 2, measured
+                            // -7 % update at 8192 bits; 3 stays best at 4096, profiles/r02_cfinish_stages_ab.log)
 #endif
 constexpr uint32_t CF_FULL = 0xffffffffu;
 constexpr int CF_GE = 8;  // elements (warps) per block
@@ -502,7 +503,7 @@ __device__ __forceinline__ void cf_cp4(uint32_t* sdst, const uint32_t* gsrc) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(256, DS_VAR_CF_MINB) k_cfw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
+__global__ void __launch_bounds__(256, K >= 9 ? 2 : DS_VAR_CF_MINB) k_cfw_finish(TcArgs a, TwArgs w, int row_first, uint32_t* scratch,
                                                        int64_t sstride) {
   if (a.status[0] >= 0 && a.status[0] <= a.step) return;
   extern __shared__ __align__(16) uint32_t cfs[];
